@@ -1,0 +1,330 @@
+"""Pins of the oracle's route functions (O4-O8) and of the paper's printed
+arithmetic: brute force by itertools, an independent Held-Karp, the
+hand-computed 3-aisle example, Theorem 3.1 counts (§3),
+2,903,040 = 9!*8 (§4.6). CPU only."""
+import itertools
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from test_oracle_bf import load_three_aisle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+INF = np.iinfo(np.int32).max
+
+
+def load_paper_values():
+    rec = {}
+    for line in open(os.path.join(GOLD, "paper_values.txt")):
+        line = line.split("#")[0].split()
+        if line:
+            rec.setdefault(line[0], []).append([int(x) for x in line[1:]])
+    return rec
+
+
+def lr_cost(D, seq):
+    """Left-to-right route cost written independently (numpy scalars)."""
+    if len(seq) < 2:
+        return D.dtype.type(0)
+    c = D[seq[0], seq[1]]
+    for a, b in zip(seq[1:-1], seq[2:]):
+        if D.dtype == np.int32:
+            if c == INF or D[a, b] == INF:
+                c = np.int32(INF)
+            else:
+                c = np.int32(int(c) + int(D[a, b]))
+        else:
+            c = np.float32(c + D[a, b])
+    return c
+
+
+def brute(D):
+    n = D.shape[0]
+    best = None
+    for r, p in enumerate(itertools.permutations(range(n))):
+        c = lr_cost(D, p)
+        if best is None or c < best[0]:
+            best = (c, r, p)
+    return best
+
+
+def held_karp(D):
+    """Independent O(n^2 2^n) open-path DP (§3) with the same
+    left-to-right association: best[S][j] = min_i fl(best[S-j][i] + D[i][j])."""
+    n = D.shape[0]
+    fp = D.dtype == np.float32
+    add = (lambda a, b: np.float32(a + b)) if fp else (lambda a, b: a + b)
+    best = {}
+    for j in range(n):
+        best[(1 << j, j)] = D.dtype.type(0) if fp else 0
+    for size in range(2, n + 1):
+        for S in range(1 << n):
+            if bin(S).count("1") != size:
+                continue
+            for j in range(n):
+                if not S >> j & 1:
+                    continue
+                P = S & ~(1 << j)
+                vals = [add(best[(P, i)], D[i, j]) for i in range(n) if P >> i & 1]
+                best[(S, j)] = min(vals)
+    full = (1 << n) - 1
+    return min(best[(full, j)] for j in range(n))
+
+
+def lex_argmin_int(D):
+    """Exact lexicographically smallest optimal open path for int D: suffix DP
+    g[S][j] = cost of best path covering S starting at j, then greedy."""
+    n = D.shape[0]
+    from functools import lru_cache
+
+    @lru_cache(maxsize=None)
+    def g(S, j):
+        rest = S & ~(1 << j)
+        if rest == 0:
+            return 0
+        return min(int(D[j, k]) + g(rest, k) for k in range(n) if rest >> k & 1)
+
+    full = (1 << n) - 1
+    opt = min(g(full, j) for j in range(n))
+    seq, S, cost = [], full, 0
+    j = min(j for j in range(n) if g(full, j) == opt)
+    seq.append(j)
+    while S & ~(1 << j):
+        rest = S & ~(1 << j)
+        k = min(k for k in range(n) if rest >> k & 1 and int(D[j, k]) + g(rest, k) == g(S, j))
+        cost += int(D[j, k])
+        S, j = rest, k
+        seq.append(j)
+    return opt, seq
+
+
+def random_D(rng, n, kind, symmetric=False):
+    if kind == "int":
+        D = rng.integers(0, 30, (n, n)).astype(np.int32)
+    else:
+        D = rng.uniform(0, 10, (n, n)).astype(np.float32)
+        D[rng.random((n, n)) < 0.1] = np.float32(0.1)  # force some fp32 ties/absorption
+    if symmetric:
+        D = np.triu(D) + np.triu(D, 1).T
+    np.fill_diagonal(D, 0)
+    return D
+
+
+# ---------------------------------------------------------------- O4
+def test_route_cost_hand_sums():
+    rec = load_three_aisle()
+    D = rec["D"]
+    assert oracle.route_cost(D, [0, 2, 1, 3, 4]) == 6 + 2 + 6 + 3
+    assert oracle.route_cost(D, [4]) == 0
+    D2 = D.copy()
+    D2[1, 3] = INF
+    assert oracle.route_cost(D2, [0, 1, 3]) == INF
+
+
+def test_route_cost_left_to_right_fp32():
+    # legs (0.2, 1.1, 0.2, 3.7): forward 5.2000003 vs reversed 5.1999998
+    D = np.zeros((5, 5), dtype=np.float32)
+    legs = [0.2, 1.1, 0.2, 3.7]
+    for i, x in enumerate(legs):
+        D[i, i + 1] = np.float32(x)
+        D[i + 1, i] = np.float32(x)
+    fwd = oracle.route_cost(D, [0, 1, 2, 3, 4])
+    rev = oracle.route_cost(D, [4, 3, 2, 1, 0])
+    assert fwd == np.float32(np.float32(np.float32(np.float32(0.2) + np.float32(1.1)) + np.float32(0.2)) + np.float32(3.7))
+    assert fwd != rev
+    assert float(fwd) == pytest.approx(5.2000003, abs=1e-7)
+    assert float(rev) == pytest.approx(5.1999998, abs=1e-7)
+
+
+# ---------------------------------------------------------------- O5
+def test_exact_three_aisle_and_histogram():
+    rec = load_three_aisle()
+    D = rec["D"]
+    cost, rank, seq = oracle.exact_route(D)
+    exp_cost, exp_seq, exp_rank, n_opt, max_cost = rec["exact"]
+    assert (cost, rank, seq.tolist()) == (exp_cost, exp_rank, exp_seq)
+    costs = [lr_cost(D, p) for p in itertools.permutations(range(5))]
+    assert costs.count(exp_cost) == n_opt and max(costs) == max_cost
+    # every rank range returns the exact minimum of that range
+    for lo, hi in [(0, 1), (0, 7), (5, 64), (64, 120)]:
+        c, r, s = oracle.exact_route_range(D, lo, hi)
+        sub = costs[lo:hi]
+        assert c == min(sub) and r == lo + sub.index(min(sub))
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_exact_equals_brute_force(kind):
+    rng = np.random.default_rng(31 if kind == "int" else 32)
+    for trial in range(60):
+        n = int(rng.integers(1, 7))
+        D = random_D(rng, n, kind)
+        cost, rank, seq = oracle.exact_route(D)
+        bc, br, bp = brute(D)
+        assert cost.tobytes() == np.asarray(bc, dtype=D.dtype).tobytes()
+        assert rank == br and seq.tolist() == list(bp)
+        assert oracle.perm_rank(seq) == rank
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_exact_equals_held_karp(kind):
+    rng = np.random.default_rng(41 if kind == "int" else 42)
+    for trial in range(40 if kind == "int" else 30):
+        n = int(rng.integers(2, 8))
+        D = random_D(rng, n, kind)
+        cost, rank, seq = oracle.exact_route(D)
+        assert np.asarray(cost, D.dtype).tobytes() == np.asarray(held_karp(D), D.dtype).tobytes()
+        if kind == "int":
+            opt, lseq = lex_argmin_int(D)
+            assert cost == opt and seq.tolist() == lseq
+
+
+def test_reversal_invariance_int_symmetric():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        n = int(rng.integers(2, 8))
+        D = random_D(rng, n, "int", symmetric=True)
+        p = rng.permutation(n)
+        assert oracle.route_cost(D, p) == oracle.route_cost(D, p[::-1])
+        cost, rank, seq = oracle.exact_route(D)
+        assert seq[0] < seq[-1] or n == 1  # lexicographic argmin has first < last
+
+
+# ---------------------------------------------------------------- O6
+def test_chunked_equals_unchunked():
+    rng = np.random.default_rng(51)
+    for trial in range(30):
+        n = int(rng.integers(2, 8))
+        kind = "int" if trial % 2 else "fp32"
+        D = random_D(rng, n, kind)
+        c0, r0, s0 = oracle.exact_route(D)
+        chunk = int(rng.integers(1, math.factorial(n) + 2))
+        c1, r1, s1, nch = oracle.exact_route_chunked(D, chunk)
+        assert (np.asarray(c0).tobytes(), r0, s0.tolist()) == (np.asarray(c1).tobytes(), r1, s1.tolist())
+        assert nch == -(-math.factorial(n) // chunk)
+
+
+def test_paper_capacity_arithmetic():
+    pv = load_paper_values()
+    cap = pv["capacity"][0][0]
+    assert cap == math.factorial(9) * 8  # P658: 2,903,040 = 9! * (9-1)
+    assert math.factorial(9) * 8 <= cap < math.factorial(10) * 9
+    for n, nch in pv["chunks"]:
+        assert -(-math.factorial(n) // cap) == nch
+    # SPEC S445: plan_segmentation(10, 4) -> (0,4),(4,4),(8,2)
+    assert [(lo, min(4, 10 - lo)) for lo in range(0, 10, 4)] == [(0, 4), (4, 4), (8, 2)]
+
+
+def test_chunk_count_on_real_chunked_search():
+    rng = np.random.default_rng(3)
+    D = random_D(rng, 7, "int")
+    c, r, s, nch = oracle.exact_route_chunked(D, 1000)
+    assert nch == 6  # ceil(5040 / 1000)
+
+
+# ---------------------------------------------------------------- O7
+def test_segmented_three_aisle():
+    rec = load_three_aisle()
+    D = rec["D"]
+    for labels, cost, seq in rec["segmented"]:
+        c, s, counts = oracle.segmented_route(D, labels)
+        assert (int(c), s.tolist()) == (cost, seq), labels
+    c, s, counts = oracle.segmented_route(D, [0] * 5)
+    assert (c, s.tolist(), counts) == (17, [0, 2, 1, 3, 4], (120, 2))
+    c, s, counts = oracle.segmented_route(D, [0, 1, 2, 3, 4])
+    assert (c, s.tolist(), counts) == (17, [0, 2, 1, 3, 4], (5, 3840))
+
+
+def test_theorem_3_1_counts_paper():
+    pv = load_paper_values()
+    for row in pv["thm31"]:
+        expect, parts = row[0], row[1:]
+        red, brute_count = oracle.route_count_reduction(parts)
+        assert red == expect
+        assert brute_count == math.factorial(sum(parts)) // 2
+        # the oracle's directed stitch enumerates exactly twice that many
+        m = len(parts)
+        if sum(parts) <= 12:
+            D = np.zeros((sum(parts), sum(parts)), dtype=np.int32)
+            labels = np.repeat(np.arange(m), parts)
+            _, _, counts = oracle.segmented_route(D, labels)
+            assert counts[0] + counts[1] == 2 * expect
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_segmented_invariants(kind):
+    rng = np.random.default_rng(61 if kind == "int" else 62)
+    for trial in range(40):
+        n = int(rng.integers(1, 8))
+        D = random_D(rng, n, kind)
+        ec, er, es = oracle.exact_route(D)
+        c1, s1, _ = oracle.segmented_route(D, np.zeros(n, dtype=np.int32))
+        assert np.asarray(c1).tobytes() == np.asarray(ec).tobytes() and s1.tolist() == es.tolist()
+        cs, ss, _ = oracle.segmented_route(D, np.arange(n))
+        assert np.asarray(cs).tobytes() == np.asarray(ec).tobytes() and ss.tolist() == es.tolist()
+        labels = rng.integers(0, 3, n)
+        c, s, _ = oracle.segmented_route(D, labels)
+        assert c >= ec
+        assert sorted(s.tolist()) == list(range(n))
+        assert np.asarray(oracle.route_cost(D, s)).tobytes() == np.asarray(c).tobytes()
+
+
+# ---------------------------------------------------------------- O8
+def test_kmeans_separated_clusters():
+    xy = np.array([[0, 0], [100, 100], [1, 0], [0, 1], [200, 0], [101, 99], [201, 1]])
+    # farthest-point init: c0 = point 0; the farthest from it is (201,1)
+    # (40402 > 40000 > 20000) -> cluster 1; then (100,100) -> cluster 2
+    assert oracle.kmeans(xy, 3).tolist() == [0, 2, 0, 0, 1, 2, 1]
+    assert oracle.kmeans(xy, 1).tolist() == [0] * 7
+    assert oracle.kmeans(xy[:2], 3).tolist() == [0, 1]
+
+
+def test_kmeans_is_lloyd_fixpoint():
+    """Independent check with exact rationals: on convergence every point sits
+    at a nearest centroid of the final partition (ties -> lower index)."""
+    rng = np.random.default_rng(71)
+    for trial in range(100):
+        n = int(rng.integers(1, 13))
+        K = int(rng.integers(1, 4))
+        xy = rng.integers(0, 40, (n, 2))
+        lab = oracle.kmeans(xy, K)
+        Kc = min(K, n)
+        assert lab.min() >= 0 and lab.max() < Kc
+        cents = {}
+        for k in range(Kc):
+            pts = xy[lab == k]
+            if len(pts):
+                cents[k] = (Fraction(int(pts[:, 0].sum()), len(pts)), Fraction(int(pts[:, 1].sum()), len(pts)))
+        for p in range(n):
+            d = {k: (xy[p, 0] - c[0]) ** 2 + (xy[p, 1] - c[1]) ** 2 for k, c in cents.items()}
+            best = min(d.values())
+            # the point's own cluster is at minimal distance, and no nonempty
+            # lower-index cluster ties with it (a fixpoint of the tie rule)
+            assert d[lab[p]] == best
+            assert all(not (k < lab[p] and d[k] == best) for k in d)
+
+
+def test_order_stops_vs_numpy():
+    rng = np.random.default_rng(81)
+    for _ in range(50):
+        nodes = rng.integers(0, 20, int(rng.integers(1, 15)))
+        assert oracle.order_stops(nodes).tolist() == np.unique(nodes).tolist()
+
+
+# ------------------------------------------------------- composed pipeline
+def test_route_orders_composition_c2():
+    g, orders, meta = gen.config(2)
+    res = oracle.route_orders(g, orders, m=1)
+    assert res["rc"] == 0
+    for o in range(0, orders.B, 37):
+        nodes = orders.order_nodes[orders.order_ptr[o]:orders.order_ptr[o + 1]]
+        stops = np.unique(nodes)
+        rows = oracle.bf_many(g, stops)
+        D = rows[:, stops]
+        c, r, s = oracle.exact_route(D)
+        assert res["cost"][o] == c and res["rank"][o] == r
+        assert res["seq"][o, :len(stops)].tolist() == stops[s].tolist()
