@@ -1,0 +1,190 @@
+// wr_internal.cuh - shared internals of libwr (not part of the ABI).
+// Everything here is the CUDA path; it shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/wr.h"
+
+namespace wr {
+
+// ------------------------------------------------------------------ errors --
+void set_error(const std::string &msg);
+wr_status fail(wr_status code, const std::string &msg);
+
+struct CudaError {
+    wr_status code;
+};
+
+#define WR_CUDA(call)                                                            \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            ::wr::set_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+            throw ::wr::CudaError{e_ == cudaErrorMemoryAllocation ? WR_ENOMEM : WR_ECUDA}; \
+        }                                                                        \
+    } while (0)
+
+#define WR_LAUNCH_CHECK() WR_CUDA(cudaGetLastError())
+
+struct Status {
+    wr_status code;
+    std::string msg;
+};
+#define WR_THROW(code, msg) throw ::wr::Status{(code), (msg)}
+
+// Runs f() translating exceptions into wr_status + wr_last_error().
+template <class F>
+wr_status guarded(F &&f) {
+    try {
+        return f();
+    } catch (const CudaError &e) {
+        return e.code;
+    } catch (const Status &s) {
+        return fail(s.code, s.msg);
+    } catch (const std::bad_alloc &) {
+        return fail(WR_ENOMEM, "host allocation failed");
+    } catch (...) {
+        return fail(WR_EINTERNAL, "unexpected exception");
+    }
+}
+
+// Counts libwr kernel launches (reported in stats and by the bench).
+extern thread_local int64_t g_launches;
+inline void count_launch() { ++g_launches; }
+
+// --------------------------------------------------------- device memory --
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) return;
+        WR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// True if ptr is device (or managed) memory usable by kernels.
+bool is_device_ptr(const void *ptr);
+
+// Copies a caller array (host or device) into a fresh device buffer.
+template <class T>
+DBuf<T> to_device(const T *src, size_t count, cudaStream_t st) {
+    DBuf<T> d(count);
+    if (count) WR_CUDA(cudaMemcpyAsync(d.p, src, count * sizeof(T), cudaMemcpyDefault, st));
+    return d;
+}
+
+// ------------------------------------------------------------ the graph --
+struct DevGraph {           // kernel view (POD)
+    int V;
+    int E;
+    const int *in_ptr;      // [V+1] CSC offsets (in-arcs of v)
+    const int *in_src;      // [E]   tail u of each in-arc, sorted by (v, u)
+    const uint32_t *in_w;   // [E]   weight bits
+    const int *out_ptr;     // [V+1] CSR offsets (out-arcs of u)
+    const int *out_dst;     // [E]   head of each out-arc
+};
+
+}  // namespace wr
+
+struct wr_graph {
+    int device = 0;
+    int V = 0;
+    int64_t E = 0;
+    int wtype = WR_I32;
+    int has_negative = 0;
+    int32_t max_abs_w = 0;
+    wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
+    wr::DBuf<uint32_t> in_w;
+    wr::DBuf<int> xy;       // [V*2] or empty
+    wr::DevGraph view() const {
+        return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, out_ptr.p, out_dst.p};
+    }
+};
+
+namespace wr {
+
+// --------------------------------------------------------- scan helpers --
+// Exclusive prefix sum of n int64 values (device in/out may alias).
+void scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, cudaStream_t st);
+void scan_exclusive_i32(const int *in, int *out, int n, cudaStream_t st);
+
+// -------------------------------------------------------- Bellman-Ford --
+// Segment scheduler (a8): sources per BF batch for a per-source byte cost.
+int64_t budget_bytes(int64_t requested);
+int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes,
+                            int64_t S);
+
+struct BfRun {              // one BF segment over tiles of 32 sources
+    const int *tile_src;    // [ntiles*32] source vertex per lane, -1 = empty
+    int ntiles;
+    uint32_t *rows;         // [ntiles][V][32] working distances (output)
+    int variant;
+    int max_rounds;
+};
+
+struct BfTileStats {        // per-call accumulators (device)
+    unsigned long long relax;
+    int rounds_max;
+    int negcycle_tile;      // -1 or a tile with a negative cycle
+};
+
+// Launches the relaxation sweep of a segment on stream st (a3).
+void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st);
+
+// Canonical pred (a4) + output of dist/pred rows of a segment in S x T /
+// S x V row-major caller layout, row index = out_row0 + tile*32 + lane.
+void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t S_total,
+                      const int *targets, int T, void *dist_out, int32_t *pred_out,
+                      int *d_flat_tiles, cudaStream_t st);
+// Resolves "flat" predecessors of the listed tiles with a tight-arc BFS.
+void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles,
+                     int64_t out_row0, int32_t *pred_out, cudaStream_t st);
+
+// Builds tile_src for sources [lo, hi) of a device source list.
+void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int *d_tile_src, cudaStream_t st);
+
+// ------------------------------------------------------------- routing --
+struct RouteProblem {       // one exhaustive search (an order or a segment)
+    int order;              // index into the D array
+    int n;                  // stops in this problem (<= WR_MAX_EXACT)
+    uint64_t map;           // 4-bit local -> order-stop index, position k at bits 4k
+    int item0;              // first work item
+    int nitems;
+};
+
+struct RouteWorkItem {
+    int problem;
+    int prefix_lo;          // first prefix (lexicographic) of this chunk
+    int prefix_hi;
+};
+
+// Prefix depth p(n) used to split n! into subtrees of (n-p)! leaves.
+int route_prefix_depth(int n);
+int64_t factorial64(int n);
+
+}  // namespace wr

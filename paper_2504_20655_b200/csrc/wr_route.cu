@@ -1,0 +1,1146 @@
+// wr_route.cu - route evaluation over pick-node sequences (a5-a7), the
+// Theorem 3.1 segmented route, the O8 segment plan, and the orders
+// pipeline (a2..a9 phases) behind wr_route_orders.
+//
+// Paper: exhaustive evaluation of all n! orderings, one thread per
+// permutation with an (n-1)-transition inner loop (P658 §4.6), memory errors
+// above N = 2,903,040 permutations; clusters stitched through two boundary
+// nodes each (Thm 3.1, P324-337 §3).
+// Here: the n! sequences of a (sub)problem are the leaves of the permutation
+// prefix trie (reading A18); a lane owns a lexicographic prefix and walks its
+// subtree depth-first, so every internal trie node costs ONE add shared by
+// all leaves below it (~e adds per leaf instead of n-1) and the left-to-right
+// association of O4 is kept exactly. Work items are rank ranges of at most
+// opts.chunk permutations (O6); per-lane minima are packed (cost key << 32 |
+// rank) and reduced with integer min: ties resolve to the smallest rank =
+// lexicographically smallest sequence (O5). Nothing is materialised per
+// permutation, so the paper's memory limit disappears; the chunk only bounds
+// the work of one warp.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "wr_internal.cuh"
+
+namespace wr {
+
+constexpr int MS = WR_MAX_STOPS;      // 16
+constexpr int DSTRIDE = MS * MS;      // D entries per order (row-major 16 x 16)
+constexpr int TS = 32;
+
+// ------------------------------------------------------------ cost ops --
+// Route costs: int32 exact (with negatives possible when D < 0), fp32 RN.
+// key(): order-preserving map to uint32 (fp32 costs are >= 0 or +inf).
+struct CostI32 {
+    static constexpr uint32_t INF = 0x7fffffffu;
+    __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) { return (uint32_t)((int)a + (int)b); }
+    __device__ __forceinline__ static uint32_t key(uint32_t c) { return c ^ 0x80000000u; }
+    __device__ __forceinline__ static uint32_t unkey(uint32_t k) { return k ^ 0x80000000u; }
+};
+struct CostF32 {
+    static constexpr uint32_t INF = 0x7f800000u;
+    __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
+        return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(b)));
+    }
+    __device__ __forceinline__ static uint32_t key(uint32_t c) { return c; }
+    __device__ __forceinline__ static uint32_t unkey(uint32_t k) { return k; }
+};
+
+__host__ __device__ inline int64_t fact(int n) {
+    int64_t f = 1;
+    for (int k = 2; k <= n; ++k) f *= k;
+    return f;
+}
+
+// p(n): prefix depth; subtrees of (n-p)! leaves, >= 200 prefixes when possible.
+__host__ __device__ inline int prefix_depth(int n) {
+    if (n <= 1) return 0;
+    int p = n - 7 > 1 ? n - 7 : 1;
+    while (p < n - 1 && fact(n) / fact(n - p) < 200) ++p;
+    return p;
+}
+int route_prefix_depth(int n) { return prefix_depth(n); }
+
+// Lehmer decode of rank r over n elements into nibble-packed positions.
+__device__ inline uint64_t unrank_nib(int64_t r, int n) {
+    uint32_t unused = (1u << n) - 1u;
+    uint64_t out = 0;
+    for (int k = 0; k < n; ++k) {
+        const int64_t f = fact(n - 1 - k);
+        int q = (int)(r / f);
+        r %= f;
+        uint32_t m = unused;
+        for (int t = 0; t < q; ++t) m &= m - 1;
+        const int x = __ffs(m) - 1;
+        unused &= ~(1u << x);
+        out |= (uint64_t)x << (4 * k);
+    }
+    return out;
+}
+
+__device__ inline int nib(uint64_t v, int k) { return (int)((v >> (4 * k)) & 0xf); }
+
+// ---------------------------------------------------------- trie walk --
+template <class C, int L>
+struct Dfs {
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+                                               uint64_t &best, uint32_t &rank) {
+        uint32_t rem = unused;
+        while (rem) {
+            const int x = __ffs(rem) - 1;
+            rem &= rem - 1;
+            Dfs<C, L - 1>::run(Ds, n, unused & ~(1u << x), x, C::add(cost, Ds[prev * n + x]), best, rank);
+        }
+    }
+};
+template <class C>
+struct Dfs<C, 0> {
+    __device__ __forceinline__ static void run(const uint32_t *, int, uint32_t, int, uint32_t cost, uint64_t &best,
+                                               uint32_t &rank) {
+        const uint64_t k = ((uint64_t)C::key(cost) << 32) | rank;
+        best = k < best ? k : best;
+        ++rank;
+    }
+};
+
+template <class C>
+__device__ void walk_subtree(int L, const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+                             uint64_t &best, uint32_t &rank) {
+    switch (L) {
+        case 0: Dfs<C, 0>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 1: Dfs<C, 1>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 2: Dfs<C, 2>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 3: Dfs<C, 3>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 4: Dfs<C, 4>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 5: Dfs<C, 5>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 6: Dfs<C, 6>::run(Ds, n, unused, prev, cost, best, rank); break;
+        default: Dfs<C, 7>::run(Ds, n, unused, prev, cost, best, rank); break;
+    }
+}
+
+// One warp per work item (problem, prefix range). D submatrix staged in smem.
+constexpr int ENUM_WARPS = 8;
+template <class C>
+__global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const RouteProblem *__restrict__ probs,
+                                                                     const RouteWorkItem *__restrict__ items,
+                                                                     int nitems, const uint32_t *__restrict__ Dall,
+                                                                     uint64_t *item_best) {
+    __shared__ uint32_t sD[ENUM_WARPS][WR_MAX_EXACT * WR_MAX_EXACT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int it = blockIdx.x * ENUM_WARPS + warp;
+    if (it >= nitems) return;
+    const RouteWorkItem item = items[it];
+    const RouteProblem pr = probs[item.problem];
+    const int n = pr.n;
+    const uint32_t *D = Dall + (size_t)pr.order * DSTRIDE;
+    uint32_t *Ds = sD[warp];
+    for (int e = lane; e < n * n; e += 32) {
+        const int a = e / n, b = e % n;
+        Ds[e] = D[nib(pr.map, a) * MS + nib(pr.map, b)];
+    }
+    __syncwarp();
+    const int p = prefix_depth(n);
+    const int L = n - p;
+    const uint32_t sub = (uint32_t)fact(L);
+    uint64_t best = ~0ull;
+    for (int q = item.prefix_lo + lane; q < item.prefix_hi; q += 32) {
+        // decode prefix q (mixed radix n, n-1, ..., n-p+1), lexicographic
+        uint32_t unused = (1u << n) - 1u;
+        int rem = q, prev = -1;
+        uint32_t cost = 0;
+        int64_t div = fact(n - 1) / fact(L);   // prefixes per first-element choice
+        for (int k = 0; k < p; ++k) {
+            const int digit = (int)(rem / div);
+            rem = (int)(rem % div);
+            if (k + 1 < p) div /= (n - 1 - k);
+            uint32_t m = unused;
+            for (int t = 0; t < digit; ++t) m &= m - 1;
+            const int x = __ffs(m) - 1;
+            unused &= ~(1u << x);
+            if (prev >= 0) cost = C::add(cost, Ds[prev * n + x]);
+            prev = x;
+        }
+        uint32_t rank = (uint32_t)q * sub;
+        walk_subtree<C>(L, Ds, n, unused, prev, cost, best, rank);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y < best ? y : best;
+    }
+    if (lane == 0) item_best[it] = best;
+}
+
+__global__ void problem_reduce_kernel(const RouteProblem *probs, int nprob, const uint64_t *item_best,
+                                      uint64_t *prob_best) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nprob) return;
+    uint64_t b = ~0ull;
+    for (int k = probs[i].item0; k < probs[i].item0 + probs[i].nitems; ++k) b = item_best[k] < b ? item_best[k] : b;
+    prob_best[i] = b;
+}
+
+// ------------------------------------------------- O8 segment plan (K-means) --
+// Exact integer K-means with the tie rules of O8 (reading A12). With
+// |coord| < 2^20 and n <= 16, (cnt*x - Sx)^2 * cnt'^2 < 2^63: int64 is exact.
+__device__ inline int64_t sqd_scaled(int64_t x, int64_t y, int64_t sx, int64_t sy, int64_t cnt) {
+    const int64_t dx = cnt * x - sx, dy = cnt * y - sy;
+    return dx * dx + dy * dy;
+}
+
+__device__ void kmeans_dev(const int *xy, int n, int K, int *labels) {
+    if (K > n) K = n;
+    int centre[MS];
+    centre[0] = 0;
+    for (int k = 1; k < K; ++k) {
+        int64_t best = -1;
+        int arg = 0;
+        for (int p = 0; p < n; ++p) {
+            int64_t mind = -1;
+            for (int q = 0; q < k; ++q) {
+                const int64_t dx = (int64_t)xy[2 * p] - xy[2 * centre[q]];
+                const int64_t dy = (int64_t)xy[2 * p + 1] - xy[2 * centre[q] + 1];
+                const int64_t d = dx * dx + dy * dy;
+                if (mind < 0 || d < mind) mind = d;
+            }
+            if (mind > best) {
+                best = mind;
+                arg = p;
+            }
+        }
+        centre[k] = arg;
+    }
+    int64_t sx[MS], sy[MS], cnt[MS];
+    for (int k = 0; k < K; ++k) {
+        sx[k] = xy[2 * centre[k]];
+        sy[k] = xy[2 * centre[k] + 1];
+        cnt[k] = 1;
+    }
+    int prev[MS];
+    bool have_prev = false;
+    for (int it = 0; it < 100; ++it) {
+        for (int p = 0; p < n; ++p) {
+            int arg = 0;
+            for (int k = 1; k < K; ++k) {
+                const int64_t lhs = sqd_scaled(xy[2 * p], xy[2 * p + 1], sx[k], sy[k], cnt[k]) * (cnt[arg] * cnt[arg]);
+                const int64_t rhs = sqd_scaled(xy[2 * p], xy[2 * p + 1], sx[arg], sy[arg], cnt[arg]) * (cnt[k] * cnt[k]);
+                if (lhs < rhs) arg = k;
+            }
+            labels[p] = arg;
+        }
+        bool same = have_prev;
+        for (int p = 0; p < n && same; ++p) same = prev[p] == labels[p];
+        if (same) break;
+        for (int p = 0; p < n; ++p) prev[p] = labels[p];
+        have_prev = true;
+        for (int k = 0; k < K; ++k) {
+            int64_t nx = 0, ny = 0, c = 0;
+            for (int p = 0; p < n; ++p)
+                if (labels[p] == k) {
+                    nx += xy[2 * p];
+                    ny += xy[2 * p + 1];
+                    ++c;
+                }
+            if (c > 0) {
+                sx[k] = nx;
+                sy[k] = ny;
+                cnt[k] = c;
+            }
+        }
+    }
+}
+
+__global__ void segment_plan_kernel(const int *xy, int n, int m, int *labels) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) kmeans_dev(xy, n, m, labels);
+}
+
+// --------------------------------------------------- a2 stop projection --
+// Per order: distinct location nodes sorted ascending (P226-238 §2.4);
+// status ETOOLARGE if more than 16 distinct stops. Marks source vertices.
+__global__ void order_stops_kernel(const int64_t *order_ptr, const int *nodes, int64_t B, int V, int *stops,
+                                   int *n_out, int *status, int *is_src, int *bad) {
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= B) return;
+    int s[MS];
+    int n = 0;
+    int st = WR_OK;
+    for (int64_t a = order_ptr[o]; a < order_ptr[o + 1]; ++a) {
+        const int x = nodes[a];
+        if (x < 0 || x >= V) {
+            atomicOr(bad, 1);
+            st = WR_EINVAL;
+            break;
+        }
+        int pos = n;
+        bool dup = false;
+        for (int b = 0; b < n; ++b) {
+            if (s[b] == x) { dup = true; break; }
+        }
+        if (dup) continue;
+        if (n == MS) { st = WR_ETOOLARGE; break; }
+        while (pos > 0 && s[pos - 1] > x) { s[pos] = s[pos - 1]; --pos; }
+        s[pos] = x;
+        ++n;
+    }
+    for (int k = 0; k < MS; ++k) stops[o * MS + k] = k < n ? s[k] : -1;
+    n_out[o] = n;
+    status[o] = st;
+    if (st == WR_OK)
+        for (int k = 0; k < n; ++k) is_src[s[k]] = 1;
+}
+
+__global__ void sources_scatter_kernel(const int *is_src, const int *src_row, int V, int *sources) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < V && is_src[v]) sources[src_row[v]] = v;
+}
+
+__global__ void src_row_fix_kernel(const int *is_src, int *src_row, int V) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < V && !is_src[v]) src_row[v] = -1;
+}
+
+// Ownership (a9): stops of order o owned by rank q form the contiguous index
+// range [i_lo, i_hi) because stops are ascending and src_row is monotone.
+__device__ inline void owned_range(const int *stops, int n, const int *src_row, int64_t lo, int64_t hi,
+                                   int &i_lo, int &i_hi) {
+    i_lo = 0;
+    while (i_lo < n && src_row[stops[i_lo]] < lo) ++i_lo;
+    i_hi = i_lo;
+    while (i_hi < n && src_row[stops[i_hi]] < hi) ++i_hi;
+}
+
+__global__ void owned_count_kernel(const int *stops, const int *n_arr, const int *status, int64_t B,
+                                   const int *src_row, const int64_t *blk, int world, int64_t *cnt) {
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= B) return;
+    const int n = status[o] == WR_OK ? n_arr[o] : 0;
+    for (int q = 0; q < world; ++q) {
+        int a, b;
+        owned_range(stops + o * MS, n, src_row, blk[q], blk[q + 1], a, b);
+        cnt[(int64_t)q * (B + 1) + o] = (int64_t)(b - a) * n;
+    }
+}
+
+// a5 D gather: send[off[o] + (i - i_lo) * n + j] = dist(stop_i -> stop_j) for
+// the stops i whose source row lies in this BF segment [seg_lo, seg_hi).
+__global__ void gather_send_kernel(const int *stops, const int *n_arr, const int *status, int64_t B,
+                                   const int *src_row, int64_t own_lo, int64_t own_hi, int64_t seg_lo,
+                                   int64_t seg_hi, const int64_t *off, const uint32_t *rows, int V,
+                                   uint32_t *send) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= B * MS) return;
+    const int64_t o = t / MS;
+    const int i = (int)(t % MS);
+    if (status[o] != WR_OK) return;
+    const int n = n_arr[o];
+    if (i >= n) return;
+    const int *s = stops + o * MS;
+    const int64_t r = src_row[s[i]];
+    if (r < seg_lo || r >= seg_hi) return;
+    int i_lo, i_hi;
+    owned_range(s, n, src_row, own_lo, own_hi, i_lo, i_hi);
+    const int64_t rr = r - seg_lo;
+    const uint32_t *R = rows + (size_t)(rr / TS) * V * TS + (rr % TS);
+    uint32_t *dst = send + off[o] + (int64_t)(i - i_lo) * n;
+    for (int j = 0; j < n; ++j) dst[j] = R[(size_t)s[j] * TS];
+}
+
+// Reassemble D[o][i][j] (16 x 16 stride) for orders [o_lo, o_hi) from the
+// all-gathered send buffers (rank-major, max_send elements each).
+__global__ void assemble_kernel(const int *stops, const int *n_arr, const int *status, int64_t B, int64_t o_lo,
+                                int64_t o_hi, const int *src_row, const int64_t *blk, int world,
+                                const int64_t *off_all, const uint32_t *gathered, int64_t max_send,
+                                uint32_t *Dall) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (o_hi - o_lo) * MS) return;
+    const int64_t o = o_lo + t / MS;
+    const int i = (int)(t % MS);
+    uint32_t *D = Dall + (size_t)(o - o_lo) * DSTRIDE + i * MS;
+    if (status[o] != WR_OK) return;
+    const int n = n_arr[o];
+    if (i >= n) return;
+    const int *s = stops + o * MS;
+    const int64_t r = src_row[s[i]];
+    int q = 0;
+    while (q + 1 < world && r >= blk[q + 1]) ++q;
+    int i_lo, i_hi;
+    owned_range(s, n, src_row, blk[q], blk[q + 1], i_lo, i_hi);
+    const uint32_t *src = gathered + (int64_t)q * max_send + off_all[(int64_t)q * (B + 1) + o] + (int64_t)(i - i_lo) * n;
+    for (int j = 0; j < n; ++j) D[j] = src[j];
+}
+
+// ------------------------------------------------ route preparation --
+struct OrderRoute {        // per-order routing state (device)
+    int n;
+    int status;
+    int mseg;              // segments m' (1 = exact)
+    int prob0;             // first problem index
+    int nprob;
+    uint64_t segmap[WR_MAX_SEGMENTS];  // nibble map of each segment's stops
+    int seglen[WR_MAX_SEGMENTS];
+};
+
+template <class C>
+__device__ inline bool is_inf(uint32_t x) { return x == C::INF; }
+
+// Pass 1: status, segments, problem/item counts.
+template <class C>
+__global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
+                                     int64_t nord, const uint32_t *Dall, int m, const int *xy,
+                                     const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
+                                     int *item_cnt) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nord) return;
+    const int64_t o = o_lo + t;
+    OrderRoute R;
+    R.n = n_arr[o];
+    R.status = status_in[o];
+    R.mseg = 1;
+    R.prob0 = 0;
+    R.nprob = 0;
+    int nitems = 0;
+    const int n = R.n;
+    if (R.status == WR_OK) {
+        const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+        for (int i = 0; i < n && R.status == WR_OK; ++i)
+            for (int j = 0; j < n; ++j)
+                if (i != j && is_inf<C>(D[i * MS + j])) { R.status = WR_EUNREACHABLE; break; }
+    }
+    if (R.status == WR_OK) {
+        int lab[MS];
+        if (m <= 1 || n <= 1) {
+            for (int i = 0; i < n; ++i) lab[i] = 0;
+        } else if (labels_in) {
+            for (int i = 0; i < n; ++i) lab[i] = labels_in[t * MS + i];
+        } else {
+            int pxy[2 * MS];
+            const int *s = stops + o * MS;
+            for (int i = 0; i < n; ++i) {
+                pxy[2 * i] = xy[2 * s[i]];
+                pxy[2 * i + 1] = xy[2 * s[i] + 1];
+            }
+            kmeans_dev(pxy, n, m, lab);
+        }
+        // relabel by first appearance (O7 step 1)
+        int map_lab[MS], nseg = 0, seg_of[MS];
+        for (int i = 0; i < n; ++i) {
+            int id = -1;
+            for (int k = 0; k < nseg; ++k)
+                if (map_lab[k] == lab[i]) id = k;
+            if (id < 0) {
+                if (nseg == WR_MAX_SEGMENTS) { R.status = WR_ETOOLARGE; break; }
+                map_lab[nseg] = lab[i];
+                id = nseg++;
+            }
+            seg_of[i] = id;
+        }
+        if (R.status == WR_OK) {
+            R.mseg = nseg > 0 ? nseg : 1;
+            for (int k = 0; k < WR_MAX_SEGMENTS; ++k) { R.seglen[k] = 0; R.segmap[k] = 0; }
+            for (int i = 0; i < n; ++i) {
+                const int k = seg_of[i];
+                R.segmap[k] |= (uint64_t)i << (4 * R.seglen[k]);
+                R.seglen[k]++;
+            }
+            for (int k = 0; k < nseg; ++k) {
+                if (R.seglen[k] > WR_MAX_EXACT) { R.status = WR_ETOOLARGE; break; }
+                if (R.seglen[k] >= 2) {
+                    const int nj = R.seglen[k];
+                    const int p = prefix_depth(nj);
+                    const int64_t npre = fact(nj) / fact(nj - p);
+                    const int64_t per = chunk / fact(nj - p) > 0 ? chunk / fact(nj - p) : 1;
+                    R.nprob++;
+                    nitems += (int)((npre + per - 1) / per);
+                }
+            }
+        }
+    }
+    if (R.status != WR_OK) { R.nprob = 0; nitems = 0; }
+    ordr[t] = R;
+    prob_cnt[t] = R.nprob;
+    item_cnt[t] = nitems;
+}
+
+// Pass 2: emit problems and work items at the scanned offsets.
+__global__ void route_emit_kernel(int64_t nord, OrderRoute *ordr, const int *prob_off, const int *item_off,
+                                  int64_t chunk, RouteProblem *probs, RouteWorkItem *items) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nord) return;
+    OrderRoute &R = ordr[t];
+    R.prob0 = prob_off[t];
+    if (R.status != WR_OK) return;
+    int pi = prob_off[t], ii = item_off[t];
+    for (int k = 0; k < R.mseg; ++k) {
+        const int nj = R.seglen[k];
+        if (nj < 2) continue;
+        const int p = prefix_depth(nj);
+        const int npre = (int)(fact(nj) / fact(nj - p));
+        const int64_t per64 = chunk / fact(nj - p) > 0 ? chunk / fact(nj - p) : 1;
+        const int per = (int)(per64 < npre ? per64 : npre);
+        RouteProblem P;
+        P.order = (int)t;
+        P.n = nj;
+        P.map = R.segmap[k];
+        P.item0 = ii;
+        P.nitems = (npre + per - 1) / per;
+        for (int q = 0; q < npre; q += per) {
+            RouteWorkItem W;
+            W.problem = pi;
+            W.prefix_lo = q;
+            W.prefix_hi = q + per < npre ? q + per : npre;
+            items[ii++] = W;
+        }
+        probs[pi++] = P;
+    }
+}
+
+// Finalise: warp per order. Exact: unrank the best; segmented: stitch the
+// m'! 2^m' oriented concatenations (O7 step 3-4) with a full left-to-right
+// recompute, ties -> lexicographically smallest sequence.
+template <class C>
+__global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, const uint64_t *prob_best,
+                                      const RouteProblem *probs, const uint32_t *Dall, const int *stops,
+                                      int64_t o_lo, wr_route_result *out, unsigned long long *counters) {
+    __shared__ uint32_t sD[4][DSTRIDE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t = (int64_t)blockIdx.x * 4 + warp;
+    if (t >= nord) return;
+    const OrderRoute R = ordr[t];
+    const int n = R.n;
+    const int *s = stops + (o_lo + t) * MS;
+    wr_route_result res;
+    res.n = n;
+    res.status = R.status;
+    res.m_used = R.mseg;
+    res.rank = 0;
+    res.cost_bits = C::INF;
+    for (int k = 0; k < MS; ++k) res.seq[k] = -1;
+    if (R.status != WR_OK) {
+        if (lane == 0) out[t] = res;
+        return;
+    }
+    const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+    uint32_t *Ds = sD[warp];
+    for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
+    __syncwarp();
+    // each segment's best route as a nibble sequence of order-stop indices
+    uint64_t segseq[WR_MAX_SEGMENTS];
+    int pi = R.prob0;
+    unsigned long long perms = 0;
+    for (int k = 0; k < R.mseg; ++k) {
+        const int nj = R.seglen[k];
+        if (nj >= 2) {
+            const uint64_t b = prob_best[pi];
+            const uint64_t loc = unrank_nib((int64_t)(uint32_t)b, nj);
+            uint64_t g = 0;
+            for (int a = 0; a < nj; ++a) g |= (uint64_t)nib(R.segmap[k], nib(loc, a)) << (4 * a);
+            segseq[k] = g;
+            perms += (unsigned long long)fact(nj);
+            ++pi;
+        } else {
+            segseq[k] = R.segmap[k];   // 0 or 1 stop
+        }
+    }
+    uint64_t final_seq;
+    uint32_t final_cost;
+    if (R.mseg == 1) {
+        final_seq = segseq[0];
+        if (n >= 2) {
+            final_cost = C::unkey((uint32_t)(prob_best[R.prob0] >> 32));
+        } else {
+            final_cost = 0u;
+        }
+    } else {
+        const int m = R.mseg;
+        const int64_t ncand = fact(m) << m;
+        uint32_t best_key = 0xffffffffu;
+        uint64_t best_seq = ~0ull;
+        for (int64_t c = lane; c < ncand; c += 32) {
+            const uint64_t tau = unrank_nib(c >> m, m);
+            const int bits = (int)(c & ((1 << m) - 1));
+            uint64_t seq = 0;
+            int pos = 0;
+            for (int k = 0; k < m; ++k) {
+                const int j = nib(tau, k);
+                const int nj = R.seglen[j];
+                const bool rev = (bits >> k) & 1;
+                for (int a = 0; a < nj; ++a) {
+                    const int x = nib(segseq[j], rev ? nj - 1 - a : a);
+                    seq |= (uint64_t)x << (4 * pos);
+                    ++pos;
+                }
+            }
+            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
+            for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
+            const uint32_t key = C::key(cost);
+            // lexicographic key: first stop in the most significant nibble
+            uint64_t lex = 0;
+            for (int a = 0; a < n; ++a) lex |= (uint64_t)nib(seq, a) << (4 * (15 - a));
+            if (key < best_key || (key == best_key && lex < best_seq)) {
+                best_key = key;
+                best_seq = lex;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
+            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
+            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
+                best_key = k2;
+                best_seq = s2;
+            }
+        }
+        final_cost = C::unkey(best_key);
+        final_seq = 0;
+        for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
+        if (lane == 0) atomicAdd(&counters[1], (unsigned long long)ncand);
+    }
+    if (lane == 0) {
+        // Lehmer rank of the final sequence among the n! orders
+        int64_t rank = 0;
+        for (int a = 0; a < n; ++a) {
+            int smaller = 0;
+            for (int b = a + 1; b < n; ++b) smaller += nib(final_seq, b) < nib(final_seq, a);
+            rank += smaller * fact(n - 1 - a);
+        }
+        res.rank = rank;
+        res.cost_bits = n >= 2 ? final_cost : 0u;
+        for (int a = 0; a < n; ++a) res.seq[a] = s[nib(final_seq, a)];
+        out[t] = res;
+        atomicAdd(&counters[0], perms);
+    }
+}
+
+// ------------------------------------------------------ route_cost (O4) --
+template <class C>
+__global__ void route_cost_kernel(const uint32_t *D, int n, const int *seqs, int len, int64_t count,
+                                  uint32_t *costs, int *bad) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const int *s = seqs + t * len;
+    for (int a = 0; a < len; ++a)
+        if (s[a] < 0 || s[a] >= n) { atomicOr(bad, 1); return; }
+    if (len < 2) { costs[t] = 0u; return; }
+    bool inf = false;
+    uint32_t c = D[s[0] * n + s[1]];
+    int64_t ci = (int)c;
+    inf = c == C::INF;
+    for (int a = 2; a < len; ++a) {
+        const uint32_t leg = D[s[a - 1] * n + s[a]];
+        inf |= leg == C::INF;
+        c = C::add(c, leg);
+        ci += (int)leg;
+    }
+    if (C::INF == 0x7fffffffu) {     // int32: exact sum, INF legs -> INF
+        if (inf) c = C::INF;
+        else if (ci >= (int64_t)INT32_MAX || ci < (int64_t)INT32_MIN) { atomicOr(bad, 2); return; }
+        else c = (uint32_t)(int)ci;
+    }
+    costs[t] = c;
+}
+
+// =========================================================== host side ==
+struct Plan {               // wr_plan
+    int device = 0;
+    const wr_graph *g = nullptr;
+    int64_t B = 0, S = 0;
+    int rank = 0, world = 1;
+    int64_t src_lo = 0, src_hi = 0, order_lo = 0, order_hi = 0;
+    int64_t send_count = 0, max_send = 0;
+    int m = 1;
+    int64_t chunk = WR_DEFAULT_CHUNK;
+    DBuf<int> stops, n_arr, status, is_src, src_row, sources;
+    DBuf<int64_t> blk;      // world+1 source block boundaries
+    DBuf<int64_t> off_all;  // world x (B+1)
+    DBuf<int> labels;       // optional [B][16] labels override
+    std::vector<int64_t> h_blk;
+    int64_t launches = 0;
+};
+
+}  // namespace wr
+
+struct wr_plan : wr::Plan {};
+
+namespace wr {
+
+static unsigned gridn(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
+                           int32_t rank, int32_t world, const wr_route_opts *opts, const int32_t *labels16,
+                           wr_plan **out) {
+    if (!g || !out || B < 0 || (B > 0 && (!order_ptr || !order_nodes)))
+        return fail(WR_EINVAL, "wr_orders_plan: bad arguments");
+    if (world < 1 || rank < 0 || rank >= world) return fail(WR_EINVAL, "wr_orders_plan: rank/world");
+    WR_CUDA(cudaSetDevice(g->device));
+    const int64_t l0 = g_launches;
+    wr_route_opts o{};
+    if (opts) o = *opts;
+    cudaStream_t st = (cudaStream_t)o.stream;
+    auto P = std::make_unique<wr_plan>();
+    P->device = g->device;
+    P->g = g;
+    P->B = B;
+    P->rank = rank;
+    P->world = world;
+    P->m = o.m;
+    P->chunk = o.chunk > 0 ? o.chunk : WR_DEFAULT_CHUNK;
+    if (P->m >= 2 && !labels16 && !g->xy.p)
+        return fail(WR_EINVAL, "wr_orders_plan: segmented routing without labels needs graph xy (O8)");
+    const int V = g->V;
+    int64_t L = 0;
+    if (B > 0) {
+        WR_CUDA(cudaMemcpy(&L, order_ptr + B, 8, cudaMemcpyDefault));
+        int64_t first = 0;
+        WR_CUDA(cudaMemcpy(&first, order_ptr, 8, cudaMemcpyDefault));
+        if (first != 0 || L < 0) return fail(WR_EINVAL, "wr_orders_plan: order_ptr must start at 0");
+    }
+    DBuf<int64_t> d_ptr = to_device<int64_t>(order_ptr, B + 1, st);
+    DBuf<int> d_nodes = to_device<int>(order_nodes, L, st);
+    P->stops.alloc(std::max<int64_t>(B, 1) * WR_MAX_STOPS);
+    P->n_arr.alloc(std::max<int64_t>(B, 1));
+    P->status.alloc(std::max<int64_t>(B, 1));
+    P->is_src.alloc(V);
+    P->src_row.alloc(V);
+    DBuf<int> bad(1);
+    WR_CUDA(cudaMemsetAsync(P->is_src.p, 0, 4LL * V, st));
+    WR_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+    if (B > 0) {
+        order_stops_kernel<<<gridn(B, 256), 256, 0, st>>>(d_ptr.p, d_nodes.p, B, V, P->stops.p, P->n_arr.p,
+                                                         P->status.p, P->is_src.p, bad.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
+    int hbad = 0;
+    WR_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    if (hbad) return fail(WR_EINVAL, "wr_orders_plan: order node outside [0, V)");
+    scan_exclusive_i32(P->is_src.p, P->src_row.p, V, st);
+    int last_row = 0, last_flag = 0;
+    WR_CUDA(cudaMemcpyAsync(&last_row, P->src_row.p + V - 1, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaMemcpyAsync(&last_flag, P->is_src.p + V - 1, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    P->S = (int64_t)last_row + last_flag;
+    P->sources.alloc(std::max<int64_t>(P->S, 1));
+    sources_scatter_kernel<<<gridn(V, 256), 256, 0, st>>>(P->is_src.p, P->src_row.p, V, P->sources.p);
+    src_row_fix_kernel<<<gridn(V, 256), 256, 0, st>>>(P->is_src.p, P->src_row.p, V);
+    count_launch();
+    count_launch();
+    WR_LAUNCH_CHECK();
+    // source blocks and order blocks
+    P->h_blk.resize(world + 1);
+    for (int q = 0; q < world; ++q) {
+        int64_t lo, hi;
+        wr_shard_range(P->S, q, world, &lo, &hi);
+        P->h_blk[q] = lo;
+        P->h_blk[q + 1] = hi;
+    }
+    P->src_lo = P->h_blk[rank];
+    P->src_hi = P->h_blk[rank + 1];
+    wr_shard_range(B, rank, world, &P->order_lo, &P->order_hi);
+    P->blk = to_device<int64_t>(P->h_blk.data(), world + 1, st);
+    // per-rank owned-entry offsets: exclusive scans of counts over orders
+    P->off_all.alloc((size_t)world * (B + 1));
+    WR_CUDA(cudaMemsetAsync(P->off_all.p, 0, sizeof(int64_t) * world * (B + 1), st));
+    if (B > 0) {
+        owned_count_kernel<<<gridn(B, 256), 256, 0, st>>>(P->stops.p, P->n_arr.p, P->status.p, B, P->src_row.p,
+                                                         P->blk.p, world, P->off_all.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
+    std::vector<int64_t> totals(world);
+    for (int q = 0; q < world; ++q) {
+        int64_t *row = P->off_all.p + (int64_t)q * (B + 1);
+        scan_exclusive_i64(row, row, B + 1, st);
+        WR_CUDA(cudaMemcpyAsync(&totals[q], row + B, 8, cudaMemcpyDeviceToHost, st));
+    }
+    WR_CUDA(cudaStreamSynchronize(st));
+    P->send_count = totals[rank];
+    P->max_send = std::max<int64_t>(1, *std::max_element(totals.begin(), totals.end()));
+    if (labels16) P->labels = to_device<int>(labels16, (size_t)std::max<int64_t>(B, 1) * WR_MAX_STOPS, st);
+    WR_CUDA(cudaStreamSynchronize(st));
+    P->launches = g_launches - l0;
+    *out = P.release();
+    return WR_OK;
+}
+
+static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, wr_route_stats *stats) {
+    if (!P || (!send && P->send_count > 0)) return fail(WR_EINVAL, "wr_orders_local: bad arguments");
+    if (!is_device_ptr(send) && P->send_count > 0) return fail(WR_EINVAL, "wr_orders_local: send must be device memory");
+    const wr_graph *g = P->g;
+    WR_CUDA(cudaSetDevice(P->device));
+    const int64_t l0 = g_launches;
+    wr_route_opts o{};
+    if (opts) o = *opts;
+    cudaStream_t st = (cudaStream_t)o.stream;
+    const int V = g->V;
+    const int64_t nsrc = P->src_hi - P->src_lo;
+    cudaEvent_t e0, e1;
+    WR_CUDA(cudaEventCreate(&e0));
+    WR_CUDA(cudaEventCreate(&e1));
+    WR_CUDA(cudaEventRecord(e0, st));
+    BfTileStats h0{0ull, 0, -1};
+    DBuf<BfTileStats> d_stats(1);
+    WR_CUDA(cudaMemcpyAsync(d_stats.p, &h0, sizeof(h0), cudaMemcpyHostToDevice, st));
+    int segments = 0;
+    float bf_ms = 0.f, pred_ms = 0.f;
+    if (o.pred_out && (!is_device_ptr(o.pred_out) || o.pred_rows < P->src_hi))
+        return fail(WR_EINVAL, "wr_orders_local: pred_out must be device memory with >= S rows");
+    if (nsrc > 0) {
+        wr_graph_info_t gi;
+        wr_graph_info(g, &gi);
+        const int64_t budget = budget_bytes(o.hbm_budget);
+        const int64_t fixed = gi.device_bytes + (128 << 20);
+        const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc);
+        const int64_t max_tiles = sb / TS;
+        DBuf<uint32_t> rows((size_t)max_tiles * V * TS);
+        DBuf<int> tile_src(max_tiles * TS);
+        DBuf<int> flat(o.pred_out ? max_tiles : 0);
+        int max_rounds = g->has_negative ? std::max(1, V - 1) : V;
+        const int64_t *off_r = P->off_all.p + (int64_t)P->rank * (P->B + 1);
+        cudaEvent_t b0, b1, b2;
+        WR_CUDA(cudaEventCreate(&b0));
+        WR_CUDA(cudaEventCreate(&b1));
+        WR_CUDA(cudaEventCreate(&b2));
+        for (int64_t lo = P->src_lo; lo < P->src_hi; lo += sb) {
+            const int64_t hi = std::min<int64_t>(P->src_hi, lo + sb);
+            const int ntiles = (int)((hi - lo + TS - 1) / TS);
+            make_tiles(P->sources.p, lo, hi, tile_src.p, st);
+            BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds};
+            WR_CUDA(cudaEventRecord(b0, st));
+            bf_run(g, run, d_stats.p, st);
+            WR_CUDA(cudaEventRecord(b1, st));
+            if (o.pred_out) {   // a4 canonical pred of this segment's sources
+                WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
+                bf_write_outputs(g, run, lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
+                std::vector<int> hflat(ntiles);
+                WR_CUDA(cudaMemcpyAsync(hflat.data(), flat.p, sizeof(int) * ntiles, cudaMemcpyDeviceToHost, st));
+                WR_CUDA(cudaStreamSynchronize(st));
+                std::vector<int> todo;
+                for (int t = 0; t < ntiles; ++t)
+                    if (hflat[t] || g->has_negative) todo.push_back(t);
+                bf_resolve_flat(g, run, todo, lo, o.pred_out, st);
+            }
+            WR_CUDA(cudaEventRecord(b2, st));
+            WR_CUDA(cudaEventSynchronize(b2));
+            float x = 0.f, y = 0.f;
+            WR_CUDA(cudaEventElapsedTime(&x, b0, b1));
+            WR_CUDA(cudaEventElapsedTime(&y, b1, b2));
+            bf_ms += x;
+            pred_ms += y;
+            if (P->B > 0) {
+                gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, st>>>(
+                    P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, lo, hi, off_r,
+                    rows.p, V, (uint32_t *)send);
+                count_launch();
+                WR_LAUNCH_CHECK();
+            }
+            ++segments;
+        }
+        cudaEventDestroy(b0);
+        cudaEventDestroy(b1);
+        cudaEventDestroy(b2);
+    }
+    WR_CUDA(cudaEventRecord(e1, st));
+    BfTileStats hs;
+    WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (hs.negcycle_tile >= 0) return fail(WR_ENEGCYCLE, "wr_orders_local: negative cycle reachable");
+    if (stats) {
+        stats->sources = nsrc;
+        stats->segments = segments;
+        stats->rounds_max = hs.rounds_max;
+        stats->relaxations = (int64_t)hs.relax;
+        stats->ms = ms;
+        stats->kernel_launches = g_launches - l0;
+        stats->bf_ms = bf_ms;
+        stats->pred_ms = pred_ms;
+    }
+    return WR_OK;
+}
+
+template <class C>
+static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64_t nord, wr_route_result *d_res,
+                        unsigned long long *d_counters, cudaStream_t st) {
+    if (nord <= 0) return;
+    const int *xy = P.g->xy.p;
+    DBuf<OrderRoute> ordr(nord);
+    DBuf<int> pcnt(nord + 1), icnt(nord + 1);
+    WR_CUDA(cudaMemsetAsync(pcnt.p + nord, 0, 4, st));
+    WR_CUDA(cudaMemsetAsync(icnt.p + nord, 0, 4, st));
+    route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
+        P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
+        P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
+    scan_exclusive_i32(icnt.p, icnt.p, (int)(nord + 1), st);
+    int nprob = 0, nitems = 0;
+    WR_CUDA(cudaMemcpyAsync(&nprob, pcnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaMemcpyAsync(&nitems, icnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    DBuf<RouteProblem> probs(std::max(nprob, 1));
+    DBuf<RouteWorkItem> items(std::max(nitems, 1));
+    DBuf<uint64_t> item_best(std::max(nitems, 1)), prob_best(std::max(nprob, 1));
+    route_emit_kernel<<<gridn(nord, 128), 128, 0, st>>>(nord, ordr.p, pcnt.p, icnt.p, P.chunk, probs.p, items.p);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    if (nitems > 0) {
+        route_enum_kernel<C><<<gridn(nitems, ENUM_WARPS), ENUM_WARPS * 32, 0, st>>>(probs.p, items.p, nitems, Dall,
+                                                                                    item_best.p);
+        problem_reduce_kernel<<<gridn(nprob, 128), 128, 0, st>>>(probs.p, nprob, item_best.p, prob_best.p);
+        count_launch();
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
+    route_finalize_kernel<C><<<gridn(nord, 4), 128, 0, st>>>(nord, ordr.p, prob_best.p, probs.p, Dall, P.stops.p,
+                                                             o_lo, d_res, d_counters);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    WR_CUDA(cudaStreamSynchronize(st));   // temporaries are freed on return
+}
+
+static wr_status finish_impl(wr_plan *P, const void *gathered, wr_route_result *results, const wr_route_opts *opts,
+                             wr_route_stats *stats) {
+    if (!P) return fail(WR_EINVAL, "wr_orders_finish: null plan");
+    const int64_t nord = P->order_hi - P->order_lo;
+    if (nord > 0 && !results) return fail(WR_EINVAL, "wr_orders_finish: results");
+    if (nord > 0 && !is_device_ptr(gathered)) return fail(WR_EINVAL, "wr_orders_finish: gathered must be device memory");
+    WR_CUDA(cudaSetDevice(P->device));
+    const int64_t l0 = g_launches;
+    wr_route_opts o{};
+    if (opts) o = *opts;
+    cudaStream_t st = (cudaStream_t)o.stream;
+    cudaEvent_t e0, e1;
+    WR_CUDA(cudaEventCreate(&e0));
+    WR_CUDA(cudaEventCreate(&e1));
+    WR_CUDA(cudaEventRecord(e0, st));
+    DBuf<unsigned long long> counters(2);
+    WR_CUDA(cudaMemsetAsync(counters.p, 0, 16, st));
+    const bool res_dev = is_device_ptr(results);
+    DBuf<wr_route_result> d_res;
+    wr_route_result *dres = (wr_route_result *)results;
+    if (nord > 0) {
+        DBuf<uint32_t> Dall((size_t)nord * DSTRIDE);
+        WR_CUDA(cudaMemsetAsync(Dall.p, 0, Dall.bytes(), st));
+        assemble_kernel<<<gridn(nord * WR_MAX_STOPS, 256), 256, 0, st>>>(
+            P->stops.p, P->n_arr.p, P->status.p, P->B, P->order_lo, P->order_hi, P->src_row.p, P->blk.p, P->world,
+            P->off_all.p, (const uint32_t *)gathered, P->max_send, Dall.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+        if (!res_dev) {
+            d_res.alloc(nord);
+            dres = d_res.p;
+        }
+        if (P->g->wtype == WR_F32) route_block<CostF32>(*P, Dall.p, P->order_lo, nord, dres, counters.p, st);
+        else route_block<CostI32>(*P, Dall.p, P->order_lo, nord, dres, counters.p, st);
+        if (!res_dev)
+            WR_CUDA(cudaMemcpyAsync(results, d_res.p, sizeof(wr_route_result) * nord, cudaMemcpyDeviceToHost, st));
+    }
+    WR_CUDA(cudaEventRecord(e1, st));
+    unsigned long long hc[2] = {0, 0};
+    WR_CUDA(cudaMemcpyAsync(hc, counters.p, 16, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (stats) {
+        stats->orders = nord;
+        stats->permutations = (int64_t)hc[0];
+        stats->stitch_candidates = (int64_t)hc[1];
+        stats->ms = ms;
+        stats->kernel_launches = g_launches - l0;
+    }
+    return WR_OK;
+}
+
+// int32 route sums must stay exact: (n-1) legs of at most (V-1)*max|w|.
+static wr_status check_route_overflow(const wr_graph *g) {
+    if (g->wtype == WR_I32 &&
+        (int64_t)(WR_MAX_STOPS - 1) * (int64_t)(g->V - 1) * (int64_t)g->max_abs_w >= (int64_t)INT32_MAX)
+        return fail(WR_EOVERFLOW, "route: (15)(V-1)max|w| >= INT32_MAX, int32 route sums could overflow");
+    return WR_OK;
+}
+
+static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes,
+                                   int64_t B, const wr_route_opts *opts, const int32_t *labels16,
+                                   wr_route_result *results, wr_route_stats *stats) {
+    if (!g) return fail(WR_EINVAL, "wr_route_orders: null graph");
+    if (wr_status r = check_route_overflow(g)) return r;
+    WR_CUDA(cudaSetDevice(g->device));
+    const int64_t l0 = g_launches;
+    wr_route_opts o{};
+    if (opts) o = *opts;
+    cudaStream_t st = (cudaStream_t)o.stream;
+    cudaEvent_t e0, e1;
+    WR_CUDA(cudaEventCreate(&e0));
+    WR_CUDA(cudaEventCreate(&e1));
+    WR_CUDA(cudaEventRecord(e0, st));
+    wr_plan *P = nullptr;
+    wr_status rc = plan_impl(g, order_ptr, order_nodes, B, 0, 1, &o, labels16, &P);
+    if (rc) return rc;
+    std::unique_ptr<wr_plan> hold(P);
+    DBuf<uint32_t> send(std::max<int64_t>(P->max_send, 1));
+    wr_route_stats s1{}, s2{};
+    rc = local_impl(P, send.p, &o, &s1);
+    if (rc) return rc;
+    rc = finish_impl(P, send.p, results, &o, &s2);
+    if (rc) return rc;
+    WR_CUDA(cudaEventRecord(e1, st));
+    WR_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (stats) {
+        *stats = s2;
+        stats->orders = B;
+        stats->sources = P->S;
+        stats->segments = s1.segments;
+        stats->rounds_max = s1.rounds_max;
+        stats->relaxations = s1.relaxations;
+        stats->ms = ms;
+        stats->kernel_launches = g_launches - l0;
+        stats->bf_ms = s1.bf_ms;
+        stats->pred_ms = s1.pred_ms;
+    }
+    return WR_OK;
+}
+
+}  // namespace wr
+
+extern "C" {
+
+wr_status wr_orders_plan(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
+                         int32_t rank, int32_t world, const wr_route_opts *opts, wr_plan **out) {
+    return wr::guarded([&] {
+        if (wr_status r = g ? wr::check_route_overflow(g) : WR_OK) return r;
+        return wr::plan_impl(g, order_ptr, order_nodes, B, rank, world, opts, nullptr, out);
+    });
+}
+
+wr_status wr_plan_info(const wr_plan *p, wr_plan_info_t *info) {
+    if (!p || !info) return wr::fail(WR_EINVAL, "wr_plan_info: null argument");
+    info->B = p->B;
+    info->S = p->S;
+    info->rank = p->rank;
+    info->world = p->world;
+    info->src_lo = p->src_lo;
+    info->src_hi = p->src_hi;
+    info->order_lo = p->order_lo;
+    info->order_hi = p->order_hi;
+    info->send_count = p->send_count;
+    info->max_send = p->max_send;
+    info->wtype = p->g->wtype;
+    return WR_OK;
+}
+
+wr_status wr_orders_local(wr_plan *p, void *send, const wr_route_opts *opts, wr_route_stats *stats) {
+    return wr::guarded([&] { return wr::local_impl(p, send, opts, stats); });
+}
+
+wr_status wr_orders_finish(wr_plan *p, const void *gathered, wr_route_result *results, const wr_route_opts *opts,
+                           wr_route_stats *stats) {
+    return wr::guarded([&] { return wr::finish_impl(p, gathered, results, opts, stats); });
+}
+
+wr_status wr_plan_free(wr_plan *p) {
+    if (!p) return WR_OK;
+    return wr::guarded([&] {
+        WR_CUDA(cudaSetDevice(p->device));
+        delete p;
+        return WR_OK;
+    });
+}
+
+wr_status wr_route_orders(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
+                          const wr_route_opts *opts, wr_route_result *results, wr_route_stats *stats) {
+    return wr::guarded([&] { return wr::route_orders_impl(g, order_ptr, order_nodes, B, opts, nullptr, results, stats); });
+}
+
+wr_status wr_route_segmented(const wr_graph *g, const int32_t *stops, int32_t n, const int32_t *labels, int32_t m,
+                             const wr_route_opts *opts, wr_route_result *out) {
+    return wr::guarded([&]() -> wr_status {
+        if (!g || !out || n < 0 || (n > 0 && !stops)) return wr::fail(WR_EINVAL, "wr_route_segmented: bad arguments");
+        if (n > WR_MAX_STOPS) return wr::fail(WR_ETOOLARGE, "wr_route_segmented: n > 16");
+        std::vector<int32_t> hs(n);
+        if (n) WR_CUDA(cudaMemcpy(hs.data(), stops, 4LL * n, cudaMemcpyDefault));
+        std::vector<int32_t> uniq(hs);
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        std::vector<int32_t> lab16(WR_MAX_STOPS, 0);
+        if (labels) {
+            std::vector<int32_t> hl(uniq.size());
+            if (!uniq.empty()) WR_CUDA(cudaMemcpy(hl.data(), labels, 4 * uniq.size(), cudaMemcpyDefault));
+            for (size_t i = 0; i < uniq.size(); ++i) lab16[i] = hl[i];
+        }
+        int64_t ptr[2] = {0, n};
+        wr_route_opts o{};
+        if (opts) o = *opts;
+        o.m = m;
+        if (labels && m < 2) o.m = 2;   // caller labels always go through the stitch
+        return wr::route_orders_impl(g, ptr, hs.data(), 1, &o, labels ? lab16.data() : nullptr, out, nullptr);
+    });
+}
+
+wr_status wr_segment_plan(const int32_t *xy, int32_t n, int32_t m, int32_t *labels_out, int32_t device) {
+    return wr::guarded([&]() -> wr_status {
+        if (!xy || !labels_out || n < 1 || n > WR_MAX_STOPS || m < 1)
+            return wr::fail(WR_EINVAL, "wr_segment_plan: bad arguments (1 <= n <= 16, m >= 1)");
+        WR_CUDA(cudaSetDevice(device));
+        std::vector<int32_t> h(2 * n);
+        WR_CUDA(cudaMemcpy(h.data(), xy, 8LL * n, cudaMemcpyDefault));
+        for (int v : h)
+            if (v <= -(1 << 20) || v >= (1 << 20)) return wr::fail(WR_EINVAL, "wr_segment_plan: |xy| >= 2^20");
+        wr::DBuf<int> dxy = wr::to_device<int>(h.data(), 2 * n, 0), dl(n);
+        wr::segment_plan_kernel<<<1, 32>>>(dxy.p, n, m, dl.p);
+        wr::count_launch();
+        WR_LAUNCH_CHECK();
+        WR_CUDA(cudaMemcpy(labels_out, dl.p, 4LL * n, cudaMemcpyDefault));
+        return WR_OK;
+    });
+}
+
+wr_status wr_route_cost(int32_t wtype, const void *D, int32_t n, const int32_t *seqs, int32_t len, int64_t count,
+                        void *costs, void *stream) {
+    return wr::guarded([&]() -> wr_status {
+        if ((wtype != WR_I32 && wtype != WR_F32) || n < 1 || !D || len < 0 || count < 0 ||
+            (count > 0 && (!seqs || !costs)))
+            return wr::fail(WR_EINVAL, "wr_route_cost: bad arguments");
+        if (count == 0) return WR_OK;
+        cudaStream_t st = (cudaStream_t)stream;
+        int dev = 0;
+        WR_CUDA(cudaGetDevice(&dev));
+        wr::DBuf<uint32_t> dD = wr::to_device<uint32_t>((const uint32_t *)D, (size_t)n * n, st);
+        wr::DBuf<int> dS = wr::to_device<int>(seqs, (size_t)count * len, st);
+        const bool cdev = wr::is_device_ptr(costs);
+        wr::DBuf<uint32_t> dC;
+        uint32_t *cp = (uint32_t *)costs;
+        if (!cdev) {
+            dC.alloc(count);
+            cp = dC.p;
+        }
+        wr::DBuf<int> bad(1);
+        WR_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+        if (wtype == WR_F32)
+            wr::route_cost_kernel<wr::CostF32><<<wr::gridn(count, 256), 256, 0, st>>>(dD.p, n, dS.p, len, count, cp, bad.p);
+        else
+            wr::route_cost_kernel<wr::CostI32><<<wr::gridn(count, 256), 256, 0, st>>>(dD.p, n, dS.p, len, count, cp, bad.p);
+        wr::count_launch();
+        WR_LAUNCH_CHECK();
+        int hb = 0;
+        WR_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
+        if (!cdev) WR_CUDA(cudaMemcpyAsync(costs, dC.p, 4 * count, cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        if (hb & 1) return wr::fail(WR_EINVAL, "wr_route_cost: sequence index outside [0, n)");
+        if (hb & 2) return wr::fail(WR_EOVERFLOW, "wr_route_cost: int32 route sum overflows");
+        return WR_OK;
+    });
+}
+
+}  // extern "C"

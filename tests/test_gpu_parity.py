@@ -1,0 +1,306 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle, element
+by element on the same seeded inputs. Bar (north star): dist and route cost
+bit-exact for int32 AND fp32; pred equal to the canonical predecessor (O3);
+route sequences equal (lexicographic tie rules O5/O7)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import gen  # noqa: E402
+import oracle  # noqa: E402
+
+wr = pytest.importorskip("paper_2504_20655_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.set_device(0)
+
+
+class G:
+    def __init__(self, V, src, dst, w, xy=None):
+        self.V, self.src, self.dst, self.w = V, np.asarray(src, np.int32), np.asarray(dst, np.int32), np.asarray(w)
+        self.xy = xy
+
+
+def check_bf(g, sources, pred=True, variant=wr.WR_BF_AUTO, budget=0, targets=None):
+    G = wr.Graph(g.V, g.src, g.dst, g.w, xy=getattr(g, "xy", None))
+    dist, p, st = wr.bf_batch(G, sources, targets=targets, pred=pred and targets is None, variant=variant,
+                              hbm_budget=budget)
+    ref = oracle.bf_many(g, sources)
+    if targets is not None:
+        ref = ref[:, targets]
+    assert dist.tobytes() == ref.tobytes()
+    if pred and targets is None:
+        for i, s in enumerate(sources):
+            assert np.array_equal(p[i], oracle.pred(g, int(s), ref[i])), (i, s)
+    return dist, p, st
+
+
+# ------------------------------------------------------------------ a1
+def test_graph_load_validation():
+    with pytest.raises(wr.WrError) as e:
+        wr.Graph(3, [0, 3], [1, 2], np.array([1, 1], np.int32))
+    assert e.value.code == wr.WR_EINVAL
+    for bad in (np.nan, -1.0, np.inf):
+        with pytest.raises(wr.WrError) as e:
+            wr.Graph(3, [0, 1], [1, 2], np.array([1.0, bad], np.float32))
+        assert e.value.code == wr.WR_EINVAL
+    with pytest.raises(wr.WrError) as e:
+        wr.Graph(3, [0, 1], [1, 2], np.array([1, 2**30 + 5], np.int32))
+    assert e.value.code == wr.WR_EOVERFLOW
+    G = wr.Graph(4, [0, 1, 2], [1, 2, 3], np.array([1.0, -0.0, 2.0], np.float32))
+    d, _, _ = wr.bf_batch(G, [0])
+    assert d.tolist() == [[0.0, 1.0, 1.0, 3.0]] and not np.signbit(d).any()
+
+
+def test_graph_csr_input_equals_coo():
+    g = gen.config(2)[0]
+    order = np.lexsort((g.dst, g.src))
+    rp = np.zeros(g.V + 1, np.int64)
+    np.add.at(rp, g.src[order] + 1, 1)
+    rp = np.cumsum(rp)
+    Gc = wr.Graph(g.V, row_ptr=rp, col=g.dst[order], w=g.w[order])
+    Gd = wr.Graph(g.V, g.src, g.dst, g.w)
+    srcs = np.arange(0, g.V, 7, dtype=np.int32)
+    a, _, _ = wr.bf_batch(Gc, srcs)
+    b, _, _ = wr.bf_batch(Gd, srcs)
+    assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------------ a3/a4
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+@pytest.mark.parametrize("k", [1, 2])
+def test_bf_configs_all_sources(k, wtype):
+    g = gen.config(k, wtype=wtype)[0]
+    check_bf(g, np.arange(g.V, dtype=np.int32))
+
+
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_bf_config3_sample(wtype):
+    g, orders, _ = gen.config(3, wtype=wtype, B=512)
+    stops = np.unique(orders.order_nodes)
+    check_bf(g, stops[:300])
+
+
+@pytest.mark.parametrize("variant", [wr.WR_BF_FRONTIER, wr.WR_BF_DENSE])
+def test_bf_variants_equal(variant):
+    g = gen.config(2, wtype="f32")[0]
+    check_bf(g, np.arange(0, g.V, 3, dtype=np.int32), variant=variant)
+
+
+def test_bf_random_graphs_flat_and_absorption():
+    """Zero weights, tiny weights (fp32 absorption) and multi-arcs exercise the
+    flat-vertex path of the canonical pred."""
+    rng = np.random.default_rng(5)
+    for trial in range(30):
+        V = int(rng.integers(2, 300))
+        E = int(rng.integers(0, 5 * V))
+        src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+        if trial % 2:
+            w = rng.integers(0, 4, E).astype(np.int32)
+        else:
+            c = rng.integers(0, 4, E)
+            w = np.select([c == 0, c == 1, c == 2], [np.zeros(E), np.full(E, 1e-8), 1e7 * rng.random(E)],
+                          rng.random(E)).astype(np.float32)
+        g = G(V, src, dst, w)
+        check_bf(g, rng.integers(0, V, int(rng.integers(1, 70))).astype(np.int32))
+
+
+def test_bf_negative_int_weights_and_negcycle():
+    rng = np.random.default_rng(9)
+    done = 0
+    while done < 15:
+        V = int(rng.integers(2, 60))
+        E = int(rng.integers(V, 4 * V))
+        g = G(V, rng.integers(0, V, E), rng.integers(0, V, E), rng.integers(-2, 8, E).astype(np.int32))
+        srcs = rng.integers(0, V, 5).astype(np.int32)
+        try:
+            oracle.bf_many(g, srcs)
+        except oracle.OracleError:
+            with pytest.raises(wr.WrError) as e:
+                wr.bf_batch(wr.Graph(g.V, g.src, g.dst, g.w), srcs)
+            assert e.value.code == wr.WR_ENEGCYCLE
+            continue
+        check_bf(g, srcs)
+        done += 1
+
+
+def test_bf_targets_repeats_and_device_outputs():
+    g = gen.config(3, wtype="f32")[0]
+    rng = np.random.default_rng(1)
+    srcs = rng.integers(0, g.V, 77).astype(np.int32)
+    srcs[5] = srcs[6]
+    tg = rng.integers(0, g.V, 45).astype(np.int32)
+    check_bf(g, srcs, targets=tg)
+    G = wr.Graph.from_gen(g)
+    d_dev = torch.empty((77, g.V), dtype=torch.float32, device="cuda")
+    p_dev = torch.empty((77, g.V), dtype=torch.int32, device="cuda")
+    wr.bf_batch(G, srcs, pred=True, dist_out=d_dev, pred_out=p_dev)
+    d_host, p_host, _ = wr.bf_batch(G, srcs, pred=True)
+    assert np.array_equal(d_dev.cpu().numpy(), d_host) and np.array_equal(p_dev.cpu().numpy(), p_host)
+
+
+def test_bf_segment_budget_invariance():
+    g = gen.config(3)[0]
+    srcs = np.arange(0, g.V, 29, dtype=np.int32)   # 182 sources
+    G = wr.Graph.from_gen(g)
+    a, pa, sa = wr.bf_batch(G, srcs, pred=True)
+    budget = G.info().device_bytes + (64 << 20) + 64 * 4 * g.V * 2  # forces 64-source segments
+    b, pb, sb = wr.bf_batch(G, srcs, pred=True, hbm_budget=budget)
+    assert sa.segments == 1 and sb.segments > 1
+    assert a.tobytes() == b.tobytes() and np.array_equal(pa, pb)
+
+
+# ------------------------------------------------------------------ routes
+def test_route_cost_vs_oracle():
+    rng = np.random.default_rng(3)
+    for dt in (np.int32, np.float32):
+        n = 9
+        D = (rng.random((n, n)) * 50).astype(dt)
+        D[2, 5] = np.iinfo(np.int32).max if dt == np.int32 else np.inf
+        seqs = np.array([rng.permutation(n) for _ in range(300)], dtype=np.int32)
+        got = wr.route_cost(D, seqs)
+        exp = np.array([oracle.route_cost(D, s) for s in seqs], dtype=dt)
+        assert got.tobytes() == exp.tobytes()
+    with pytest.raises(wr.WrError):
+        wr.route_cost(np.zeros((3, 3), np.int32), np.array([[0, 3]], np.int32))
+
+
+def test_route_segmented_worked_example():
+    from test_oracle_bf import load_three_aisle
+    rec = load_three_aisle()
+    g = gen.aisle(3, 4, 2)
+    G = wr.Graph.from_gen(g)
+    r = wr.route_segmented(G, rec["picks"], m=1)
+    picks = np.array(rec["picks"])
+    cost, seq, rank = rec["exact"][0], rec["exact"][1], rec["exact"][2]
+    assert int(r["cost_bits"]) == cost and r["rank"] == rank and r["seq"][:5].tolist() == picks[seq].tolist()
+    for labels, c, s in rec["segmented"]:
+        r = wr.route_segmented(G, rec["picks"], labels=labels, m=3)
+        assert int(r["cost_bits"]) == c and r["seq"][:5].tolist() == picks[s].tolist()
+
+
+def compare_orders(g, orders, m, chunk=0, G=None, results=None):
+    G = G or wr.Graph.from_gen(g)
+    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk) if results is None \
+        else (results, None)
+    exp = oracle.route_orders(g, orders, m=m)
+    ok = exp["order_rc"] == 0
+    assert np.array_equal(res["status"][ok], np.zeros(ok.sum()))
+    cost = wr.decode_cost(res, G.wtype)
+    assert cost[ok].tobytes() == exp["cost"][ok].tobytes()
+    assert np.array_equal(res["seq"][ok], exp["seq"][ok])
+    assert np.array_equal(res["rank"][ok], exp["rank"][ok])
+    assert np.array_equal(res["n"], exp["n"])
+    return res, st
+
+
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+@pytest.mark.parametrize("k,B", [(1, None), (2, None), (3, 1024)])
+def test_route_orders_exact(k, B, wtype):
+    g, orders, _ = gen.config(k, wtype=wtype, B=B)
+    compare_orders(g, orders, m=1)
+
+
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_orders_segmented_config4(wtype):
+    g, orders, _ = gen.config(4, wtype=wtype, B=256)
+    res, st = compare_orders(g, orders, m=3)
+    assert st.stitch_candidates > 0
+
+
+def test_route_orders_exact_large_chunked():
+    """C4 exact mode (n = 10-11, 14 chunks of <= 2,903,040 permutations) on a
+    small sample; also a tiny chunk to force many work items."""
+    g, orders, _ = gen.config(4, B=4)
+    compare_orders(g, orders, m=1)
+    g2, o2, _ = gen.config(2, B=32)
+    compare_orders(g2, o2, m=1, chunk=50)
+
+
+def test_route_orders_edge_cases():
+    g = gen.config(2)[0]
+    G = wr.Graph.from_gen(g)
+    # empty order, single stop, duplicate lines, 17 distinct stops (too large)
+    nodes = [5, 5, 5, 7, 7] + list(range(20, 37))
+    ptr = np.array([0, 0, 3, 5, 5 + 17], np.int64)
+    res, _ = wr.route_orders(G, ptr, np.array(nodes, np.int32))
+    assert res["n"][:3].tolist() == [0, 1, 2]
+    assert res["status"].tolist() == [0, 0, 0, wr.WR_ETOOLARGE]
+    assert res["cost_bits"][1] == 0 and res["seq"][1][0] == 5
+    # unreachable stops: two components
+    g2 = G_disconnected()
+    G2 = wr.Graph(g2.V, g2.src, g2.dst, g2.w)
+    res, _ = wr.route_orders(G2, np.array([0, 2, 4], np.int64), np.array([0, 1, 0, 3], np.int32))
+    assert res["status"].tolist() == [0, wr.WR_EUNREACHABLE]
+
+
+def G_disconnected():
+    return G(4, [0, 1, 2, 3], [1, 0, 3, 2], np.array([1, 1, 1, 1], np.int32))
+
+
+def test_route_orders_budget_and_chunk_invariance():
+    g, orders, _ = gen.config(3, B=2048)
+    G = wr.Graph.from_gen(g)
+    a, sa = wr.route_orders(G, orders.order_ptr, orders.order_nodes)
+    budget = G.info().device_bytes + (128 << 20) + 256 * 4 * g.V
+    b, sb = wr.route_orders(G, orders.order_ptr, orders.order_nodes, hbm_budget=budget, chunk=97)
+    assert sb.segments > 1
+    assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------------ a9
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_phases_equal_single(world):
+    """Virtual ranks run one after another on one GPU; the all-gather is a
+    rank-major concatenation of the padded send buffers (what
+    torch.distributed.all_gather_into_tensor produces). No kernel waits on
+    another rank."""
+    g, orders, _ = gen.config(3, B=1500)
+    G = wr.Graph.from_gen(g)
+    ref, _ = wr.route_orders(G, orders.order_ptr, orders.order_nodes)
+    plans = [wr.OrdersPlan(G, orders.order_ptr, orders.order_nodes, r, world) for r in range(world)]
+    max_send = plans[0].info.max_send
+    assert all(p.info.max_send == max_send for p in plans)
+    gathered = torch.zeros(world * max_send, dtype=torch.int32, device="cuda")
+    for r, p in enumerate(plans):
+        p.local(gathered[r * max_send:(r + 1) * max_send])
+    parts = [p.finish(gathered)[0] for p in plans]
+    got = np.concatenate(parts)
+    assert got.tobytes() == ref.tobytes()
+
+
+# ------------------------------------------------------------------ full size
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_config5_full_size_sampled(wtype):
+    """BASELINE.json configs[4] at full size (262,144 orders, 100k-vertex
+    lattice, ~84.7k BF sources) in the bench's launch configuration; sampled
+    orders and sources are recomputed by the oracle one by one."""
+    g, orders, _ = gen.config(5, wtype=wtype)
+    G = wr.Graph.from_gen(g)
+    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes)
+    assert st.sources == np.unique(orders.order_nodes).size
+    assert (res["status"] == 0).all()
+    rng = np.random.default_rng(55)
+    sample = np.sort(rng.choice(orders.B, 12, replace=False))
+    for o in sample:
+        nodes = orders.order_nodes[orders.order_ptr[o]:orders.order_ptr[o + 1]]
+        stops = np.unique(nodes)
+        rows = oracle.bf_many(g, stops)
+        D = rows[:, stops]
+        c, r, s = oracle.exact_route(D)
+        assert wr.decode_cost(res[o:o + 1], G.wtype)[0] == c
+        assert res["seq"][o][:stops.size].tolist() == stops[s].tolist() and res["rank"][o] == r
+    # sampled full dist + pred rows of the same launch family
+    srcs = np.sort(rng.choice(g.V, 40, replace=False)).astype(np.int32)
+    dist, pred, _ = wr.bf_batch(G, srcs, pred=True)
+    ref = oracle.bf_many(g, srcs)
+    assert dist.tobytes() == ref.tobytes()
+    for i in range(0, 40, 8):
+        assert np.array_equal(pred[i], oracle.pred(g, int(srcs[i]), ref[i]))
+    assert oracle.certificate(g, srcs, dist, pred) == 0
