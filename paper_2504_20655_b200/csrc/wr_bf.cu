@@ -98,6 +98,116 @@ void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int *d_tile_src, c
     WR_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------- relaxing one word --
+constexpr uint32_t FULL = 0xffffffffu;
+
+// Pull over all in-arcs of v for the 32 lanes (generic degree).
+template <class Op>
+__device__ __forceinline__ uint32_t relax_vertex(const DevGraph &g, const uint32_t *__restrict__ R, int a0, int a1,
+                                                 int lane, uint32_t d) {
+    for (int base = a0; base < a1; base += 32) {
+        const int cnt = min(32, a1 - base);
+        int my_u = 0;
+        uint32_t my_w = 0;
+        if (lane < cnt) {
+            my_u = g.in_src[base + lane];
+            my_w = g.in_w[base + lane];
+        }
+        int k = 0;
+        for (; k + 4 <= cnt; k += 4) {
+            const int u0 = __shfl_sync(FULL, my_u, k), u1 = __shfl_sync(FULL, my_u, k + 1);
+            const int u2 = __shfl_sync(FULL, my_u, k + 2), u3 = __shfl_sync(FULL, my_u, k + 3);
+            const uint32_t w0 = __shfl_sync(FULL, my_w, k), w1 = __shfl_sync(FULL, my_w, k + 1);
+            const uint32_t w2 = __shfl_sync(FULL, my_w, k + 2), w3 = __shfl_sync(FULL, my_w, k + 3);
+            const uint32_t x0 = R[(size_t)u0 * TS + lane], x1 = R[(size_t)u1 * TS + lane];
+            const uint32_t x2 = R[(size_t)u2 * TS + lane], x3 = R[(size_t)u3 * TS + lane];
+            d = Op::relax(d, x0, w0);
+            d = Op::relax(d, x1, w1);
+            d = Op::relax(d, x2, w2);
+            d = Op::relax(d, x3, w3);
+        }
+        for (; k < cnt; ++k) {
+            const int u = __shfl_sync(FULL, my_u, k);
+            const uint32_t wk = __shfl_sync(FULL, my_w, k);
+            d = Op::relax(d, R[(size_t)u * TS + lane], wk);
+        }
+    }
+    return d;
+}
+
+// Relaxes the candidate vertices (bits of m) of word w for all 32 lanes.
+// The word's CSC offsets are read with one coalesced load; two candidates
+// are processed per iteration (lanes 0-15 hold the first one's arcs, 16-31
+// the second's) so four independent 128-B row gathers are in flight.
+// Returns the word's change mask (one __any_sync vote per vertex).
+template <class Op>
+__device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
+                                               int lane, unsigned long long &relax) {
+    const int vl = (w << 5) + lane;
+    int p_lo = 0, p_hi = 0;
+    if (vl < g.V) {
+        p_lo = g.in_ptr[vl];
+        p_hi = g.in_ptr[vl + 1];
+    }
+    uint32_t chg = 0;
+    while (m) {
+        const int b0 = __ffs(m) - 1;
+        m &= m - 1;
+        const bool two = m != 0;
+        int b1 = b0;
+        if (two) {
+            b1 = __ffs(m) - 1;
+            m &= m - 1;
+        }
+        const int v0 = (w << 5) + b0, v1 = (w << 5) + b1;
+        const int a00 = __shfl_sync(FULL, p_lo, b0), a01 = __shfl_sync(FULL, p_hi, b0);
+        const int a10 = __shfl_sync(FULL, p_lo, b1), a11 = __shfl_sync(FULL, p_hi, b1);
+        const int n0 = a01 - a00, n1 = two ? a11 - a10 : 0;
+        const uint32_t e0 = R[(size_t)v0 * TS + lane];
+        const uint32_t e1 = two ? R[(size_t)v1 * TS + lane] : 0u;
+        uint32_t d0 = e0, d1 = e1;
+        if (n0 <= 16 && n1 <= 16) {
+            const int sub = lane & 15;
+            const int base = lane < 16 ? a00 : a10;
+            const int cnt = lane < 16 ? n0 : n1;
+            int my_u = 0;
+            uint32_t my_w = 0;
+            if (sub < cnt) {
+                my_u = g.in_src[base + sub];
+                my_w = g.in_w[base + sub];
+            }
+            const int kmax = max(n0, n1);
+            for (int k = 0; k < kmax; k += 2) {
+                const int u00 = __shfl_sync(FULL, my_u, k), u01 = __shfl_sync(FULL, my_u, k + 1);
+                const int u10 = __shfl_sync(FULL, my_u, 16 + k), u11 = __shfl_sync(FULL, my_u, 17 + k);
+                const uint32_t w00 = __shfl_sync(FULL, my_w, k), w01 = __shfl_sync(FULL, my_w, k + 1);
+                const uint32_t w10 = __shfl_sync(FULL, my_w, 16 + k), w11 = __shfl_sync(FULL, my_w, 17 + k);
+                const uint32_t x00 = k < n0 ? R[(size_t)u00 * TS + lane] : 0u;
+                const uint32_t x01 = k + 1 < n0 ? R[(size_t)u01 * TS + lane] : 0u;
+                const uint32_t x10 = k < n1 ? R[(size_t)u10 * TS + lane] : 0u;
+                const uint32_t x11 = k + 1 < n1 ? R[(size_t)u11 * TS + lane] : 0u;
+                if (k < n0) d0 = Op::relax(d0, x00, w00);
+                if (k + 1 < n0) d0 = Op::relax(d0, x01, w01);
+                if (k < n1) d1 = Op::relax(d1, x10, w10);
+                if (k + 1 < n1) d1 = Op::relax(d1, x11, w11);
+            }
+        } else {
+            d0 = relax_vertex<Op>(g, R, a00, a01, lane, d0);
+            if (two) d1 = relax_vertex<Op>(g, R, a10, a11, lane, d1);
+        }
+        relax += (unsigned long long)(n0 + n1);
+        const bool c0 = Op::less(d0, e0);
+        if (c0) R[(size_t)v0 * TS + lane] = d0;
+        if (__any_sync(FULL, c0)) chg |= 1u << b0;
+        if (two) {
+            const bool c1 = Op::less(d1, e1);
+            if (c1) R[(size_t)v1 * TS + lane] = d1;
+            if (__any_sync(FULL, c1)) chg |= 1u << b1;
+        }
+    }
+    return chg;
+}
+
 // ------------------------------------------------------ the sweep kernel --
 // One CTA per tile at a time. Shared memory: two V-bit bitmaps
 // (changed = vertices improved last round, cand = their out-neighbours).
@@ -179,52 +289,7 @@ __global__ void __launch_bounds__(BF_THREADS) bf_frontier_kernel(DevGraph g, con
                 if (!m) continue;
                 __syncwarp();
                 if (lane == 0) cand[w] = 0u;
-                uint32_t chg = 0;
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int v = (w << 5) + b;
-                    const int a0 = g.in_ptr[v], a1 = g.in_ptr[v + 1];
-                    const uint32_t d0 = R[(size_t)v * TS + lane];
-                    uint32_t d = d0;
-                    for (int base = a0; base < a1; base += 32) {
-                        const int cnt = min(32, a1 - base);
-                        int my_u = 0;
-                        uint32_t my_w = 0;
-                        if (lane < cnt) {
-                            my_u = g.in_src[base + lane];
-                            my_w = g.in_w[base + lane];
-                        }
-                        int k = 0;
-                        for (; k + 4 <= cnt; k += 4) {
-                            const int u0 = __shfl_sync(0xffffffffu, my_u, k);
-                            const int u1 = __shfl_sync(0xffffffffu, my_u, k + 1);
-                            const int u2 = __shfl_sync(0xffffffffu, my_u, k + 2);
-                            const int u3 = __shfl_sync(0xffffffffu, my_u, k + 3);
-                            const uint32_t w0 = __shfl_sync(0xffffffffu, my_w, k);
-                            const uint32_t w1 = __shfl_sync(0xffffffffu, my_w, k + 1);
-                            const uint32_t w2 = __shfl_sync(0xffffffffu, my_w, k + 2);
-                            const uint32_t w3 = __shfl_sync(0xffffffffu, my_w, k + 3);
-                            const uint32_t x0 = R[(size_t)u0 * TS + lane];
-                            const uint32_t x1 = R[(size_t)u1 * TS + lane];
-                            const uint32_t x2 = R[(size_t)u2 * TS + lane];
-                            const uint32_t x3 = R[(size_t)u3 * TS + lane];
-                            d = Op::relax(d, x0, w0);
-                            d = Op::relax(d, x1, w1);
-                            d = Op::relax(d, x2, w2);
-                            d = Op::relax(d, x3, w3);
-                        }
-                        for (; k < cnt; ++k) {
-                            const int u = __shfl_sync(0xffffffffu, my_u, k);
-                            const uint32_t wk = __shfl_sync(0xffffffffu, my_w, k);
-                            d = Op::relax(d, R[(size_t)u * TS + lane], wk);
-                        }
-                    }
-                    relax += (unsigned long long)(a1 - a0);
-                    const bool c = Op::less(d, d0);
-                    if (c) R[(size_t)v * TS + lane] = d;
-                    if (__any_sync(0xffffffffu, c)) chg |= 1u << b;
-                }
+                const uint32_t chg = relax_word<Op>(g, R, w, m, lane, relax);
                 if (chg) {
                     if (lane == 0) changed[w] = chg;
                     any = 1;
@@ -312,27 +377,29 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
         const uint32_t d = R[(size_t)v * TS + lane];
         sd[warp][j][lane] = d;
         if (pred_out && !targets) {
-            int p = -1;
-            if (v != s && s >= 0 && Op::finite(d)) {
-                int best = 0x7fffffff;
-                if (!neg_graph) {
-                    const int a0 = g.in_ptr[v], a1 = g.in_ptr[v + 1];
-                    for (int base = a0; base < a1; base += 32) {
-                        const int cnt = min(32, a1 - base);
-                        int my_u = 0;
-                        uint32_t my_w = 0;
-                        if (lane < cnt) {
-                            my_u = g.in_src[base + lane];
-                            my_w = g.in_w[base + lane];
-                        }
-                        for (int k = 0; k < cnt; ++k) {
-                            const int u = __shfl_sync(0xffffffffu, my_u, k);
-                            const uint32_t wk = __shfl_sync(0xffffffffu, my_w, k);
-                            const uint32_t du = R[(size_t)u * TS + lane];
-                            if (Op::tight(du, wk, d) && Op::less(du, d) && u < best) best = u;
-                        }
+            // lane-divergent predicate; the shuffles below stay warp-uniform
+            const bool active = v != s && s >= 0 && Op::finite(d);
+            int best = 0x7fffffff;
+            if (!neg_graph) {
+                const int a0 = g.in_ptr[v], a1 = g.in_ptr[v + 1];
+                for (int base = a0; base < a1; base += 32) {
+                    const int cnt = min(32, a1 - base);
+                    int my_u = 0;
+                    uint32_t my_w = 0;
+                    if (lane < cnt) {
+                        my_u = g.in_src[base + lane];
+                        my_w = g.in_w[base + lane];
+                    }
+                    for (int k = 0; k < cnt; ++k) {
+                        const int u = __shfl_sync(0xffffffffu, my_u, k);
+                        const uint32_t wk = __shfl_sync(0xffffffffu, my_w, k);
+                        const uint32_t du = R[(size_t)u * TS + lane];
+                        if (active && Op::tight(du, wk, d) && Op::less(du, d) && u < best) best = u;
                     }
                 }
+            }
+            int p = -1;
+            if (active) {
                 if (best != 0x7fffffff) p = best;
                 else flat = true;   // resolved by the tight-arc BFS pass
             }

@@ -53,14 +53,27 @@ __host__ __device__ inline int64_t fact(int n) {
     return f;
 }
 
-// p(n): prefix depth; subtrees of (n-p)! leaves, >= 200 prefixes when possible.
+// p(n): prefix depth; a lane walks subtrees of (n-p)! leaves. Chosen to
+// minimise the warp's cost ceil(P/32) * (decode + leaves * ~12 instr),
+// P = n!/(n-p)! prefixes, with subtrees of at most 7! leaves (template depth).
 __host__ __device__ inline int prefix_depth(int n) {
     if (n <= 1) return 0;
-    int p = n - 7 > 1 ? n - 7 : 1;
-    while (p < n - 1 && fact(n) / fact(n - p) < 200) ++p;
-    return p;
+    int best_p = n - 1;
+    int64_t best_c = -1;
+    for (int p = (n - 7 > 1 ? n - 7 : 1); p <= n - 1; ++p) {
+        const int64_t P = fact(n) / fact(n - p);
+        const int64_t c = ((P + 31) / 32) * (40 + 12 * fact(n - p));
+        if (best_c < 0 || c < best_c) {
+            best_c = c;
+            best_p = p;
+        }
+    }
+    return best_p;
 }
 int route_prefix_depth(int n) { return prefix_depth(n); }
+
+__constant__ uint32_t c_fact[13] = {1u, 1u, 2u, 6u, 24u, 120u, 720u, 5040u, 40320u, 362880u, 3628800u,
+                                    39916800u, 479001600u};
 
 // Lehmer decode of rank r over n elements into nibble-packed positions.
 __device__ inline uint64_t unrank_nib(int64_t r, int n) {
@@ -82,10 +95,27 @@ __device__ inline uint64_t unrank_nib(int64_t r, int n) {
 __device__ inline int nib(uint64_t v, int k) { return (int)((v >> (4 * k)) & 0xf); }
 
 // ---------------------------------------------------------- trie walk --
+// Leaves are visited in lexicographic order, so within a lane ranks only
+// grow and a strict "<" on the cost key keeps the smallest rank (O5).
+struct Best {
+    uint32_t key;
+    uint32_t rank;
+};
+
+template <class C>
+__device__ __forceinline__ void leaf(uint32_t cost, Best &best, uint32_t &rank) {
+    const uint32_t k = C::key(cost);
+    if (k < best.key) {
+        best.key = k;
+        best.rank = rank;
+    }
+    ++rank;
+}
+
 template <class C, int L>
 struct Dfs {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
-                                               uint64_t &best, uint32_t &rank) {
+                                               Best &best, uint32_t &rank) {
         uint32_t rem = unused;
         while (rem) {
             const int x = __ffs(rem) - 1;
@@ -95,20 +125,30 @@ struct Dfs {
     }
 };
 template <class C>
-struct Dfs<C, 0> {
-    __device__ __forceinline__ static void run(const uint32_t *, int, uint32_t, int, uint32_t cost, uint64_t &best,
-                                               uint32_t &rank) {
-        const uint64_t k = ((uint64_t)C::key(cost) << 32) | rank;
-        best = k < best ? k : best;
-        ++rank;
+struct Dfs<C, 2> {   // two stops left, a < b: leaves (a, b) then (b, a)
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+                                               Best &best, uint32_t &rank) {
+        const int a = __ffs(unused) - 1;
+        const int b = __ffs(unused & (unused - 1)) - 1;
+        const uint32_t cab = C::add(C::add(cost, Ds[prev * n + a]), Ds[a * n + b]);
+        const uint32_t cba = C::add(C::add(cost, Ds[prev * n + b]), Ds[b * n + a]);
+        leaf<C>(cab, best, rank);
+        leaf<C>(cba, best, rank);
+    }
+};
+template <class C>
+struct Dfs<C, 1> {
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+                                               Best &best, uint32_t &rank) {
+        const int a = __ffs(unused) - 1;
+        leaf<C>(C::add(cost, Ds[prev * n + a]), best, rank);
     }
 };
 
 template <class C>
-__device__ void walk_subtree(int L, const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
-                             uint64_t &best, uint32_t &rank) {
+__device__ __forceinline__ void walk_subtree(int L, const uint32_t *Ds, int n, uint32_t unused, int prev,
+                                             uint32_t cost, Best &best, uint32_t &rank) {
     switch (L) {
-        case 0: Dfs<C, 0>::run(Ds, n, unused, prev, cost, best, rank); break;
         case 1: Dfs<C, 1>::run(Ds, n, unused, prev, cost, best, rank); break;
         case 2: Dfs<C, 2>::run(Ds, n, unused, prev, cost, best, rank); break;
         case 3: Dfs<C, 3>::run(Ds, n, unused, prev, cost, best, rank); break;
@@ -142,20 +182,21 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
     __syncwarp();
     const int p = prefix_depth(n);
     const int L = n - p;
-    const uint32_t sub = (uint32_t)fact(L);
-    uint64_t best = ~0ull;
+    const uint32_t sub = c_fact[L];
+    const uint32_t div0 = c_fact[n - 1] / sub;   // prefixes per first-element choice
+    Best best{0xffffffffu, 0xffffffffu};
     for (int q = item.prefix_lo + lane; q < item.prefix_hi; q += 32) {
         // decode prefix q (mixed radix n, n-1, ..., n-p+1), lexicographic
         uint32_t unused = (1u << n) - 1u;
-        int rem = q, prev = -1;
+        uint32_t rem = (uint32_t)q, div = div0;
+        int prev = -1;
         uint32_t cost = 0;
-        int64_t div = fact(n - 1) / fact(L);   // prefixes per first-element choice
         for (int k = 0; k < p; ++k) {
-            const int digit = (int)(rem / div);
-            rem = (int)(rem % div);
-            if (k + 1 < p) div /= (n - 1 - k);
+            const uint32_t digit = rem / div;
+            rem -= digit * div;
+            if (k + 1 < p) div /= (uint32_t)(n - 1 - k);
             uint32_t m = unused;
-            for (int t = 0; t < digit; ++t) m &= m - 1;
+            for (uint32_t t = 0; t < digit; ++t) m &= m - 1;
             const int x = __ffs(m) - 1;
             unused &= ~(1u << x);
             if (prev >= 0) cost = C::add(cost, Ds[prev * n + x]);
@@ -164,12 +205,13 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
         uint32_t rank = (uint32_t)q * sub;
         walk_subtree<C>(L, Ds, n, unused, prev, cost, best, rank);
     }
+    uint64_t packed = ((uint64_t)best.key << 32) | best.rank;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
-        best = y < best ? y : best;
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, packed, o);
+        packed = y < packed ? y : packed;
     }
-    if (lane == 0) item_best[it] = best;
+    if (lane == 0) item_best[it] = packed;
 }
 
 __global__ void problem_reduce_kernel(const RouteProblem *probs, int nprob, const uint64_t *item_best,

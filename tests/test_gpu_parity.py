@@ -227,12 +227,13 @@ def test_route_orders_edge_cases():
     g = gen.config(2)[0]
     G = wr.Graph.from_gen(g)
     # empty order, single stop, duplicate lines, 17 distinct stops (too large)
-    nodes = [5, 5, 5, 7, 7] + list(range(20, 37))
+    nodes = [5, 5, 5, 9, 7] + list(range(20, 37))
     ptr = np.array([0, 0, 3, 5, 5 + 17], np.int64)
     res, _ = wr.route_orders(G, ptr, np.array(nodes, np.int32))
     assert res["n"][:3].tolist() == [0, 1, 2]
     assert res["status"].tolist() == [0, 0, 0, wr.WR_ETOOLARGE]
     assert res["cost_bits"][1] == 0 and res["seq"][1][0] == 5
+    assert sorted(res["seq"][2][:2].tolist()) == [7, 9] and res["seq"][3][0] == -1
     # unreachable stops: two components
     g2 = G_disconnected()
     G2 = wr.Graph(g2.V, g2.src, g2.dst, g2.w)
