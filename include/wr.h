@@ -60,6 +60,9 @@ typedef int32_t wr_status;
 
 const char *wr_last_error(void);
 int32_t wr_version(void);
+/* Device work memory comes from a per-device stream-ordered pool that keeps
+ * freed blocks for the next call; this returns the idle part to the driver. */
+wr_status wr_release_cached(int32_t device);
 
 /* ---------------------------------------------------------------- graphs -- */
 /* a1 Graph ingest (P721 §4.7: "edge-list format using integer arrays u, v,
@@ -71,8 +74,11 @@ int32_t wr_version(void);
  *   format   WR_COO (src, dst used) or WR_CSR (row_ptr, col used)
  *   w        E weights of wtype, in arc order (COO order, or CSR order)
  *   xy       optional V x 2 int32 planar coordinates (|x|,|y| < 2^20) used
- *            by the default segment plan (O8); NULL = none
+ *            by the default segment plan (O8) and to group nearby sources
+ *            into Bellman-Ford tiles; NULL = none
  *   device   CUDA device ordinal
+ *   z        optional V int32 rack level (|z| < 2^20), used with xy for the
+ *            source tiling only; NULL = none
  * Validation: indices in [0, V); fp32 weights finite and >= 0 (-0.0 is
  * stored as +0.0); int32 weights any sign but (V-1) * max|w| < INT32_MAX
  * (else WR_EOVERFLOW). The device copy is a CSC (in-arcs sorted by (v,u))
@@ -89,6 +95,7 @@ typedef struct {
     const void *w;
     const int32_t *xy;
     int32_t device;
+    const int32_t *z;
 } wr_graph_desc;
 
 typedef struct wr_graph wr_graph;

@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-from . import build as _build
+
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libwr.so")
@@ -30,6 +30,7 @@ EXPORTS = [
     "wr_last_error", "wr_version", "wr_graph_load", "wr_graph_free", "wr_graph_info", "wr_bf_batch",
     "wr_route_cost", "wr_route_segmented", "wr_route_orders", "wr_segment_plan", "wr_route_count_reduction",
     "wr_orders_plan", "wr_plan_info", "wr_orders_local", "wr_orders_finish", "wr_plan_free", "wr_shard_range",
+    "wr_release_cached",
 ]
 
 
@@ -42,7 +43,7 @@ class WrError(RuntimeError):
 class GraphDesc(C.Structure):
     _fields_ = [("V", C.c_int32), ("E", C.c_int64), ("wtype", C.c_int32), ("format", C.c_int32),
                 ("src", C.c_void_p), ("dst", C.c_void_p), ("row_ptr", C.c_void_p), ("col", C.c_void_p),
-                ("w", C.c_void_p), ("xy", C.c_void_p), ("device", C.c_int32)]
+                ("w", C.c_void_p), ("xy", C.c_void_p), ("device", C.c_int32), ("z", C.c_void_p)]
 
 
 class GraphInfo(C.Structure):
@@ -110,7 +111,8 @@ def _load():
     lib.wr_plan_free.argtypes = [vp]
     lib.wr_shard_range.argtypes = [i64, i32, i32, P(i64), P(i64)]
     lib.wr_shard_range.restype = None
-    for name in ["wr_graph_load", "wr_graph_free", "wr_graph_info", "wr_bf_batch", "wr_route_cost",
+    lib.wr_release_cached.argtypes = [i32]
+    for name in ["wr_release_cached", "wr_graph_load", "wr_graph_free", "wr_graph_info", "wr_bf_batch", "wr_route_cost",
                  "wr_route_segmented", "wr_route_orders", "wr_segment_plan", "wr_route_count_reduction",
                  "wr_orders_plan", "wr_plan_info", "wr_orders_local", "wr_orders_finish", "wr_plan_free"]:
         getattr(lib, name).restype = i32
@@ -153,6 +155,11 @@ def _stream_ptr(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
+def release_cached(device: int = 0):
+    """Return libwr's idle pooled device memory to the driver."""
+    _check(lib.wr_release_cached(device))
+
+
 def shard_range(n: int, rank: int, world: int):
     lo, hi = C.c_int64(0), C.c_int64(0)
     lib.wr_shard_range(n, rank, world, C.byref(lo), C.byref(hi))
@@ -162,7 +169,7 @@ def shard_range(n: int, rank: int, world: int):
 class Graph:
     """a1: a warehouse graph resident on one device (wr_graph)."""
 
-    def __init__(self, V, src=None, dst=None, w=None, xy=None, device=0, row_ptr=None, col=None):
+    def __init__(self, V, src=None, dst=None, w=None, xy=None, device=0, row_ptr=None, col=None, z=None):
         wdt = np.asarray(w).dtype if isinstance(w, np.ndarray) else None
         if wdt is None and hasattr(w, "dtype"):
             wdt = np.float32 if "float" in str(w.dtype) else np.int32
@@ -192,6 +199,10 @@ class Graph:
             xy = _arr(xy, np.int32)
             d.xy = _ptr(xy)
             self._keep.append(xy)
+        if z is not None:
+            z = _arr(z, np.int32)
+            d.z = _ptr(z)
+            self._keep.append(z)
         self._keep.append(w)
         h = C.c_void_p()
         _check(lib.wr_graph_load(C.byref(d), C.byref(h)))
@@ -203,7 +214,8 @@ class Graph:
 
     @classmethod
     def from_gen(cls, g, device=0, with_xy=True):
-        return cls(g.V, g.src, g.dst, g.w, xy=g.xy if with_xy else None, device=device)
+        return cls(g.V, g.src, g.dst, g.w, xy=g.xy if with_xy else None, device=device,
+                   z=g.z if with_xy else None)
 
     def info(self) -> GraphInfo:
         i = GraphInfo()

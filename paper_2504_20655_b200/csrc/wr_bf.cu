@@ -4,17 +4,19 @@
 // The paper's kernel (P720-724 §4.7) is edge-parallel, one thread per edge,
 // (V-1) rounds with a host sync per round, dist/pred V x N in global memory
 // with write contention. This design is B200-first instead:
-//   * sources are the SIMD lanes: a tile of 32 sources is one 128-byte row
-//     per vertex (rows[tile][v][lane]); every neighbour gather is one fully
-//     coalesced 128-B line and the graph arc (u, w) is loaded once per 32
-//     relaxations;
+//   * sources are the SIMD lanes: a tile of 32*SPL sources stores one
+//     128*SPL-byte row per vertex (rows[tile][v][slot]); lane l owns the SPL
+//     consecutive slots l*SPL.., so every neighbour gather is a fully
+//     coalesced vector load and each graph arc (u, w) is fetched once per
+//     32*SPL relaxations;
 //   * one CTA owns a tile and iterates its rounds alone (no grid sync, no
 //     host sync per round - the paper's 10.3 us/round), tiles are claimed
 //     from a persistent work counter;
 //   * frontier pull: a round relaxes only vertices with an in-neighbour that
-//     changed in the previous round (bitmaps in shared memory, expanded over
-//     the CSR out-arcs); the change mask of a vertex is one __any_sync vote;
-//   * atomic-free commit: each (v, lane) has exactly one writer (the warp
+//     improved in the previous round (two V-bit bitmaps in shared memory);
+//     the improvement of a vertex is one __any_sync vote, and the improving
+//     warp marks its out-neighbours for the next round lane-parallel;
+//   * atomic-free commit: each (v, slot) has exactly one writer (the warp
 //     that owns v's candidate word), updates are in place (chaotic /
 //     Gauss-Seidel), which reaches the same unique fixpoint (reading O2:
 //     the relaxation operator is monotone and deflationary for w >= 0, and
@@ -22,6 +24,7 @@
 //   * pred is not written inside the racy sweep: a4 recomputes the
 //     canonical predecessor from the converged dist (O3), deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -30,8 +33,7 @@
 
 namespace wr {
 
-constexpr int TS = 32;          // sources per tile (lanes)
-constexpr int BF_THREADS = 512; // 16 warps per CTA
+constexpr uint32_t FULL = 0xffffffffu;
 
 // ------------------------------------------------------------- weight ops --
 // Nonnegative int32: unsigned add + min (DPX VIADDMNMX). INF = INT32_MAX, and
@@ -82,6 +84,52 @@ struct OpI32N {
     }
 };
 
+// --------------------------------------------------- per-lane row vectors --
+template <int SPL>
+struct Vec {
+    uint32_t x[SPL];
+};
+template <int SPL>
+__device__ __forceinline__ Vec<SPL> vload(const uint32_t *p) {
+    Vec<SPL> r;
+    if constexpr (SPL == 1) {
+        r.x[0] = *p;
+    } else if constexpr (SPL == 2) {
+        const uint2 t = *reinterpret_cast<const uint2 *>(p);
+        r.x[0] = t.x;
+        r.x[1] = t.y;
+    } else {
+        const uint4 t = *reinterpret_cast<const uint4 *>(p);
+        r.x[0] = t.x;
+        r.x[1] = t.y;
+        r.x[2] = t.z;
+        r.x[3] = t.w;
+    }
+    return r;
+}
+template <int SPL>
+__device__ __forceinline__ void vstore(uint32_t *p, const Vec<SPL> &v) {
+    if constexpr (SPL == 1) {
+        *p = v.x[0];
+    } else if constexpr (SPL == 2) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(v.x[0], v.x[1]);
+    } else {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(v.x[0], v.x[1], v.x[2], v.x[3]);
+    }
+}
+template <class Op, int SPL>
+__device__ __forceinline__ void vrelax(Vec<SPL> &d, const Vec<SPL> &x, uint32_t w) {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) d.x[j] = Op::relax(d.x[j], x.x[j], w);
+}
+template <class Op, int SPL>
+__device__ __forceinline__ bool vless(const Vec<SPL> &a, const Vec<SPL> &b) {
+    bool r = false;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) r |= Op::less(a.x[j], b.x[j]);
+    return r;
+}
+
 // ------------------------------------------------------------ tile setup --
 __global__ void make_tiles_kernel(const int *sources, int64_t lo, int64_t hi, int *tile_src, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -89,9 +137,9 @@ __global__ void make_tiles_kernel(const int *sources, int64_t lo, int64_t hi, in
     tile_src[i] = (lo + i < hi) ? sources[lo + i] : -1;
 }
 
-void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int *d_tile_src, cudaStream_t st) {
-    const int64_t ntiles = (hi - lo + TS - 1) / TS;
-    const int64_t n = ntiles * TS;
+void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_tile_src, cudaStream_t st) {
+    const int64_t ntiles = (hi - lo + tsw - 1) / tsw;
+    const int64_t n = ntiles * tsw;
     if (n == 0) return;
     make_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_sources, lo, hi, d_tile_src, n);
     count_launch();
@@ -99,12 +147,12 @@ void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int *d_tile_src, c
 }
 
 // ---------------------------------------------------- relaxing one word --
-constexpr uint32_t FULL = 0xffffffffu;
-
-// Pull over all in-arcs of v for the 32 lanes (generic degree).
-template <class Op>
-__device__ __forceinline__ uint32_t relax_vertex(const DevGraph &g, const uint32_t *__restrict__ R, int a0, int a1,
-                                                 int lane, uint32_t d) {
+// Pull over all in-arcs of one vertex (generic degree). Rl = this lane's
+// first slot of the tile; rows are TSW = 32*SPL words.
+template <class Op, int SPL>
+__device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32_t *__restrict__ Rl, int a0, int a1,
+                                                 int lane, Vec<SPL> d) {
+    constexpr int TSW = 32 * SPL;
     for (int base = a0; base < a1; base += 32) {
         const int cnt = min(32, a1 - base);
         int my_u = 0;
@@ -114,42 +162,54 @@ __device__ __forceinline__ uint32_t relax_vertex(const DevGraph &g, const uint32
             my_w = g.in_w[base + lane];
         }
         int k = 0;
-        for (; k + 4 <= cnt; k += 4) {
+        for (; k + 2 <= cnt; k += 2) {
             const int u0 = __shfl_sync(FULL, my_u, k), u1 = __shfl_sync(FULL, my_u, k + 1);
-            const int u2 = __shfl_sync(FULL, my_u, k + 2), u3 = __shfl_sync(FULL, my_u, k + 3);
             const uint32_t w0 = __shfl_sync(FULL, my_w, k), w1 = __shfl_sync(FULL, my_w, k + 1);
-            const uint32_t w2 = __shfl_sync(FULL, my_w, k + 2), w3 = __shfl_sync(FULL, my_w, k + 3);
-            const uint32_t x0 = R[(size_t)u0 * TS + lane], x1 = R[(size_t)u1 * TS + lane];
-            const uint32_t x2 = R[(size_t)u2 * TS + lane], x3 = R[(size_t)u3 * TS + lane];
-            d = Op::relax(d, x0, w0);
-            d = Op::relax(d, x1, w1);
-            d = Op::relax(d, x2, w2);
-            d = Op::relax(d, x3, w3);
+            const Vec<SPL> x0 = vload<SPL>(Rl + (size_t)u0 * TSW), x1 = vload<SPL>(Rl + (size_t)u1 * TSW);
+            vrelax<Op, SPL>(d, x0, w0);
+            vrelax<Op, SPL>(d, x1, w1);
         }
         for (; k < cnt; ++k) {
             const int u = __shfl_sync(FULL, my_u, k);
             const uint32_t wk = __shfl_sync(FULL, my_w, k);
-            d = Op::relax(d, R[(size_t)u * TS + lane], wk);
+            vrelax<Op, SPL>(d, vload<SPL>(Rl + (size_t)u * TSW), wk);
         }
     }
     return d;
 }
 
-// Relaxes the candidate vertices (bits of m) of word w for all 32 lanes.
-// The word's CSC offsets are read with one coalesced load; two candidates
-// are processed per iteration (lanes 0-15 hold the first one's arcs, 16-31
-// the second's) so four independent 128-B row gathers are in flight.
-// Returns the word's change mask (one __any_sync vote per vertex).
-template <class Op>
-__device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
-                                               int lane, unsigned long long &relax) {
+template <bool MARK>
+__device__ __forceinline__ void mark_out(const DevGraph &g, int q_lo, int q_hi, int b, int lane, uint32_t *nxt) {
+    const int o0 = __shfl_sync(FULL, q_lo, b), o1 = __shfl_sync(FULL, q_hi, b);
+    for (int e = o0 + lane; e < o1; e += 32) {
+        const int x = g.out_dst[e];
+        atomicOr(&nxt[x >> 5], 1u << (x & 31));
+    }
+}
+
+// Relaxes the candidate vertices (bits of m) of word w for every slot.
+// The word's CSC/CSR offsets are read with one coalesced load each; two
+// candidates are processed per iteration (lanes 0-15 hold the first one's
+// in-arcs, 16-31 the second's) so four independent row gathers are in
+// flight. A vertex that improved for any slot (one __any_sync vote) marks its
+// out-neighbours in the next round's candidate bitmap, lane-parallel over its
+// out-arcs (shared-memory atomicOr; OR is order-independent).
+template <class Op, bool MARK, int SPL>
+__device__ __forceinline__ bool relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m, int lane,
+                                           unsigned long long &relax, uint32_t *nxt) {
+    constexpr int TSW = 32 * SPL;
     const int vl = (w << 5) + lane;
-    int p_lo = 0, p_hi = 0;
+    int p_lo = 0, p_hi = 0, q_lo = 0, q_hi = 0;
     if (vl < g.V) {
         p_lo = g.in_ptr[vl];
         p_hi = g.in_ptr[vl + 1];
+        if (MARK) {
+            q_lo = g.out_ptr[vl];
+            q_hi = g.out_ptr[vl + 1];
+        }
     }
-    uint32_t chg = 0;
+    uint32_t *Rl = R + lane * SPL;           // this lane's slots of the tile
+    bool any = false;
     while (m) {
         const int b0 = __ffs(m) - 1;
         m &= m - 1;
@@ -163,9 +223,10 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         const int a00 = __shfl_sync(FULL, p_lo, b0), a01 = __shfl_sync(FULL, p_hi, b0);
         const int a10 = __shfl_sync(FULL, p_lo, b1), a11 = __shfl_sync(FULL, p_hi, b1);
         const int n0 = a01 - a00, n1 = two ? a11 - a10 : 0;
-        const uint32_t e0 = R[(size_t)v0 * TS + lane];
-        const uint32_t e1 = two ? R[(size_t)v1 * TS + lane] : 0u;
-        uint32_t d0 = e0, d1 = e1;
+        const Vec<SPL> e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
+        Vec<SPL> e1 = e0;
+        if (two) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
+        Vec<SPL> d0 = e0, d1 = e1;
         if (n0 <= 16 && n1 <= 16) {
             const int sub = lane & 15;
             const int base = lane < 16 ? a00 : a10;
@@ -182,48 +243,52 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
                 const int u10 = __shfl_sync(FULL, my_u, 16 + k), u11 = __shfl_sync(FULL, my_u, 17 + k);
                 const uint32_t w00 = __shfl_sync(FULL, my_w, k), w01 = __shfl_sync(FULL, my_w, k + 1);
                 const uint32_t w10 = __shfl_sync(FULL, my_w, 16 + k), w11 = __shfl_sync(FULL, my_w, 17 + k);
-                const uint32_t x00 = k < n0 ? R[(size_t)u00 * TS + lane] : 0u;
-                const uint32_t x01 = k + 1 < n0 ? R[(size_t)u01 * TS + lane] : 0u;
-                const uint32_t x10 = k < n1 ? R[(size_t)u10 * TS + lane] : 0u;
-                const uint32_t x11 = k + 1 < n1 ? R[(size_t)u11 * TS + lane] : 0u;
-                if (k < n0) d0 = Op::relax(d0, x00, w00);
-                if (k + 1 < n0) d0 = Op::relax(d0, x01, w01);
-                if (k < n1) d1 = Op::relax(d1, x10, w10);
-                if (k + 1 < n1) d1 = Op::relax(d1, x11, w11);
+                Vec<SPL> x00, x01, x10, x11;
+                if (k < n0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
+                if (k + 1 < n0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
+                if (k < n1) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
+                if (k + 1 < n1) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
+                if (k < n0) vrelax<Op, SPL>(d0, x00, w00);
+                if (k + 1 < n0) vrelax<Op, SPL>(d0, x01, w01);
+                if (k < n1) vrelax<Op, SPL>(d1, x10, w10);
+                if (k + 1 < n1) vrelax<Op, SPL>(d1, x11, w11);
             }
         } else {
-            d0 = relax_vertex<Op>(g, R, a00, a01, lane, d0);
-            if (two) d1 = relax_vertex<Op>(g, R, a10, a11, lane, d1);
+            d0 = relax_vertex<Op, SPL>(g, Rl, a00, a01, lane, d0);
+            if (two) d1 = relax_vertex<Op, SPL>(g, Rl, a10, a11, lane, d1);
         }
         relax += (unsigned long long)(n0 + n1);
-        const bool c0 = Op::less(d0, e0);
-        if (c0) R[(size_t)v0 * TS + lane] = d0;
-        if (__any_sync(FULL, c0)) chg |= 1u << b0;
-        if (two) {
-            const bool c1 = Op::less(d1, e1);
-            if (c1) R[(size_t)v1 * TS + lane] = d1;
-            if (__any_sync(FULL, c1)) chg |= 1u << b1;
+        const bool c0 = vless<Op, SPL>(d0, e0);
+        if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
+        const bool c1 = two && vless<Op, SPL>(d1, e1);
+        if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
+        const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
+        any |= any0 | any1;
+        if (MARK) {
+            if (any0) mark_out<MARK>(g, q_lo, q_hi, b0, lane, nxt);
+            if (any1) mark_out<MARK>(g, q_lo, q_hi, b1, lane, nxt);
         }
     }
-    return chg;
+    return any;
 }
 
 // ------------------------------------------------------ the sweep kernel --
-// One CTA per tile at a time. Shared memory: two V-bit bitmaps
-// (changed = vertices improved last round, cand = their out-neighbours).
-template <class Op, bool DENSE>
-__global__ void __launch_bounds__(BF_THREADS) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
-                                                                 int ntiles, uint32_t *__restrict__ rows,
-                                                                 int *tile_counter, int max_rounds,
-                                                                 BfTileStats *stats) {
+// One CTA per tile at a time. Shared memory: two V-bit candidate bitmaps,
+// cur (relaxed this round) and nxt (out-neighbours of this round's
+// improvements), swapped after each round's barrier. Dense variant: every
+// vertex is a candidate every round (the paper's edge-parallel class).
+template <class Op, bool DENSE, int NT, int MINB, int SPL>
+__global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
+                                                               int ntiles, uint32_t *__restrict__ rows,
+                                                               int *tile_counter, int max_rounds,
+                                                               BfTileStats *stats) {
+    constexpr int TSW = 32 * SPL;
     extern __shared__ uint32_t smem[];
     const int V = g.V;
     const int NW = (V + 31) >> 5;
-    uint32_t *changed = smem;
-    uint32_t *cand = smem + NW;
     __shared__ int s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NWARPS = BF_THREADS / 32;
+    constexpr int NWARPS = NT / 32;
     const uint32_t last_mask = (V & 31) ? ((1u << (V & 31)) - 1u) : 0xffffffffu;
 
     for (;;) {
@@ -231,25 +296,30 @@ __global__ void __launch_bounds__(BF_THREADS) bf_frontier_kernel(DevGraph g, con
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
-        uint32_t *R = rows + (size_t)tile * V * TS;
+        uint32_t *R = rows + (size_t)tile * V * TSW;
+        uint32_t *cur = smem, *nxt = smem + NW;
 
         // init: every row INF, bitmaps empty
         {
             uint4 inf4 = make_uint4(Op::INF, Op::INF, Op::INF, Op::INF);
             uint4 *R4 = reinterpret_cast<uint4 *>(R);
-            const size_t n4 = (size_t)V * (TS / 4);
-            for (size_t i = threadIdx.x; i < n4; i += BF_THREADS) R4[i] = inf4;
-            for (int w = threadIdx.x; w < NW; w += BF_THREADS) {
-                changed[w] = 0u;
-                cand[w] = 0u;
-            }
+            const size_t n4 = (size_t)V * (TSW / 4);
+            for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
+            for (int w = threadIdx.x; w < 2 * NW; w += NT) smem[w] = 0u;
         }
         __syncthreads();
-        if (warp == 0) {
-            const int s = tile_src[tile * TS + lane];
-            if (s >= 0) {
-                R[(size_t)s * TS + lane] = Op::ZERO;
-                atomicOr(&changed[s >> 5], 1u << (s & 31));
+        if (warp == 0) {   // seed: d[s][slot] = 0, candidates = out-neighbours of the sources
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                const int slot = lane * SPL + j;
+                const int s = tile_src[tile * TSW + slot];
+                if (s >= 0) {
+                    R[(size_t)s * TSW + slot] = Op::ZERO;
+                    for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
+                        const int x = g.out_dst[e];
+                        atomicOr(&cur[x >> 5], 1u << (x & 31));
+                    }
+                }
             }
         }
         __syncthreads();
@@ -258,54 +328,67 @@ __global__ void __launch_bounds__(BF_THREADS) bf_frontier_kernel(DevGraph g, con
         unsigned long long relax = 0;
         bool more = true;
         while (more) {
-            // ---- expand: cand = out-neighbours of changed (dense: all)
             if (DENSE) {
-                for (int w = threadIdx.x; w < NW; w += BF_THREADS) {
-                    cand[w] = (w == NW - 1) ? last_mask : 0xffffffffu;
-                    changed[w] = 0u;
-                }
-            } else {
-                for (int w = threadIdx.x; w < NW; w += BF_THREADS) {
-                    uint32_t m = changed[w];
-                    if (!m) continue;
-                    changed[w] = 0u;
-                    while (m) {
-                        const int b = __ffs(m) - 1;
-                        m &= m - 1;
-                        const int u = (w << 5) + b;
-                        const int e1 = g.out_ptr[u + 1];
-                        for (int e = g.out_ptr[u]; e < e1; ++e) {
-                            const int x = g.out_dst[e];
-                            atomicOr(&cand[x >> 5], 1u << (x & 31));
-                        }
-                    }
-                }
+                for (int w = threadIdx.x; w < NW; w += NT) cur[w] = (w == NW - 1) ? last_mask : 0xffffffffu;
+                __syncthreads();
             }
-            __syncthreads();
-            // ---- relax: warp per candidate word, lane = source
+            // ---- relax: warp per candidate word, lane = SPL source slots
             int any = 0;
             for (int w = warp; w < NW; w += NWARPS) {
-                uint32_t m = cand[w];
+                const uint32_t m = cur[w];
                 if (!m) continue;
                 __syncwarp();
-                if (lane == 0) cand[w] = 0u;
-                const uint32_t chg = relax_word<Op>(g, R, w, m, lane, relax);
-                if (chg) {
-                    if (lane == 0) changed[w] = chg;
-                    any = 1;
-                }
+                if (lane == 0) cur[w] = 0u;
+                any |= relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, nxt);
             }
             ++rounds;
             more = __syncthreads_or(any) != 0;
+            uint32_t *t = cur;
+            cur = nxt;
+            nxt = t;
             if (more && rounds >= max_rounds) {
                 if (threadIdx.x == 0) atomicMax(&stats->negcycle_tile, tile);
                 more = false;
             }
         }
         // per-tile statistics (one lane per warp contributes its arc count)
-        if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TS);
+        if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TSW);
         if (threadIdx.x == 0) atomicMax(&stats->rounds_max, rounds);
         __syncthreads();
+    }
+}
+
+// Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
+// WR_BF_CONFIG selects one (tuning knob; default measured best).
+template <class Op, bool DENSE, int NT, int MINB, int SPL>
+static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
+    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL>;
+    WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, nsm = 0;
+    WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    per_sm = std::max(per_sm, 1);
+    const int grid = (int)std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
+    DBuf<int> counter(1);
+    WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+    kern<<<grid, NT, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p, run.max_rounds, d_stats);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <class Op, bool DENSE, int SPL>
+static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
+    static const int cfg = env_int("WR_BF_CONFIG", 0);
+    switch (cfg) {
+        case 1: launch_shape<Op, DENSE, 512, 3, SPL>(g, run, d_stats, st, smem); break;
+        case 2: launch_shape<Op, DENSE, 256, 4, SPL>(g, run, d_stats, st, smem); break;
+        default: launch_shape<Op, DENSE, 512, 2, SPL>(g, run, d_stats, st, smem); break;
     }
 }
 
@@ -314,25 +397,25 @@ static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     const int V = g->V;
     const int NW = (V + 31) / 32;
     const size_t smem = (size_t)2 * NW * sizeof(uint32_t);
-    int dev = g->device;
     int max_optin = 0;
-    WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem + 1024 > (size_t)max_optin)
         WR_THROW(WR_ETOOLARGE, "bf: V too large for the shared-memory frontier bitmaps");
-    auto kern = run.variant == WR_BF_DENSE ? bf_frontier_kernel<Op, true> : bf_frontier_kernel<Op, false>;
-    WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0, nsm = 0;
-    WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BF_THREADS, smem));
-    WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    per_sm = std::max(per_sm, 1);
-    const int grid = std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
-    DBuf<int> counter(1);
-    WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
-    kern<<<grid, BF_THREADS, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p,
-                                         run.max_rounds, d_stats);
-    count_launch();
-    WR_LAUNCH_CHECK();
-    WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
+    const bool dense = run.variant == WR_BF_DENSE;
+    switch (run.spl) {
+        case 4:
+            if (dense) launch_dispatch<Op, true, 4>(g, run, d_stats, st, smem);
+            else launch_dispatch<Op, false, 4>(g, run, d_stats, st, smem);
+            break;
+        case 2:
+            if (dense) launch_dispatch<Op, true, 2>(g, run, d_stats, st, smem);
+            else launch_dispatch<Op, false, 2>(g, run, d_stats, st, smem);
+            break;
+        default:
+            if (dense) launch_dispatch<Op, true, 1>(g, run, d_stats, st, smem);
+            else launch_dispatch<Op, false, 1>(g, run, d_stats, st, smem);
+            break;
+    }
 }
 
 void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
@@ -342,39 +425,54 @@ void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStrea
     else launch_sweep<OpU32>(g, run, d_stats, st);
 }
 
+// Sources per lane for S sources: as wide as possible while the tile count
+// still fills the GPU (>= 2 tiles per CTA slot); WR_BF_SPL forces a width.
+int choose_spl(int64_t S, int nsm) {
+    const int forced = env_int("WR_BF_SPL", 0);
+    if (forced == 1 || forced == 2 || forced == 4) return forced;
+    int spl = 4;
+    while (spl > 1 && S / (32 * spl) < (int64_t)4 * nsm) spl /= 2;
+    return spl;
+}
+
 // --------------------------------------------------- a4 + output layout --
-// Block = 8 warps; warp handles 32 consecutive output columns (vertices or
-// targets) of one tile: computes dist/pred for (column j, lane = source k),
-// stages them in shared memory and writes each source's 32 columns as one
-// coalesced 128-B segment of the caller's row-major S x T / S x V arrays.
-// Canonical pred (O3, w >= 0): smallest tail of a steep tight in-arc; a
-// reachable non-source vertex without one is "flat" and is resolved by
-// bf_resolve_flat. Graphs with a negative weight resolve every vertex there.
+// Block = 4 warps; a warp handles 32 consecutive output columns (vertices or
+// targets) of one 32-slot group of one tile: computes dist/pred for (column
+// j, slot = group*32 + lane), stages them in shared memory and writes each
+// source's 32 columns as one coalesced 128-B segment of the caller's
+// row-major S x T / S x V arrays. Canonical pred (O3, w >= 0): smallest tail
+// of a steep tight in-arc; a reachable non-source vertex without one is
+// "flat" and is resolved by bf_resolve_flat. Graphs with a negative weight
+// resolve every vertex there.
 constexpr int OUT_WARPS = 4;
 template <class Op>
 __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, const int *__restrict__ tile_src,
-                                                         int ntiles, const uint32_t *__restrict__ rows,
-                                                         int64_t out_row0, const int *__restrict__ targets,
-                                                         int T, uint32_t *dist_out, int32_t *pred_out,
-                                                         int *flat_tiles, int neg_graph) {
+                                                                    int ntiles, int tsw, const uint32_t *__restrict__ rows,
+                                                                    const int *__restrict__ slot_row,
+                                                                    int64_t out_row0, const int *__restrict__ targets,
+                                                                    int T, uint32_t *dist_out, int32_t *pred_out,
+                                                                    int *flat_tiles, int neg_graph) {
     __shared__ uint32_t sd[OUT_WARPS][32][33];
     __shared__ int32_t sp[OUT_WARPS][32][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int V = g.V;
     const int ncols = targets ? T : V;
     const int chunks = (ncols + 31) / 32;
+    const int groups = tsw / 32;
     const int64_t job = (int64_t)blockIdx.x * OUT_WARPS + warp;
-    if (job >= (int64_t)ntiles * chunks) return;
-    const int tile = (int)(job / chunks);
+    if (job >= (int64_t)ntiles * groups * chunks) return;
+    const int tg = (int)(job / chunks);        // tile * groups + group
+    const int tile = tg / groups, grp = tg % groups;
     const int c0 = (int)(job % chunks) * 32;
-    const uint32_t *R = rows + (size_t)tile * V * TS;
-    const int s = tile_src[tile * TS + lane];
+    const int slot = grp * 32 + lane;
+    const uint32_t *R = rows + (size_t)tile * V * tsw + grp * 32;
+    const int s = tile_src[tile * tsw + slot];
     bool flat = false;
     for (int j = 0; j < 32; ++j) {
         const int col = c0 + j;
         if (col >= ncols) break;
         const int v = targets ? targets[col] : col;
-        const uint32_t d = R[(size_t)v * TS + lane];
+        const uint32_t d = R[(size_t)v * tsw + lane];
         sd[warp][j][lane] = d;
         if (pred_out && !targets) {
             // lane-divergent predicate; the shuffles below stay warp-uniform
@@ -391,9 +489,9 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
                         my_w = g.in_w[base + lane];
                     }
                     for (int k = 0; k < cnt; ++k) {
-                        const int u = __shfl_sync(0xffffffffu, my_u, k);
-                        const uint32_t wk = __shfl_sync(0xffffffffu, my_w, k);
-                        const uint32_t du = R[(size_t)u * TS + lane];
+                        const int u = __shfl_sync(FULL, my_u, k);
+                        const uint32_t wk = __shfl_sync(FULL, my_w, k);
+                        const uint32_t du = R[(size_t)u * tsw + lane];
                         if (active && Op::tight(du, wk, d) && Op::less(du, d) && u < best) best = u;
                     }
                 }
@@ -407,74 +505,78 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
         }
     }
     __syncwarp();
-    // write out: for each source row k, columns c0..c0+31 (lane = column)
+    // write out: for each source slot k of the group, columns c0..c0+31
     const int col = c0 + lane;
-    for (int k = 0; k < TS; ++k) {
-        const int sk = tile_src[tile * TS + k];
-        if (sk < 0) break;                       // tiles are filled lane 0 first
-        const int64_t row = out_row0 + (int64_t)tile * TS + k;
+    for (int k = 0; k < 32; ++k) {
+        const int sk = tile_src[tile * tsw + grp * 32 + k];
+        if (sk < 0) break;                       // tiles are filled slot 0 first
+        const int64_t sl = (int64_t)tile * tsw + grp * 32 + k;
+        const int64_t row = out_row0 + (slot_row ? slot_row[sl] : sl);
         if (col < ncols) {
             if (dist_out) dist_out[row * ncols + col] = sd[warp][lane][k];
             if (pred_out && !targets) pred_out[row * (int64_t)V + col] = sp[warp][lane][k];
         }
     }
-    if (__any_sync(0xffffffffu, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
+    if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
-void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t, const int *targets,
-                      int T, void *dist_out, int32_t *pred_out, int *d_flat_tiles, cudaStream_t st) {
+void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t, const int *targets, int T,
+                      void *dist_out, int32_t *pred_out, int *d_flat_tiles, cudaStream_t st) {
     if (run.ntiles <= 0 || (!dist_out && !pred_out)) return;
+    const int tsw = 32 * run.spl;
     const int ncols = targets ? T : g->V;
-    const int64_t jobs = (int64_t)run.ntiles * ((ncols + 31) / 32);
+    const int64_t jobs = (int64_t)run.ntiles * run.spl * ((ncols + 31) / 32);
     const unsigned grid = (unsigned)((jobs + OUT_WARPS - 1) / OUT_WARPS);
     const int neg = g->has_negative;
     if (g->wtype == WR_F32)
-        bf_outputs_kernel<OpF32><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, out_row0,
-                                                       targets, T, (uint32_t *)dist_out, pred_out,
-                                                       d_flat_tiles, neg);
+        bf_outputs_kernel<OpF32><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, tsw, run.rows,
+                                                                  run.slot_row, out_row0, targets, T,
+                                                                  (uint32_t *)dist_out, pred_out, d_flat_tiles, neg);
     else if (neg)
-        bf_outputs_kernel<OpI32N><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, out_row0,
-                                                        targets, T, (uint32_t *)dist_out, pred_out,
-                                                        d_flat_tiles, neg);
+        bf_outputs_kernel<OpI32N><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, tsw, run.rows,
+                                                                   run.slot_row, out_row0, targets, T,
+                                                                   (uint32_t *)dist_out, pred_out, d_flat_tiles, neg);
     else
-        bf_outputs_kernel<OpU32><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, out_row0,
-                                                       targets, T, (uint32_t *)dist_out, pred_out,
-                                                       d_flat_tiles, neg);
+        bf_outputs_kernel<OpU32><<<grid, OUT_WARPS * 32, 0, st>>>(g->view(), run.tile_src, run.ntiles, tsw, run.rows,
+                                                                  run.slot_row, out_row0, targets, T,
+                                                                  (uint32_t *)dist_out, pred_out, d_flat_tiles, neg);
     count_launch();
     WR_LAUNCH_CHECK();
 }
 
 // --------------------------------------------- flat predecessors (rare) --
-// hop[v][k] = BFS layer of v over the tight arcs of source k (a min-plus
-// sweep with unit weights restricted to tight arcs), then for every flat
-// (v, k) - or every reachable vertex of a negative-weight graph -
+// For one 32-slot group of a tile: hop[v][lane] = BFS layer of v over the
+// tight arcs of that slot's source (a min-plus sweep with unit weights
+// restricted to tight arcs), then for every flat (v, slot) - or every
+// reachable vertex of a negative-weight graph -
 // pred = argmin over tight in-arcs of (hop[u], u)  (O3).
+constexpr int HOP_THREADS = 512;
 template <class Op>
-__global__ void __launch_bounds__(BF_THREADS) hop_bfs_kernel(DevGraph g, const int *__restrict__ tile_src,
-                                                             int tile, const uint32_t *__restrict__ rows,
-                                                             uint32_t *__restrict__ hop) {
+__global__ void __launch_bounds__(HOP_THREADS) hop_bfs_kernel(DevGraph g, const int *__restrict__ tile_src, int tile,
+                                                              int grp, int tsw, const uint32_t *__restrict__ rows,
+                                                              uint32_t *__restrict__ hop) {
     extern __shared__ uint32_t smem[];
     const int V = g.V;
     const int NW = (V + 31) >> 5;
     uint32_t *changed = smem;
     uint32_t *cand = smem + NW;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NWARPS = BF_THREADS / 32;
-    const uint32_t *R = rows + (size_t)tile * V * TS;
-    for (size_t i = threadIdx.x; i < (size_t)V * TS; i += BF_THREADS) hop[i] = 0xffffffffu;
-    for (int w = threadIdx.x; w < NW; w += BF_THREADS) changed[w] = cand[w] = 0u;
+    constexpr int NWARPS = HOP_THREADS / 32;
+    const uint32_t *R = rows + (size_t)tile * V * tsw + grp * 32;
+    for (size_t i = threadIdx.x; i < (size_t)V * 32; i += HOP_THREADS) hop[i] = 0xffffffffu;
+    for (int w = threadIdx.x; w < NW; w += HOP_THREADS) changed[w] = cand[w] = 0u;
     __syncthreads();
     if (warp == 0) {
-        const int s = tile_src[tile * TS + lane];
+        const int s = tile_src[tile * tsw + grp * 32 + lane];
         if (s >= 0) {
-            hop[(size_t)s * TS + lane] = 0;
+            hop[(size_t)s * 32 + lane] = 0;
             atomicOr(&changed[s >> 5], 1u << (s & 31));
         }
     }
     __syncthreads();
     bool more = true;
     while (more) {
-        for (int w = threadIdx.x; w < NW; w += BF_THREADS) {
+        for (int w = threadIdx.x; w < NW; w += HOP_THREADS) {
             uint32_t m = changed[w];
             if (!m) continue;
             changed[w] = 0u;
@@ -500,18 +602,18 @@ __global__ void __launch_bounds__(BF_THREADS) hop_bfs_kernel(DevGraph g, const i
                 const int b = __ffs(m) - 1;
                 m &= m - 1;
                 const int v = (w << 5) + b;
-                const uint32_t dv = R[(size_t)v * TS + lane];
-                const uint32_t h0 = hop[(size_t)v * TS + lane];
+                const uint32_t dv = R[(size_t)v * tsw + lane];
+                const uint32_t h0 = hop[(size_t)v * 32 + lane];
                 uint32_t h = h0;
                 for (int e = g.in_ptr[v]; e < g.in_ptr[v + 1]; ++e) {
                     const int u = g.in_src[e];
-                    const uint32_t hu = hop[(size_t)u * TS + lane];
-                    if (hu != 0xffffffffu && Op::tight(R[(size_t)u * TS + lane], g.in_w[e], dv) && hu + 1 < h)
+                    const uint32_t hu = hop[(size_t)u * 32 + lane];
+                    if (hu != 0xffffffffu && Op::tight(R[(size_t)u * tsw + lane], g.in_w[e], dv) && hu + 1 < h)
                         h = hu + 1;
                 }
                 const bool c = h < h0;
-                if (c) hop[(size_t)v * TS + lane] = h;
-                if (__any_sync(0xffffffffu, c)) chg |= 1u << b;
+                if (c) hop[(size_t)v * 32 + lane] = h;
+                if (__any_sync(FULL, c)) chg |= 1u << b;
             }
             if (chg) {
                 if (lane == 0) changed[w] = chg;
@@ -523,60 +625,64 @@ __global__ void __launch_bounds__(BF_THREADS) hop_bfs_kernel(DevGraph g, const i
 }
 
 template <class Op>
-__global__ void flat_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int tile,
+__global__ void flat_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int tile, int grp, int tsw,
                                  const uint32_t *__restrict__ rows, const uint32_t *__restrict__ hop,
-                                 int64_t out_row0, int32_t *pred_out, int neg_graph) {
+                                 const int *__restrict__ slot_row, int64_t out_row0, int32_t *pred_out,
+                                 int neg_graph) {
     const int lane = threadIdx.x & 31;
     const int v = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int V = g.V;
     if (v >= V) return;
-    const uint32_t *R = rows + (size_t)tile * V * TS;
-    const int s = tile_src[tile * TS + lane];
-    const uint32_t d = R[(size_t)v * TS + lane];
+    const uint32_t *R = rows + (size_t)tile * V * tsw + grp * 32;
+    const int slot = grp * 32 + lane;
+    const int s = tile_src[tile * tsw + slot];
+    const uint32_t d = R[(size_t)v * tsw + lane];
     if (s < 0 || v == s || !Op::finite(d)) return;
     bool steep = false;
     int best = -1;
     uint32_t best_h = 0xffffffffu;
     for (int e = g.in_ptr[v]; e < g.in_ptr[v + 1]; ++e) {
         const int u = g.in_src[e];
-        const uint32_t du = R[(size_t)u * TS + lane];
+        const uint32_t du = R[(size_t)u * tsw + lane];
         if (!Op::tight(du, g.in_w[e], d)) continue;
         if (Op::less(du, d)) steep = true;
-        const uint32_t hu = hop[(size_t)u * TS + lane];
+        const uint32_t hu = hop[(size_t)u * 32 + lane];
         if (hu < best_h || (hu == best_h && u < best)) {
             best_h = hu;
             best = u;
         }
     }
-    if (neg_graph || !steep) pred_out[(out_row0 + (int64_t)tile * TS + lane) * V + v] = best;
+    const int64_t sl = (int64_t)tile * tsw + slot;
+    if (neg_graph || !steep) pred_out[(out_row0 + (slot_row ? slot_row[sl] : sl)) * V + v] = best;
+}
+
+template <class Op>
+static void resolve_group(const wr_graph *g, const BfRun &run, int t, int grp, uint32_t *hop, size_t smem,
+                          int64_t out_row0, int32_t *pred_out, int neg, cudaStream_t st) {
+    const int V = g->V;
+    const int tsw = 32 * run.spl;
+    WR_CUDA(cudaFuncSetAttribute(hop_bfs_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    hop_bfs_kernel<Op><<<1, HOP_THREADS, smem, st>>>(g->view(), run.tile_src, t, grp, tsw, run.rows, hop);
+    flat_pred_kernel<Op><<<(V + 7) / 8, 256, 0, st>>>(g->view(), run.tile_src, t, grp, tsw, run.rows, hop,
+                                                     run.slot_row, out_row0,
+                                                     pred_out, neg);
+    count_launch();
+    count_launch();
+    WR_LAUNCH_CHECK();
 }
 
 void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles, int64_t out_row0,
                      int32_t *pred_out, cudaStream_t st) {
     if (tiles.empty() || !pred_out) return;
     const int V = g->V;
-    DBuf<uint32_t> hop((size_t)V * TS);
+    DBuf<uint32_t> hop((size_t)V * 32);
     const size_t smem = (size_t)2 * ((V + 31) / 32) * sizeof(uint32_t);
     for (int t : tiles) {
-        if (g->wtype == WR_F32) {
-            WR_CUDA(cudaFuncSetAttribute(hop_bfs_kernel<OpF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hop_bfs_kernel<OpF32><<<1, BF_THREADS, smem, st>>>(g->view(), run.tile_src, t, run.rows, hop.p);
-            flat_pred_kernel<OpF32><<<(V + 7) / 8, 256, 0, st>>>(g->view(), run.tile_src, t, run.rows, hop.p,
-                                                                 out_row0, pred_out, 0);
-        } else if (g->has_negative) {
-            WR_CUDA(cudaFuncSetAttribute(hop_bfs_kernel<OpI32N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hop_bfs_kernel<OpI32N><<<1, BF_THREADS, smem, st>>>(g->view(), run.tile_src, t, run.rows, hop.p);
-            flat_pred_kernel<OpI32N><<<(V + 7) / 8, 256, 0, st>>>(g->view(), run.tile_src, t, run.rows, hop.p,
-                                                                  out_row0, pred_out, 1);
-        } else {
-            WR_CUDA(cudaFuncSetAttribute(hop_bfs_kernel<OpU32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hop_bfs_kernel<OpU32><<<1, BF_THREADS, smem, st>>>(g->view(), run.tile_src, t, run.rows, hop.p);
-            flat_pred_kernel<OpU32><<<(V + 7) / 8, 256, 0, st>>>(g->view(), run.tile_src, t, run.rows, hop.p,
-                                                                 out_row0, pred_out, 0);
+        for (int grp = 0; grp < run.spl; ++grp) {
+            if (g->wtype == WR_F32) resolve_group<OpF32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, st);
+            else if (g->has_negative) resolve_group<OpI32N>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 1, st);
+            else resolve_group<OpU32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, st);
         }
-        count_launch();
-        count_launch();
-        WR_LAUNCH_CHECK();
     }
     WR_CUDA(cudaStreamSynchronize(st));
 }
@@ -585,17 +691,23 @@ void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int>
 int64_t budget_bytes(int64_t requested) {
     size_t free_b = 0, total_b = 0;
     WR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    int dev = 0;
+    WR_CUDA(cudaGetDevice(&dev));
+    free_b += pool_idle_bytes(dev);   // reserved by libwr's pool, reusable
     int64_t b = requested > 0 ? requested : (int64_t)180e9;
     return std::min<int64_t>(b, (int64_t)(0.9 * (double)free_b));
 }
 
-int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes, int64_t S) {
+// Sources per Bellman-Ford segment: the per-segment working set
+// (per_source_bytes each, plus fixed) stays within the budget; a multiple of
+// the tile width tsw.
+int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes, int64_t S, int tsw) {
     const int64_t room = budget - fixed_bytes;
-    if (room < per_source_bytes * TS)
-        WR_THROW(WR_ENOMEM, "scheduler: HBM budget below one 32-source tile");
+    if (room < per_source_bytes * tsw)
+        WR_THROW(WR_ENOMEM, "scheduler: HBM budget below one source tile");
     int64_t sb = room / per_source_bytes;
-    sb = (sb / TS) * TS;
-    return std::max<int64_t>(TS, std::min<int64_t>(sb, ((S + TS - 1) / TS) * TS));
+    sb = (sb / tsw) * tsw;
+    return std::max<int64_t>(tsw, std::min<int64_t>(sb, ((S + tsw - 1) / tsw) * tsw));
 }
 
 // ----------------------------------------------------- validation kernel --
@@ -629,11 +741,16 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     wr_bf_opts o{};
     if (opts) o = *opts;
     cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
     const int V = g->V;
     const int ncols = targets ? T : V;
     int max_rounds = o.max_rounds > 0 ? o.max_rounds : std::max(1, V - 1);
     if (!g->has_negative && o.max_rounds <= 0) max_rounds = V;  // no negative cycle possible
     const int variant = o.variant == WR_BF_DENSE ? WR_BF_DENSE : WR_BF_FRONTIER;
+    int nsm = 0;
+    WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    const int spl = choose_spl(S, nsm);
+    const int tsw = 32 * spl;
 
     cudaEvent_t e0, e1;
     WR_CUDA(cudaEventCreate(&e0));
@@ -657,11 +774,11 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     wr_graph_info_t gi;
     wr_graph_info(g, &gi);
     const int64_t budget = budget_bytes(o.hbm_budget);
-    const int64_t sb = sources_per_segment(budget, gi.device_bytes + (64 << 20), per_src, std::max(S, 1));
-    const int64_t max_tiles = sb / TS;
+    const int64_t sb = sources_per_segment(budget, gi.device_bytes + (64 << 20), per_src, std::max(S, 1), tsw);
+    const int64_t max_tiles = sb / tsw;
 
-    DBuf<uint32_t> rows((size_t)max_tiles * V * TS);
-    DBuf<int> tile_src(max_tiles * TS);
+    DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
+    DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
     DBuf<int> flat(max_tiles);
     DBuf<uint32_t> dist_stage;
     DBuf<int32_t> pred_stage;
@@ -675,16 +792,16 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     int64_t total_tiles = 0;
     for (int64_t lo = 0; lo < S; lo += sb) {
         const int64_t hi = std::min<int64_t>(S, lo + sb);
-        const int ntiles = (int)((hi - lo + TS - 1) / TS);
-        make_tiles(d_src.p, lo, hi, tile_src.p, st);
-        BfRun run{tile_src.p, ntiles, rows.p, variant, max_rounds};
+        const int ntiles = (int)((hi - lo + tsw - 1) / tsw);
+        make_tiles_ordered(g, d_src.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
+        BfRun run{tile_src.p, ntiles, rows.p, variant, max_rounds, spl, slot_row.p};
         bf_run(g, run, d_stats.p, st);
         BfTileStats hs;
         WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
         WR_CUDA(cudaStreamSynchronize(st));
         if (hs.negcycle_tile >= 0) {
             int s_bad = -1;
-            WR_CUDA(cudaMemcpy(&s_bad, tile_src.p + hs.negcycle_tile * TS, 4, cudaMemcpyDeviceToHost));
+            WR_CUDA(cudaMemcpy(&s_bad, tile_src.p + (size_t)hs.negcycle_tile * tsw, 4, cudaMemcpyDeviceToHost));
             if (stats) stats->negcycle_source = s_bad;
             if (g->has_negative && o.max_rounds <= 0)
                 return fail(WR_ENEGCYCLE, "wr_bf_batch: negative cycle reachable from a source");
@@ -709,7 +826,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
             std::vector<int> todo;
             for (int t = 0; t < ntiles; ++t)
                 if (hflat[t] || g->has_negative) todo.push_back(t);
-            bf_resolve_flat(g, run, todo, pred_dev ? lo : 0, pout, st);
+            bf_resolve_flat(g, run, todo, row_p, pout, st);
         }
         if (dist && !dist_dev)
             WR_CUDA(cudaMemcpyAsync((char *)dist + (size_t)lo * ncols * 4, dist_stage.p,
@@ -723,8 +840,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     WR_CUDA(cudaEventRecord(e1, st));
     BfTileStats hs{};
     WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    if (!o.async || !dist_dev || (pred && !pred_dev)) WR_CUDA(cudaStreamSynchronize(st));
-    else WR_CUDA(cudaStreamSynchronize(st));  // stats/temporaries need the sync; async reserved
+    WR_CUDA(cudaStreamSynchronize(st));  // stats and temporaries need the sync (async is reserved)
     float ms = 0.f;
     WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);

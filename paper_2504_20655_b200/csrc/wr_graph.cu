@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 
 #include "wr_internal.cuh"
 
@@ -15,6 +16,58 @@ namespace wr {
 
 static thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+thread_local cudaStream_t g_stream = 0;
+
+// ----------------------------------------------------------- memory pool --
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64] = {};
+
+static cudaMemPool_t pool_for(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64) WR_THROW(WR_EINVAL, "device ordinal out of range");
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        WR_CUDA(cudaMemPoolCreate(&g_pools[dev], &props));
+        uint64_t thr = UINT64_MAX;
+        WR_CUDA(cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return g_pools[dev];
+}
+
+void *pool_alloc(size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    WR_CUDA(cudaGetDevice(&dev));
+    void *p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool_for(dev), s);
+    if (e == cudaErrorMemoryAllocation) {   // give idle pool memory back and retry once
+        cudaGetLastError();
+        WR_CUDA(cudaStreamSynchronize(s));
+        WR_CUDA(cudaMemPoolTrimTo(pool_for(dev), 0));
+        e = cudaMallocFromPoolAsync(&p, bytes, pool_for(dev), s);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error(std::string("device allocation of ") + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
+        throw CudaError{e == cudaErrorMemoryAllocation ? WR_ENOMEM : WR_ECUDA};
+    }
+    return p;
+}
+
+void pool_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+size_t pool_idle_bytes(int dev) {
+    cudaMemPool_t pool = pool_for(dev);
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return reserved > used ? (size_t)(reserved - used) : 0;
+}
 
 void set_error(const std::string &msg) { g_err = msg; }
 wr_status fail(wr_status code, const std::string &msg) {
@@ -160,6 +213,22 @@ __global__ void validate_xy_kernel(const int *xy, int V, int *flags) {
     if (x <= -(1 << 20) || x >= (1 << 20)) atomicOr(flags, BAD_XY);
 }
 
+// bbox = {xmin, xmax, ymin, ymax, zmin, zmax}; also validates |z| < 2^20.
+__global__ void bbox_kernel(const int *xy, const int *z, int V, int *bbox, int *flags) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    atomicMin(&bbox[0], xy[2 * v]);
+    atomicMax(&bbox[1], xy[2 * v]);
+    atomicMin(&bbox[2], xy[2 * v + 1]);
+    atomicMax(&bbox[3], xy[2 * v + 1]);
+    if (z) {
+        const int zz = z[v];
+        if (zz <= -(1 << 20) || zz >= (1 << 20)) atomicOr(flags, BAD_XY);
+        atomicMin(&bbox[4], zz);
+        atomicMax(&bbox[5], zz);
+    }
+}
+
 __global__ void narrow_kernel(const int64_t *a, int *b, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) b[i] = (int)a[i];
@@ -265,11 +334,23 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
         count_launch();
         WR_LAUNCH_CHECK();
     }
+    DBuf<int> bbox(6);
     if (d->xy) {
         g->xy = to_device<int>(d->xy, (size_t)V * 2, st);
         validate_xy_kernel<<<grid_for(2 * (int64_t)V, 256), 256, 0, st>>>(g->xy.p, V, flags.p);
         count_launch();
         WR_LAUNCH_CHECK();
+        if (d->z) g->z = to_device<int>(d->z, (size_t)V, st);
+        const int init[6] = {INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN, 0, 0};
+        WR_CUDA(cudaMemcpyAsync(bbox.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        if (d->z) {
+            const int zi[2] = {INT32_MAX, INT32_MIN};
+            WR_CUDA(cudaMemcpyAsync(bbox.p + 4, zi, sizeof(zi), cudaMemcpyHostToDevice, st));
+        }
+        bbox_kernel<<<grid_for(V, 256), 256, 0, st>>>(g->xy.p, g->z.p, V, bbox.p, flags.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+        WR_CUDA(cudaMemcpyAsync(g->bbox, bbox.p, sizeof(g->bbox), cudaMemcpyDeviceToHost, st));
     }
     int hf[3];
     WR_CUDA(cudaMemcpyAsync(hf, flags.p, 12, cudaMemcpyDeviceToHost, st));
@@ -320,6 +401,15 @@ extern "C" {
 
 const char *wr_last_error(void) { return wr::g_err.c_str(); }
 int32_t wr_version(void) { return 1; }
+
+wr_status wr_release_cached(int32_t device) {
+    return wr::guarded([&] {
+        WR_CUDA(cudaSetDevice(device));
+        WR_CUDA(cudaDeviceSynchronize());
+        WR_CUDA(cudaMemPoolTrimTo(wr::pool_for(device), 0));
+        return WR_OK;
+    });
+}
 
 wr_status wr_graph_load(const wr_graph_desc *desc, wr_graph **out) {
     return wr::guarded([&] { return wr::graph_load_impl(desc, out); });

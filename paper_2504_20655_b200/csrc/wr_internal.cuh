@@ -59,28 +59,48 @@ extern thread_local int64_t g_launches;
 inline void count_launch() { ++g_launches; }
 
 // --------------------------------------------------------- device memory --
+// Stream-ordered allocations from a per-device memory pool that keeps freed
+// blocks reserved (release threshold = max), so a steady stream of calls
+// (the bench, a serving loop) does not pay cudaMalloc/cudaFree of the
+// multi-GB Bellman-Ford working set on every call. Each API entry point sets
+// the calling thread's stream (StreamScope); buffers are allocated and freed
+// in that stream's order.
+extern thread_local cudaStream_t g_stream;
+void *pool_alloc(size_t bytes, cudaStream_t s);
+void pool_free(void *p, cudaStream_t s);
+// Bytes reserved by the pool but not in use (reusable by the next call).
+size_t pool_idle_bytes(int device);
+
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(g_stream) { g_stream = s; }
+    ~StreamScope() { g_stream = prev; }
+};
+
 template <class T>
 struct DBuf {
     T *p = nullptr;
     size_t n = 0;
+    cudaStream_t s = 0;
     DBuf() = default;
     explicit DBuf(size_t count) { alloc(count); }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
     DBuf &operator=(DBuf &&o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
         return *this;
     }
     ~DBuf() { release(); }
     void alloc(size_t count) {
         release();
         if (count == 0) return;
-        WR_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        s = g_stream;
+        p = (T *)pool_alloc(count * sizeof(T), s);
         n = count;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, s);
         p = nullptr;
         n = 0;
     }
@@ -121,6 +141,8 @@ struct wr_graph {
     wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
     wr::DBuf<uint32_t> in_w;
     wr::DBuf<int> xy;       // [V*2] or empty
+    wr::DBuf<int> z;        // [V] rack level or empty
+    int bbox[6] = {0, 0, 0, 0, 0, 0};   // xmin, xmax, ymin, ymax, zmin, zmax
     wr::DevGraph view() const {
         return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, out_ptr.p, out_dst.p};
     }
@@ -137,14 +159,18 @@ void scan_exclusive_i32(const int *in, int *out, int n, cudaStream_t st);
 // Segment scheduler (a8): sources per BF batch for a per-source byte cost.
 int64_t budget_bytes(int64_t requested);
 int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes,
-                            int64_t S);
+                            int64_t S, int tsw);
+// Sources per lane (1, 2, 4) for S sources on nsm SMs (env WR_BF_SPL forces).
+int choose_spl(int64_t S, int nsm);
 
-struct BfRun {              // one BF segment over tiles of 32 sources
-    const int *tile_src;    // [ntiles*32] source vertex per lane, -1 = empty
+struct BfRun {              // one BF segment over tiles of 32*spl sources
+    const int *tile_src;    // [ntiles*tsw] source vertex per slot, -1 = empty
     int ntiles;
-    uint32_t *rows;         // [ntiles][V][32] working distances (output)
+    uint32_t *rows;         // [ntiles][V][tsw] working distances (output)
     int variant;
     int max_rounds;
+    int spl;                // sources per lane; tsw = 32*spl slots per tile
+    const int *slot_row = nullptr;  // [ntiles*tsw] output row offset per slot (null = identity)
 };
 
 struct BfTileStats {        // per-call accumulators (device)
@@ -165,8 +191,13 @@ void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int
 void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles,
                      int64_t out_row0, int32_t *pred_out, cudaStream_t st);
 
-// Builds tile_src for sources [lo, hi) of a device source list.
-void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int *d_tile_src, cudaStream_t st);
+// Builds tile_src for sources [lo, hi) of a device source list (tsw slots/tile).
+void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_tile_src, cudaStream_t st);
+// Same, with the sources ordered along a Morton curve of the graph's
+// coordinates (when present): slot_row[slot] = source offset in [0, hi-lo)
+// (-1 = empty slot), pos_of[offset] = slot position (wr_tiles.cu).
+void make_tiles_ordered(const wr_graph *g, const int *d_sources, int64_t lo, int64_t hi, int tsw, int *tile_src,
+                        int *slot_row, int *pos_of, cudaStream_t st);
 
 // ------------------------------------------------------------- routing --
 struct RouteProblem {       // one exhaustive search (an order or a segment)

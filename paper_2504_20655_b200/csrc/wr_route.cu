@@ -368,8 +368,8 @@ __global__ void owned_count_kernel(const int *stops, const int *n_arr, const int
 // the stops i whose source row lies in this BF segment [seg_lo, seg_hi).
 __global__ void gather_send_kernel(const int *stops, const int *n_arr, const int *status, int64_t B,
                                    const int *src_row, int64_t own_lo, int64_t own_hi, int64_t seg_lo,
-                                   int64_t seg_hi, const int64_t *off, const uint32_t *rows, int V,
-                                   uint32_t *send) {
+                                   int64_t seg_hi, const int64_t *off, const uint32_t *rows, int V, int tsw,
+                                   const int *pos_of, uint32_t *send) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= B * MS) return;
     const int64_t o = t / MS;
@@ -382,10 +382,10 @@ __global__ void gather_send_kernel(const int *stops, const int *n_arr, const int
     if (r < seg_lo || r >= seg_hi) return;
     int i_lo, i_hi;
     owned_range(s, n, src_row, own_lo, own_hi, i_lo, i_hi);
-    const int64_t rr = r - seg_lo;
-    const uint32_t *R = rows + (size_t)(rr / TS) * V * TS + (rr % TS);
+    const int64_t rr = pos_of[r - seg_lo];   // slot position of the source in the segment's tiles
+    const uint32_t *R = rows + (size_t)(rr / tsw) * V * tsw + (rr % tsw);
     uint32_t *dst = send + off[o] + (int64_t)(i - i_lo) * n;
-    for (int j = 0; j < n; ++j) dst[j] = R[(size_t)s[j] * TS];
+    for (int j = 0; j < n; ++j) dst[j] = R[(size_t)s[j] * tsw];
 }
 
 // Reassemble D[o][i][j] (16 x 16 stride) for orders [o_lo, o_hi) from the
@@ -719,6 +719,7 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     wr_route_opts o{};
     if (opts) o = *opts;
     cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
     auto P = std::make_unique<wr_plan>();
     P->device = g->device;
     P->g = g;
@@ -815,6 +816,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     wr_route_opts o{};
     if (opts) o = *opts;
     cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
     const int V = g->V;
     const int64_t nsrc = P->src_hi - P->src_lo;
     cudaEvent_t e0, e1;
@@ -833,10 +835,14 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         wr_graph_info(g, &gi);
         const int64_t budget = budget_bytes(o.hbm_budget);
         const int64_t fixed = gi.device_bytes + (128 << 20);
-        const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc);
-        const int64_t max_tiles = sb / TS;
-        DBuf<uint32_t> rows((size_t)max_tiles * V * TS);
-        DBuf<int> tile_src(max_tiles * TS);
+        int nsm = 0;
+        WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+        const int spl = choose_spl(nsrc, nsm);
+        const int tsw = 32 * spl;
+        const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc, tsw);
+        const int64_t max_tiles = sb / tsw;
+        DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
+        DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
         DBuf<int> flat(o.pred_out ? max_tiles : 0);
         int max_rounds = g->has_negative ? std::max(1, V - 1) : V;
         const int64_t *off_r = P->off_all.p + (int64_t)P->rank * (P->B + 1);
@@ -846,9 +852,9 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         WR_CUDA(cudaEventCreate(&b2));
         for (int64_t lo = P->src_lo; lo < P->src_hi; lo += sb) {
             const int64_t hi = std::min<int64_t>(P->src_hi, lo + sb);
-            const int ntiles = (int)((hi - lo + TS - 1) / TS);
-            make_tiles(P->sources.p, lo, hi, tile_src.p, st);
-            BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds};
+            const int ntiles = (int)((hi - lo + tsw - 1) / tsw);
+            make_tiles_ordered(g, P->sources.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
+            BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
             WR_CUDA(cudaEventRecord(b0, st));
             bf_run(g, run, d_stats.p, st);
             WR_CUDA(cudaEventRecord(b1, st));
@@ -873,7 +879,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             if (P->B > 0) {
                 gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, st>>>(
                     P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, lo, hi, off_r,
-                    rows.p, V, (uint32_t *)send);
+                    rows.p, V, tsw, pos_of.p, (uint32_t *)send);
                 count_launch();
                 WR_LAUNCH_CHECK();
             }
@@ -957,6 +963,7 @@ static wr_status finish_impl(wr_plan *P, const void *gathered, wr_route_result *
     wr_route_opts o{};
     if (opts) o = *opts;
     cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
     cudaEvent_t e0, e1;
     WR_CUDA(cudaEventCreate(&e0));
     WR_CUDA(cudaEventCreate(&e1));
@@ -1019,6 +1026,7 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
     wr_route_opts o{};
     if (opts) o = *opts;
     cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
     cudaEvent_t e0, e1;
     WR_CUDA(cudaEventCreate(&e0));
     WR_CUDA(cudaEventCreate(&e1));
@@ -1156,6 +1164,7 @@ wr_status wr_route_cost(int32_t wtype, const void *D, int32_t n, const int32_t *
             return wr::fail(WR_EINVAL, "wr_route_cost: bad arguments");
         if (count == 0) return WR_OK;
         cudaStream_t st = (cudaStream_t)stream;
+        wr::StreamScope stream_scope(st);
         int dev = 0;
         WR_CUDA(cudaGetDevice(&dev));
         wr::DBuf<uint32_t> dD = wr::to_device<uint32_t>((const uint32_t *)D, (size_t)n * n, st);

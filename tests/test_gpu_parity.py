@@ -147,10 +147,12 @@ def test_bf_targets_repeats_and_device_outputs():
 
 def test_bf_segment_budget_invariance():
     g = gen.config(3)[0]
-    srcs = np.arange(0, g.V, 29, dtype=np.int32)   # 182 sources
+    srcs = np.arange(0, g.V, 13, dtype=np.int32)   # 404 sources
     G = wr.Graph.from_gen(g)
     a, pa, sa = wr.bf_batch(G, srcs, pred=True)
-    budget = G.info().device_bytes + (64 << 20) + 64 * 4 * g.V * 2  # forces 64-source segments
+    # rows + dist/pred staging = 12V bytes per source: room for 128-source
+    # segments (one tile at the widest 32x4 layout)
+    budget = G.info().device_bytes + (64 << 20) + 128 * 4 * g.V * 3 + 4096
     b, pb, sb = wr.bf_batch(G, srcs, pred=True, hbm_budget=budget)
     assert sa.segments == 1 and sb.segments > 1
     assert a.tobytes() == b.tobytes() and np.array_equal(pa, pb)
