@@ -147,38 +147,49 @@ void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_ti
 }
 
 // ---------------------------------------------------- relaxing one word --
-// Pull over all in-arcs of one vertex (generic degree). Rl = this lane's
-// first slot of the tile; rows are TSW = 32*SPL words.
-template <class Op, int SPL>
-__device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32_t *__restrict__ Rl, int a0, int a1,
-                                                 int lane, Vec<SPL> d) {
+// Delta pull. In round r+1 a candidate only needs the in-arcs whose tail
+// improved in round r: an in-neighbour that did not change since the
+// candidate's previous relaxation was already folded in (if it changed
+// after that read, it is in the changed set and comes back next round).
+// The tails' change bits are tested lane-parallel (one bitmap probe per
+// arc, ballot), and only the set arcs are gathered. Dense mode tests nothing.
+
+// Generic-degree pull of one vertex. Rl = this lane's first slot.
+template <class Op, bool DELTA, int SPL>
+__device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32_t *__restrict__ Rl,
+                                                 const uint32_t *pchg, int a0, int a1, int lane, Vec<SPL> d,
+                                                 unsigned long long &relax) {
     constexpr int TSW = 32 * SPL;
     for (int base = a0; base < a1; base += 32) {
         const int cnt = min(32, a1 - base);
         int my_u = 0;
         uint32_t my_w = 0;
+        bool take = false;
         if (lane < cnt) {
             my_u = g.in_src[base + lane];
             my_w = g.in_w[base + lane];
+            take = !DELTA || ((pchg[my_u >> 5] >> (my_u & 31)) & 1u);
         }
-        int k = 0;
-        for (; k + 2 <= cnt; k += 2) {
-            const int u0 = __shfl_sync(FULL, my_u, k), u1 = __shfl_sync(FULL, my_u, k + 1);
-            const uint32_t w0 = __shfl_sync(FULL, my_w, k), w1 = __shfl_sync(FULL, my_w, k + 1);
-            const Vec<SPL> x0 = vload<SPL>(Rl + (size_t)u0 * TSW), x1 = vload<SPL>(Rl + (size_t)u1 * TSW);
+        uint32_t m = __ballot_sync(FULL, take);
+        relax += (unsigned long long)__popc(m);
+        while (m) {
+            const int k0 = __ffs(m) - 1;
+            m &= m - 1;
+            const bool two = m != 0;
+            const int k1 = two ? __ffs(m) - 1 : k0;
+            if (two) m &= m - 1;
+            const int u0 = __shfl_sync(FULL, my_u, k0), u1 = __shfl_sync(FULL, my_u, k1);
+            const uint32_t w0 = __shfl_sync(FULL, my_w, k0), w1 = __shfl_sync(FULL, my_w, k1);
+            const Vec<SPL> x0 = vload<SPL>(Rl + (size_t)u0 * TSW);
+            Vec<SPL> x1 = x0;
+            if (two) x1 = vload<SPL>(Rl + (size_t)u1 * TSW);
             vrelax<Op, SPL>(d, x0, w0);
-            vrelax<Op, SPL>(d, x1, w1);
-        }
-        for (; k < cnt; ++k) {
-            const int u = __shfl_sync(FULL, my_u, k);
-            const uint32_t wk = __shfl_sync(FULL, my_w, k);
-            vrelax<Op, SPL>(d, vload<SPL>(Rl + (size_t)u * TSW), wk);
+            if (two) vrelax<Op, SPL>(d, x1, w1);
         }
     }
     return d;
 }
 
-template <bool MARK>
 __device__ __forceinline__ void mark_out(const DevGraph &g, int q_lo, int q_hi, int b, int lane, uint32_t *nxt) {
     const int o0 = __shfl_sync(FULL, q_lo, b), o1 = __shfl_sync(FULL, q_hi, b);
     for (int e = o0 + lane; e < o1; e += 32) {
@@ -190,26 +201,28 @@ __device__ __forceinline__ void mark_out(const DevGraph &g, int q_lo, int q_hi, 
 // Relaxes the candidate vertices (bits of m) of word w for every slot.
 // The word's CSC/CSR offsets are read with one coalesced load each; two
 // candidates are processed per iteration (lanes 0-15 hold the first one's
-// in-arcs, 16-31 the second's) so four independent row gathers are in
-// flight. A vertex that improved for any slot (one __any_sync vote) marks its
-// out-neighbours in the next round's candidate bitmap, lane-parallel over its
-// out-arcs (shared-memory atomicOr; OR is order-independent).
-template <class Op, bool MARK, int SPL>
-__device__ __forceinline__ bool relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m, int lane,
-                                           unsigned long long &relax, uint32_t *nxt) {
+// in-arcs, 16-31 the second's) so up to four independent row gathers are
+// in flight. A vertex that improved for any slot (one __any_sync vote) is
+// recorded in the word's change mask (returned) and marks its out-neighbours
+// in the next round's candidate bitmap, lane-parallel over its out-arcs
+// (shared-memory atomicOr; OR is order-independent).
+template <class Op, bool DELTA, int SPL>
+__device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
+                                               int lane, unsigned long long &relax, const uint32_t *pchg,
+                                               uint32_t *nxt) {
     constexpr int TSW = 32 * SPL;
     const int vl = (w << 5) + lane;
     int p_lo = 0, p_hi = 0, q_lo = 0, q_hi = 0;
     if (vl < g.V) {
         p_lo = g.in_ptr[vl];
         p_hi = g.in_ptr[vl + 1];
-        if (MARK) {
+        if (DELTA) {
             q_lo = g.out_ptr[vl];
             q_hi = g.out_ptr[vl + 1];
         }
     }
     uint32_t *Rl = R + lane * SPL;           // this lane's slots of the tile
-    bool any = false;
+    uint32_t chg = 0;
     while (m) {
         const int b0 = __ffs(m) - 1;
         m &= m - 1;
@@ -233,50 +246,67 @@ __device__ __forceinline__ bool relax_word(const DevGraph &g, uint32_t *__restri
             const int cnt = lane < 16 ? n0 : n1;
             int my_u = 0;
             uint32_t my_w = 0;
+            bool take = false;
             if (sub < cnt) {
                 my_u = g.in_src[base + sub];
                 my_w = g.in_w[base + sub];
+                take = !DELTA || ((pchg[my_u >> 5] >> (my_u & 31)) & 1u);
             }
-            const int kmax = max(n0, n1);
-            for (int k = 0; k < kmax; k += 2) {
-                const int u00 = __shfl_sync(FULL, my_u, k), u01 = __shfl_sync(FULL, my_u, k + 1);
-                const int u10 = __shfl_sync(FULL, my_u, 16 + k), u11 = __shfl_sync(FULL, my_u, 17 + k);
-                const uint32_t w00 = __shfl_sync(FULL, my_w, k), w01 = __shfl_sync(FULL, my_w, k + 1);
-                const uint32_t w10 = __shfl_sync(FULL, my_w, 16 + k), w11 = __shfl_sync(FULL, my_w, 17 + k);
+            const uint32_t bal = __ballot_sync(FULL, take);
+            uint32_t m0 = bal & 0xffffu, m1 = bal >> 16;
+            relax += (unsigned long long)__popc(bal);
+            while (m0 | m1) {
+                // up to two arcs of each vertex per step: four gathers in flight
+                const int k00 = m0 ? __ffs(m0) - 1 : -1;
+                if (m0) m0 &= m0 - 1;
+                const int k01 = m0 ? __ffs(m0) - 1 : -1;
+                if (m0) m0 &= m0 - 1;
+                const int k10 = m1 ? __ffs(m1) - 1 : -1;
+                if (m1) m1 &= m1 - 1;
+                const int k11 = m1 ? __ffs(m1) - 1 : -1;
+                if (m1) m1 &= m1 - 1;
+                const int u00 = __shfl_sync(FULL, my_u, k00 & 31), u01 = __shfl_sync(FULL, my_u, k01 & 31);
+                const int u10 = __shfl_sync(FULL, my_u, (16 + k10) & 31), u11 = __shfl_sync(FULL, my_u, (16 + k11) & 31);
+                const uint32_t w00 = __shfl_sync(FULL, my_w, k00 & 31), w01 = __shfl_sync(FULL, my_w, k01 & 31);
+                const uint32_t w10 = __shfl_sync(FULL, my_w, (16 + k10) & 31);
+                const uint32_t w11 = __shfl_sync(FULL, my_w, (16 + k11) & 31);
                 Vec<SPL> x00, x01, x10, x11;
-                if (k < n0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
-                if (k + 1 < n0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
-                if (k < n1) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
-                if (k + 1 < n1) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
-                if (k < n0) vrelax<Op, SPL>(d0, x00, w00);
-                if (k + 1 < n0) vrelax<Op, SPL>(d0, x01, w01);
-                if (k < n1) vrelax<Op, SPL>(d1, x10, w10);
-                if (k + 1 < n1) vrelax<Op, SPL>(d1, x11, w11);
+                if (k00 >= 0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
+                if (k01 >= 0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
+                if (k10 >= 0) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
+                if (k11 >= 0) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
+                if (k00 >= 0) vrelax<Op, SPL>(d0, x00, w00);
+                if (k01 >= 0) vrelax<Op, SPL>(d0, x01, w01);
+                if (k10 >= 0) vrelax<Op, SPL>(d1, x10, w10);
+                if (k11 >= 0) vrelax<Op, SPL>(d1, x11, w11);
             }
         } else {
-            d0 = relax_vertex<Op, SPL>(g, Rl, a00, a01, lane, d0);
-            if (two) d1 = relax_vertex<Op, SPL>(g, Rl, a10, a11, lane, d1);
+            d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, a00, a01, lane, d0, relax);
+            if (two) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, a10, a11, lane, d1, relax);
         }
-        relax += (unsigned long long)(n0 + n1);
         const bool c0 = vless<Op, SPL>(d0, e0);
         if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
         const bool c1 = two && vless<Op, SPL>(d1, e1);
         if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
         const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
-        any |= any0 | any1;
-        if (MARK) {
-            if (any0) mark_out<MARK>(g, q_lo, q_hi, b0, lane, nxt);
-            if (any1) mark_out<MARK>(g, q_lo, q_hi, b1, lane, nxt);
+        if (any0) chg |= 1u << b0;
+        if (any1) chg |= 1u << b1;
+        if (DELTA) {
+            if (any0) mark_out(g, q_lo, q_hi, b0, lane, nxt);
+            if (any1) mark_out(g, q_lo, q_hi, b1, lane, nxt);
         }
     }
-    return any;
+    return chg;
 }
 
 // ------------------------------------------------------ the sweep kernel --
-// One CTA per tile at a time. Shared memory: two V-bit candidate bitmaps,
-// cur (relaxed this round) and nxt (out-neighbours of this round's
-// improvements), swapped after each round's barrier. Dense variant: every
-// vertex is a candidate every round (the paper's edge-parallel class).
+// One CTA per tile at a time. Shared memory: four V-bit bitmaps - the
+// candidate sets cur (relaxed this round) and nxt (out-neighbours of this
+// round's improvements), and the change sets pchg (improved last round,
+// read-only now) and cchg (improved this round) - swapped after each round's
+// barrier. Word w of every bitmap is written by one warp only (w mod warps).
+// Dense variant: every vertex is a candidate every round, all arcs pulled
+// (the paper's edge-parallel class of work).
 template <class Op, bool DENSE, int NT, int MINB, int SPL>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
@@ -297,7 +327,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         const int tile = s_tile;
         if (tile >= ntiles) break;
         uint32_t *R = rows + (size_t)tile * V * TSW;
-        uint32_t *cur = smem, *nxt = smem + NW;
+        uint32_t *cur = smem, *nxt = smem + NW, *pchg = smem + 2 * NW, *cchg = smem + 3 * NW;
 
         // init: every row INF, bitmaps empty
         {
@@ -305,16 +335,17 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             uint4 *R4 = reinterpret_cast<uint4 *>(R);
             const size_t n4 = (size_t)V * (TSW / 4);
             for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
-            for (int w = threadIdx.x; w < 2 * NW; w += NT) smem[w] = 0u;
+            for (int w = threadIdx.x; w < 4 * NW; w += NT) smem[w] = 0u;
         }
         __syncthreads();
-        if (warp == 0) {   // seed: d[s][slot] = 0, candidates = out-neighbours of the sources
+        if (warp == 0) {   // seed: d[s][slot] = 0; the sources "changed" in round 0
 #pragma unroll
             for (int j = 0; j < SPL; ++j) {
                 const int slot = lane * SPL + j;
                 const int s = tile_src[tile * TSW + slot];
                 if (s >= 0) {
                     R[(size_t)s * TSW + slot] = Op::ZERO;
+                    atomicOr(&pchg[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
                         const int x = g.out_dst[e];
                         atomicOr(&cur[x >> 5], 1u << (x & 31));
@@ -336,16 +367,23 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             int any = 0;
             for (int w = warp; w < NW; w += NWARPS) {
                 const uint32_t m = cur[w];
-                if (!m) continue;
-                __syncwarp();
-                if (lane == 0) cur[w] = 0u;
-                any |= relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, nxt);
+                uint32_t c = 0;
+                if (m) {
+                    __syncwarp();
+                    if (lane == 0) cur[w] = 0u;
+                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt);
+                    any |= c != 0;
+                }
+                if (!DENSE && lane == 0 && cchg[w] != c) cchg[w] = c;   // also clears stale words
             }
             ++rounds;
             more = __syncthreads_or(any) != 0;
             uint32_t *t = cur;
             cur = nxt;
             nxt = t;
+            t = pchg;
+            pchg = cchg;
+            cchg = t;
             if (more && rounds >= max_rounds) {
                 if (threadIdx.x == 0) atomicMax(&stats->negcycle_tile, tile);
                 more = false;
@@ -396,7 +434,7 @@ template <class Op>
 static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
     const int V = g->V;
     const int NW = (V + 31) / 32;
-    const size_t smem = (size_t)2 * NW * sizeof(uint32_t);
+    const size_t smem = (size_t)4 * NW * sizeof(uint32_t);
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem + 1024 > (size_t)max_optin)
@@ -430,7 +468,9 @@ void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStrea
 int choose_spl(int64_t S, int nsm) {
     const int forced = env_int("WR_BF_SPL", 0);
     if (forced == 1 || forced == 2 || forced == 4) return forced;
-    int spl = 4;
+    // measured on config 5: SPL 2 beats 1 and 4 (4 spills
+    // registers and widens the tiles' wavefront spread)
+    int spl = 2;
     while (spl > 1 && S / (32 * spl) < (int64_t)4 * nsm) spl /= 2;
     return spl;
 }
