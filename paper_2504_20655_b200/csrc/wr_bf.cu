@@ -190,8 +190,7 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
     return d;
 }
 
-__device__ __forceinline__ void mark_out(const DevGraph &g, int q_lo, int q_hi, int b, int lane, uint32_t *nxt) {
-    const int o0 = __shfl_sync(FULL, q_lo, b), o1 = __shfl_sync(FULL, q_hi, b);
+__device__ __forceinline__ void mark_out_range(const DevGraph &g, int o0, int o1, int lane, uint32_t *nxt) {
     for (int e = o0 + lane; e < o1; e += 32) {
         const int x = g.out_dst[e];
         atomicOr(&nxt[x >> 5], 1u << (x & 31));
@@ -199,102 +198,163 @@ __device__ __forceinline__ void mark_out(const DevGraph &g, int q_lo, int q_hi, 
 }
 
 // Relaxes the candidate vertices (bits of m) of word w for every slot.
-// The word's CSC/CSR offsets are read with one coalesced load each; two
-// candidates are processed per iteration (lanes 0-15 hold the first one's
-// in-arcs, 16-31 the second's) so up to four independent row gathers are
-// in flight. A vertex that improved for any slot (one __any_sync vote) is
-// recorded in the word's change mask (returned) and marks its out-neighbours
-// in the next round's candidate bitmap, lane-parallel over its out-arcs
-// (shared-memory atomicOr; OR is order-independent).
+// The word's CSC/CSR offsets are read with one coalesced load each. Two
+// candidates form a pair (lanes 0-15 hold the first one's arcs, 16-31 the
+// second's) and pairs are software-pipelined: the next pair's own rows,
+// in-arcs (with their change-bit ballot) and out-arcs are loaded before the
+// current pair's row gathers, so a warp keeps two pairs' worth of memory
+// traffic in flight instead of one dependent chain per vertex. A vertex
+// that improved for any slot (one __any_sync vote) is recorded in the
+// word's change mask (returned) and marks its out-neighbours in the next
+// round's candidate bitmap (shared-memory atomicOr; OR is order-free).
+template <int SPL>
+struct PairState {
+    int b0, b1;
+    bool two, fast;
+    int a00, a01, a10, a11, o00, o01, o10, o11;
+    Vec<SPL> e0, e1;
+    int my_u, my_x;
+    uint32_t my_w, bal;
+};
+
+template <class Op, bool DELTA, int SPL>
+__device__ __forceinline__ PairState<SPL> load_pair(const DevGraph &g, const uint32_t *Rl, int w, uint32_t &m,
+                                                    int lane, int p_lo, int p_hi, int q_lo, int q_hi,
+                                                    const uint32_t *pchg) {
+    constexpr int TSW = 32 * SPL;
+    PairState<SPL> S;
+    S.b0 = __ffs(m) - 1;
+    m &= m - 1;
+    S.two = m != 0;
+    S.b1 = S.b0;
+    if (S.two) {
+        S.b1 = __ffs(m) - 1;
+        m &= m - 1;
+    }
+    S.a00 = __shfl_sync(FULL, p_lo, S.b0);
+    S.a01 = __shfl_sync(FULL, p_hi, S.b0);
+    S.a10 = __shfl_sync(FULL, p_lo, S.b1);
+    S.a11 = __shfl_sync(FULL, p_hi, S.b1);
+    S.o00 = __shfl_sync(FULL, q_lo, S.b0);
+    S.o01 = __shfl_sync(FULL, q_hi, S.b0);
+    S.o10 = __shfl_sync(FULL, q_lo, S.b1);
+    S.o11 = __shfl_sync(FULL, q_hi, S.b1);
+    if (!S.two) {
+        S.a11 = S.a10;
+        S.o11 = S.o10;
+    }
+    const int n0 = S.a01 - S.a00, n1 = S.a11 - S.a10;
+    const int on0 = S.o01 - S.o00, on1 = S.o11 - S.o10;
+    S.e0 = vload<SPL>(Rl + (size_t)((w << 5) + S.b0) * TSW);
+    S.e1 = S.e0;
+    if (S.two) S.e1 = vload<SPL>(Rl + (size_t)((w << 5) + S.b1) * TSW);
+    S.fast = n0 <= 16 && n1 <= 16 && on0 <= 16 && on1 <= 16;
+    S.my_u = 0;
+    S.my_w = 0;
+    S.my_x = -1;
+    S.bal = 0;
+    if (S.fast) {
+        const int sub = lane & 15;
+        const int base = lane < 16 ? S.a00 : S.a10;
+        const int cnt = lane < 16 ? n0 : n1;
+        bool take = false;
+        if (sub < cnt) {
+            S.my_u = g.in_src[base + sub];
+            S.my_w = g.in_w[base + sub];
+            take = !DELTA || ((pchg[S.my_u >> 5] >> (S.my_u & 31)) & 1u);
+        }
+        if (DELTA) {
+            const int ob = lane < 16 ? S.o00 : S.o10;
+            const int oc = lane < 16 ? on0 : on1;
+            if (sub < oc) S.my_x = g.out_dst[ob + sub];
+        }
+        S.bal = __ballot_sync(FULL, take);
+    }
+    return S;
+}
+
+template <class Op, bool DELTA, int SPL>
+__device__ __forceinline__ uint32_t process_pair(const DevGraph &g, uint32_t *Rl, int w, const PairState<SPL> &S,
+                                                 int lane, unsigned long long &relax, const uint32_t *pchg,
+                                                 uint32_t *nxt) {
+    constexpr int TSW = 32 * SPL;
+    Vec<SPL> d0 = S.e0, d1 = S.e1;
+    if (S.fast) {
+        uint32_t m0 = S.bal & 0xffffu, m1 = S.bal >> 16;
+        relax += (unsigned long long)__popc(S.bal);
+        while (m0 | m1) {
+            // up to two arcs of each vertex per step: four gathers in flight
+            const int k00 = m0 ? __ffs(m0) - 1 : -1;
+            if (m0) m0 &= m0 - 1;
+            const int k01 = m0 ? __ffs(m0) - 1 : -1;
+            if (m0) m0 &= m0 - 1;
+            const int k10 = m1 ? __ffs(m1) - 1 : -1;
+            if (m1) m1 &= m1 - 1;
+            const int k11 = m1 ? __ffs(m1) - 1 : -1;
+            if (m1) m1 &= m1 - 1;
+            const int u00 = __shfl_sync(FULL, S.my_u, k00 & 31), u01 = __shfl_sync(FULL, S.my_u, k01 & 31);
+            const int u10 = __shfl_sync(FULL, S.my_u, (16 + k10) & 31);
+            const int u11 = __shfl_sync(FULL, S.my_u, (16 + k11) & 31);
+            const uint32_t w00 = __shfl_sync(FULL, S.my_w, k00 & 31), w01 = __shfl_sync(FULL, S.my_w, k01 & 31);
+            const uint32_t w10 = __shfl_sync(FULL, S.my_w, (16 + k10) & 31);
+            const uint32_t w11 = __shfl_sync(FULL, S.my_w, (16 + k11) & 31);
+            Vec<SPL> x00, x01, x10, x11;
+            if (k00 >= 0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
+            if (k01 >= 0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
+            if (k10 >= 0) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
+            if (k11 >= 0) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
+            if (k00 >= 0) vrelax<Op, SPL>(d0, x00, w00);
+            if (k01 >= 0) vrelax<Op, SPL>(d0, x01, w01);
+            if (k10 >= 0) vrelax<Op, SPL>(d1, x10, w10);
+            if (k11 >= 0) vrelax<Op, SPL>(d1, x11, w11);
+        }
+    } else {
+        d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, S.a00, S.a01, lane, d0, relax);
+        if (S.two) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, S.a10, S.a11, lane, d1, relax);
+    }
+    const int v0 = (w << 5) + S.b0, v1 = (w << 5) + S.b1;
+    const bool c0 = vless<Op, SPL>(d0, S.e0);
+    if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
+    const bool c1 = S.two && vless<Op, SPL>(d1, S.e1);
+    if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
+    const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
+    uint32_t chg = 0;
+    if (any0) chg |= 1u << S.b0;
+    if (any1) chg |= 1u << S.b1;
+    if (DELTA && (any0 | any1)) {
+        if (S.fast) {
+            const bool mine = lane < 16 ? any0 : any1;
+            if (mine && S.my_x >= 0) atomicOr(&nxt[S.my_x >> 5], 1u << (S.my_x & 31));
+        } else {
+            if (any0) mark_out_range(g, S.o00, S.o01, lane, nxt);
+            if (any1) mark_out_range(g, S.o10, S.o11, lane, nxt);
+        }
+    }
+    return chg;
+}
+
 template <class Op, bool DELTA, int SPL>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const uint32_t *pchg,
                                                uint32_t *nxt) {
-    constexpr int TSW = 32 * SPL;
     const int vl = (w << 5) + lane;
     int p_lo = 0, p_hi = 0, q_lo = 0, q_hi = 0;
     if (vl < g.V) {
         p_lo = g.in_ptr[vl];
         p_hi = g.in_ptr[vl + 1];
-        if (DELTA) {
-            q_lo = g.out_ptr[vl];
-            q_hi = g.out_ptr[vl + 1];
-        }
+        q_lo = g.out_ptr[vl];
+        q_hi = g.out_ptr[vl + 1];
     }
     uint32_t *Rl = R + lane * SPL;           // this lane's slots of the tile
     uint32_t chg = 0;
-    while (m) {
-        const int b0 = __ffs(m) - 1;
-        m &= m - 1;
-        const bool two = m != 0;
-        int b1 = b0;
-        if (two) {
-            b1 = __ffs(m) - 1;
-            m &= m - 1;
-        }
-        const int v0 = (w << 5) + b0, v1 = (w << 5) + b1;
-        const int a00 = __shfl_sync(FULL, p_lo, b0), a01 = __shfl_sync(FULL, p_hi, b0);
-        const int a10 = __shfl_sync(FULL, p_lo, b1), a11 = __shfl_sync(FULL, p_hi, b1);
-        const int n0 = a01 - a00, n1 = two ? a11 - a10 : 0;
-        const Vec<SPL> e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
-        Vec<SPL> e1 = e0;
-        if (two) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
-        Vec<SPL> d0 = e0, d1 = e1;
-        if (n0 <= 16 && n1 <= 16) {
-            const int sub = lane & 15;
-            const int base = lane < 16 ? a00 : a10;
-            const int cnt = lane < 16 ? n0 : n1;
-            int my_u = 0;
-            uint32_t my_w = 0;
-            bool take = false;
-            if (sub < cnt) {
-                my_u = g.in_src[base + sub];
-                my_w = g.in_w[base + sub];
-                take = !DELTA || ((pchg[my_u >> 5] >> (my_u & 31)) & 1u);
-            }
-            const uint32_t bal = __ballot_sync(FULL, take);
-            uint32_t m0 = bal & 0xffffu, m1 = bal >> 16;
-            relax += (unsigned long long)__popc(bal);
-            while (m0 | m1) {
-                // up to two arcs of each vertex per step: four gathers in flight
-                const int k00 = m0 ? __ffs(m0) - 1 : -1;
-                if (m0) m0 &= m0 - 1;
-                const int k01 = m0 ? __ffs(m0) - 1 : -1;
-                if (m0) m0 &= m0 - 1;
-                const int k10 = m1 ? __ffs(m1) - 1 : -1;
-                if (m1) m1 &= m1 - 1;
-                const int k11 = m1 ? __ffs(m1) - 1 : -1;
-                if (m1) m1 &= m1 - 1;
-                const int u00 = __shfl_sync(FULL, my_u, k00 & 31), u01 = __shfl_sync(FULL, my_u, k01 & 31);
-                const int u10 = __shfl_sync(FULL, my_u, (16 + k10) & 31), u11 = __shfl_sync(FULL, my_u, (16 + k11) & 31);
-                const uint32_t w00 = __shfl_sync(FULL, my_w, k00 & 31), w01 = __shfl_sync(FULL, my_w, k01 & 31);
-                const uint32_t w10 = __shfl_sync(FULL, my_w, (16 + k10) & 31);
-                const uint32_t w11 = __shfl_sync(FULL, my_w, (16 + k11) & 31);
-                Vec<SPL> x00, x01, x10, x11;
-                if (k00 >= 0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
-                if (k01 >= 0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
-                if (k10 >= 0) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
-                if (k11 >= 0) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
-                if (k00 >= 0) vrelax<Op, SPL>(d0, x00, w00);
-                if (k01 >= 0) vrelax<Op, SPL>(d0, x01, w01);
-                if (k10 >= 0) vrelax<Op, SPL>(d1, x10, w10);
-                if (k11 >= 0) vrelax<Op, SPL>(d1, x11, w11);
-            }
-        } else {
-            d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, a00, a01, lane, d0, relax);
-            if (two) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, a10, a11, lane, d1, relax);
-        }
-        const bool c0 = vless<Op, SPL>(d0, e0);
-        if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
-        const bool c1 = two && vless<Op, SPL>(d1, e1);
-        if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
-        const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
-        if (any0) chg |= 1u << b0;
-        if (any1) chg |= 1u << b1;
-        if (DELTA) {
-            if (any0) mark_out(g, q_lo, q_hi, b0, lane, nxt);
-            if (any1) mark_out(g, q_lo, q_hi, b1, lane, nxt);
-        }
+    PairState<SPL> S = load_pair<Op, DELTA, SPL>(g, Rl, w, m, lane, p_lo, p_hi, q_lo, q_hi, pchg);
+    for (;;) {
+        const bool more = m != 0;
+        PairState<SPL> N;
+        if (more) N = load_pair<Op, DELTA, SPL>(g, Rl, w, m, lane, p_lo, p_hi, q_lo, q_hi, pchg);
+        chg |= process_pair<Op, DELTA, SPL>(g, Rl, w, S, lane, relax, pchg, nxt);
+        if (!more) break;
+        S = N;
     }
     return chg;
 }
@@ -422,10 +482,16 @@ static int env_int(const char *name, int dflt) {
 
 template <class Op, bool DENSE, int SPL>
 static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    static const int cfg = env_int("WR_BF_CONFIG", 0);
+    // default 5 = 448 threads x 2 CTAs/SM (73 regs, no spills): measured best
+    // on config 5 among 512x2 / 512x3 / 256x4 / 256x3 / 384x2 / 448x2 / 320x2
+    static const int cfg = env_int("WR_BF_CONFIG", 5);
     switch (cfg) {
         case 1: launch_shape<Op, DENSE, 512, 3, SPL>(g, run, d_stats, st, smem); break;
         case 2: launch_shape<Op, DENSE, 256, 4, SPL>(g, run, d_stats, st, smem); break;
+        case 3: launch_shape<Op, DENSE, 256, 3, SPL>(g, run, d_stats, st, smem); break;
+        case 4: launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st, smem); break;
+        case 5: launch_shape<Op, DENSE, 448, 2, SPL>(g, run, d_stats, st, smem); break;
+        case 6: launch_shape<Op, DENSE, 320, 2, SPL>(g, run, d_stats, st, smem); break;
         default: launch_shape<Op, DENSE, 512, 2, SPL>(g, run, d_stats, st, smem); break;
     }
 }
@@ -560,9 +626,166 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
+// a4 canonical pred, vectorised over the tile: warp per (tile, 32 vertices),
+// lane = SPL source slots. In-arcs are sorted by tail, so the first steep
+// tight in-arc met is the smallest-tail one: the arc loop stops as soon as
+// every slot that needs a predecessor has one. Results are staged in shared
+// memory and written as one 128-B segment per source row.
+template <int SPL>
+struct PredShape {
+    static constexpr int WARPS = SPL == 4 ? 2 : 4;   // static smem staging <= 48 KB
+};
+
+template <class Op, int SPL>
+__global__ void __launch_bounds__(PredShape<SPL>::WARPS * 32) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
+                                                      const uint32_t *__restrict__ rows,
+                                                      const int *__restrict__ slot_row, int64_t out_row0,
+                                                      int32_t *pred_out, int *flat_tiles) {
+    constexpr int TSW = 32 * SPL;
+    constexpr int PW = PredShape<SPL>::WARPS;
+    __shared__ int32_t sp[PW][32][TSW + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int V = g.V;
+    const int chunks = (V + 31) / 32;
+    const int64_t job = (int64_t)blockIdx.x * PW + warp;
+    if (job >= (int64_t)ntiles * chunks) return;
+    const int tile = (int)(job / chunks);
+    const int c0 = (int)(job % chunks) * 32;
+    const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
+    int src[SPL];
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) src[j] = tile_src[tile * TSW + lane * SPL + j];
+    bool flat = false;
+    const int nv = min(32, V - c0);
+    int p_lo = 0, p_hi = 0;
+    if (lane < nv) {
+        p_lo = g.in_ptr[c0 + lane];
+        p_hi = g.in_ptr[c0 + lane + 1];
+    }
+    // steep-tight test of one gathered in-neighbour row for all slots
+    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, bool (&need)[SPL], int (&best)[SPL]) {
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            if (need[j] && Op::tight(x.x[j], w, d.x[j]) && Op::less(x.x[j], d.x[j])) {
+                best[j] = u;
+                need[j] = false;
+            }
+        }
+    };
+    // two vertices per step (lanes 0-15 / 16-31 hold their in-arcs), up to
+    // four row gathers in flight; stop when no slot still needs a pred
+    for (int jv = 0; jv < nv; jv += 2) {
+        const bool two = jv + 1 < nv;
+        const int jv1 = two ? jv + 1 : jv;
+        const int v0 = c0 + jv, v1 = c0 + jv1;
+        const int a00 = __shfl_sync(FULL, p_lo, jv), a01 = __shfl_sync(FULL, p_hi, jv);
+        const int a10 = __shfl_sync(FULL, p_lo, jv1), a11 = __shfl_sync(FULL, p_hi, jv1);
+        const int n0 = a01 - a00, n1 = two ? a11 - a10 : 0;
+        const Vec<SPL> d0 = vload<SPL>(Rl + (size_t)v0 * TSW);
+        Vec<SPL> d1 = d0;
+        if (two) d1 = vload<SPL>(Rl + (size_t)v1 * TSW);
+        bool need0[SPL], need1[SPL];
+        int best0[SPL], best1[SPL];
+        bool anyn = false;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            need0[j] = src[j] >= 0 && v0 != src[j] && Op::finite(d0.x[j]);
+            need1[j] = two && src[j] >= 0 && v1 != src[j] && Op::finite(d1.x[j]);
+            best0[j] = best1[j] = -1;
+            anyn |= need0[j] | need1[j];
+        }
+        if (n0 <= 16 && n1 <= 16) {
+            const int sub = lane & 15;
+            const int base = lane < 16 ? a00 : a10;
+            const int cnt = lane < 16 ? n0 : n1;
+            int my_u = 0;
+            uint32_t my_w = 0;
+            if (sub < cnt) {
+                my_u = g.in_src[base + sub];
+                my_w = g.in_w[base + sub];
+            }
+            const int kmax = max(n0, n1);
+            for (int k = 0; k < kmax && __any_sync(FULL, anyn); k += 2) {
+                const int u00 = __shfl_sync(FULL, my_u, k), u01 = __shfl_sync(FULL, my_u, k + 1);
+                const int u10 = __shfl_sync(FULL, my_u, 16 + k), u11 = __shfl_sync(FULL, my_u, 17 + k);
+                const uint32_t w00 = __shfl_sync(FULL, my_w, k), w01 = __shfl_sync(FULL, my_w, k + 1);
+                const uint32_t w10 = __shfl_sync(FULL, my_w, 16 + k), w11 = __shfl_sync(FULL, my_w, 17 + k);
+                Vec<SPL> x00, x01, x10, x11;
+                if (k < n0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
+                if (k + 1 < n0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
+                if (k < n1) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
+                if (k + 1 < n1) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
+                if (k < n0) test(x00, w00, u00, d0, need0, best0);
+                if (k + 1 < n0) test(x01, w01, u01, d0, need0, best0);
+                if (k < n1) test(x10, w10, u10, d1, need1, best1);
+                if (k + 1 < n1) test(x11, w11, u11, d1, need1, best1);
+                anyn = false;
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) anyn |= need0[j] | need1[j];
+            }
+        } else {
+            auto slow = [&](int lo, int hi, const Vec<SPL> &d, bool (&need)[SPL], int (&best)[SPL]) {
+                for (int base = lo; base < hi; base += 32) {
+                    const int cnt = min(32, hi - base);
+                    int my_u = 0;
+                    uint32_t my_w = 0;
+                    if (lane < cnt) {
+                        my_u = g.in_src[base + lane];
+                        my_w = g.in_w[base + lane];
+                    }
+                    for (int k = 0; k < cnt; ++k) {
+                        const int u = __shfl_sync(FULL, my_u, k);
+                        const uint32_t w = __shfl_sync(FULL, my_w, k);
+                        test(vload<SPL>(Rl + (size_t)u * TSW), w, u, d, need, best);
+                    }
+                }
+            };
+            slow(a00, a01, d0, need0, best0);
+            if (two) slow(a10, a11, d1, need1, best1);
+        }
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            flat |= need0[j] | need1[j];      // reachable, no steep tight in-arc: flat
+            sp[warp][jv][lane * SPL + j] = need0[j] ? -1 : best0[j];
+            if (two) sp[warp][jv1][lane * SPL + j] = need1[j] ? -1 : best1[j];
+        }
+    }
+    __syncwarp();
+    for (int s = 0; s < TSW; ++s) {
+        const int sl = tile * TSW + s;
+        if (tile_src[sl] < 0) break;
+        const int64_t row = out_row0 + (slot_row ? slot_row[sl] : sl);
+        if (lane < nv) pred_out[row * (int64_t)V + c0 + lane] = sp[warp][lane][s];
+    }
+    if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
+}
+
+template <class Op>
+static void launch_pred(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
+                        cudaStream_t st) {
+    const int64_t jobs = (int64_t)run.ntiles * ((g->V + 31) / 32);
+    if (run.spl == 2)
+        bf_pred_kernel<Op, 2><<<(unsigned)((jobs + 3) / 4), 128, 0, st>>>(
+            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+    else if (run.spl == 4)
+        bf_pred_kernel<Op, 4><<<(unsigned)((jobs + 1) / 2), 64, 0, st>>>(
+            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+    else
+        bf_pred_kernel<Op, 1><<<(unsigned)((jobs + 3) / 4), 128, 0, st>>>(
+            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+    count_launch();
+    WR_LAUNCH_CHECK();
+}
+
 void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t, const int *targets, int T,
                       void *dist_out, int32_t *pred_out, int *d_flat_tiles, cudaStream_t st) {
     if (run.ntiles <= 0 || (!dist_out && !pred_out)) return;
+    if (pred_out && !g->has_negative) {     // fast vectorised pred pass (flat vertices flagged)
+        if (g->wtype == WR_F32) launch_pred<OpF32>(g, run, out_row0, pred_out, d_flat_tiles, st);
+        else launch_pred<OpU32>(g, run, out_row0, pred_out, d_flat_tiles, st);
+        pred_out = nullptr;
+        if (!dist_out) return;
+    }
     const int tsw = 32 * run.spl;
     const int ncols = targets ? T : g->V;
     const int64_t jobs = (int64_t)run.ntiles * run.spl * ((ncols + 31) / 32);

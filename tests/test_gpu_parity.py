@@ -187,6 +187,32 @@ def test_route_segmented_worked_example():
         assert int(r["cost_bits"]) == c and r["seq"][:5].tolist() == picks[s].tolist()
 
 
+def test_segment_plan_vs_oracle():
+    rng = np.random.default_rng(17)
+    for trial in range(200):
+        n = int(rng.integers(1, 17))
+        K = int(rng.integers(1, 5))
+        span = int(rng.choice([3, 40, 1 << 19]))
+        xy = rng.integers(-span, span, (n, 2)).astype(np.int32)
+        assert wr.segment_plan(xy, K).tolist() == oracle.kmeans(xy, K).tolist(), (trial, n, K)
+
+
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_segmented_random_labels(wtype):
+    g = gen.config(3, wtype=wtype)[0]
+    G = wr.Graph.from_gen(g)
+    rng = np.random.default_rng(23 if wtype == "i32" else 24)
+    for trial in range(25):
+        n = int(rng.integers(2, 13))
+        stops = np.sort(rng.choice(5000, n, replace=False)).astype(np.int32)
+        labels = rng.integers(0, min(6, n), n).astype(np.int32)
+        r = wr.route_segmented(G, stops, labels=labels, m=6)
+        D = oracle.bf_many(g, stops)[:, stops]
+        c, s, counts = oracle.segmented_route(D, labels)
+        assert wr.decode_cost(np.array([r]), G.wtype)[0].tobytes() == np.asarray(c).tobytes()
+        assert r["seq"][:n].tolist() == stops[s].tolist()
+
+
 def compare_orders(g, orders, m, chunk=0, G=None, results=None):
     G = G or wr.Graph.from_gen(g)
     res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk) if results is None \
