@@ -197,165 +197,114 @@ __device__ __forceinline__ void mark_out_range(const DevGraph &g, int o0, int o1
     }
 }
 
-// Relaxes the candidate vertices (bits of m) of word w for every slot.
-// The word's CSC/CSR offsets are read with one coalesced load each. Two
-// candidates form a pair (lanes 0-15 hold the first one's arcs, 16-31 the
-// second's) and pairs are software-pipelined: the next pair's own rows,
-// in-arcs (with their change-bit ballot) and out-arcs are loaded before the
-// current pair's row gathers, so a warp keeps two pairs' worth of memory
-// traffic in flight instead of one dependent chain per vertex. A vertex
-// that improved for any slot (one __any_sync vote) is recorded in the
-// word's change mask (returned) and marks its out-neighbours in the next
-// round's candidate bitmap (shared-memory atomicOr; OR is order-free).
-template <int SPL>
-struct PairState {
-    int b0, b1;
-    bool two, fast;
-    int a00, a01, a10, a11, o00, o01, o10, o11;
-    Vec<SPL> e0, e1;
-    int my_u, my_x;
-    uint32_t my_w, bal;
-};
-
-template <class Op, bool DELTA, int SPL>
-__device__ __forceinline__ PairState<SPL> load_pair(const DevGraph &g, const uint32_t *Rl, int w, uint32_t &m,
-                                                    int lane, int p_lo, int p_hi, int q_lo, int q_hi,
-                                                    const uint32_t *pchg) {
-    constexpr int TSW = 32 * SPL;
-    PairState<SPL> S;
-    S.b0 = __ffs(m) - 1;
-    m &= m - 1;
-    S.two = m != 0;
-    S.b1 = S.b0;
-    if (S.two) {
-        S.b1 = __ffs(m) - 1;
-        m &= m - 1;
-    }
-    S.a00 = __shfl_sync(FULL, p_lo, S.b0);
-    S.a01 = __shfl_sync(FULL, p_hi, S.b0);
-    S.a10 = __shfl_sync(FULL, p_lo, S.b1);
-    S.a11 = __shfl_sync(FULL, p_hi, S.b1);
-    S.o00 = __shfl_sync(FULL, q_lo, S.b0);
-    S.o01 = __shfl_sync(FULL, q_hi, S.b0);
-    S.o10 = __shfl_sync(FULL, q_lo, S.b1);
-    S.o11 = __shfl_sync(FULL, q_hi, S.b1);
-    if (!S.two) {
-        S.a11 = S.a10;
-        S.o11 = S.o10;
-    }
-    const int n0 = S.a01 - S.a00, n1 = S.a11 - S.a10;
-    const int on0 = S.o01 - S.o00, on1 = S.o11 - S.o10;
-    S.e0 = vload<SPL>(Rl + (size_t)((w << 5) + S.b0) * TSW);
-    S.e1 = S.e0;
-    if (S.two) S.e1 = vload<SPL>(Rl + (size_t)((w << 5) + S.b1) * TSW);
-    S.fast = n0 <= 16 && n1 <= 16 && on0 <= 16 && on1 <= 16;
-    S.my_u = 0;
-    S.my_w = 0;
-    S.my_x = -1;
-    S.bal = 0;
-    if (S.fast) {
-        const int sub = lane & 15;
-        const int base = lane < 16 ? S.a00 : S.a10;
-        const int cnt = lane < 16 ? n0 : n1;
-        bool take = false;
-        if (sub < cnt) {
-            S.my_u = g.in_src[base + sub];
-            S.my_w = g.in_w[base + sub];
-            take = !DELTA || ((pchg[S.my_u >> 5] >> (S.my_u & 31)) & 1u);
-        }
-        if (DELTA) {
-            const int ob = lane < 16 ? S.o00 : S.o10;
-            const int oc = lane < 16 ? on0 : on1;
-            if (sub < oc) S.my_x = g.out_dst[ob + sub];
-        }
-        S.bal = __ballot_sync(FULL, take);
-    }
-    return S;
-}
-
-template <class Op, bool DELTA, int SPL>
-__device__ __forceinline__ uint32_t process_pair(const DevGraph &g, uint32_t *Rl, int w, const PairState<SPL> &S,
-                                                 int lane, unsigned long long &relax, const uint32_t *pchg,
-                                                 uint32_t *nxt) {
-    constexpr int TSW = 32 * SPL;
-    Vec<SPL> d0 = S.e0, d1 = S.e1;
-    if (S.fast) {
-        uint32_t m0 = S.bal & 0xffffu, m1 = S.bal >> 16;
-        relax += (unsigned long long)__popc(S.bal);
-        while (m0 | m1) {
-            // up to two arcs of each vertex per step: four gathers in flight
-            const int k00 = m0 ? __ffs(m0) - 1 : -1;
-            if (m0) m0 &= m0 - 1;
-            const int k01 = m0 ? __ffs(m0) - 1 : -1;
-            if (m0) m0 &= m0 - 1;
-            const int k10 = m1 ? __ffs(m1) - 1 : -1;
-            if (m1) m1 &= m1 - 1;
-            const int k11 = m1 ? __ffs(m1) - 1 : -1;
-            if (m1) m1 &= m1 - 1;
-            const int u00 = __shfl_sync(FULL, S.my_u, k00 & 31), u01 = __shfl_sync(FULL, S.my_u, k01 & 31);
-            const int u10 = __shfl_sync(FULL, S.my_u, (16 + k10) & 31);
-            const int u11 = __shfl_sync(FULL, S.my_u, (16 + k11) & 31);
-            const uint32_t w00 = __shfl_sync(FULL, S.my_w, k00 & 31), w01 = __shfl_sync(FULL, S.my_w, k01 & 31);
-            const uint32_t w10 = __shfl_sync(FULL, S.my_w, (16 + k10) & 31);
-            const uint32_t w11 = __shfl_sync(FULL, S.my_w, (16 + k11) & 31);
-            Vec<SPL> x00, x01, x10, x11;
-            if (k00 >= 0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
-            if (k01 >= 0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
-            if (k10 >= 0) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
-            if (k11 >= 0) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
-            if (k00 >= 0) vrelax<Op, SPL>(d0, x00, w00);
-            if (k01 >= 0) vrelax<Op, SPL>(d0, x01, w01);
-            if (k10 >= 0) vrelax<Op, SPL>(d1, x10, w10);
-            if (k11 >= 0) vrelax<Op, SPL>(d1, x11, w11);
-        }
-    } else {
-        d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, S.a00, S.a01, lane, d0, relax);
-        if (S.two) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, S.a10, S.a11, lane, d1, relax);
-    }
-    const int v0 = (w << 5) + S.b0, v1 = (w << 5) + S.b1;
-    const bool c0 = vless<Op, SPL>(d0, S.e0);
-    if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
-    const bool c1 = S.two && vless<Op, SPL>(d1, S.e1);
-    if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
-    const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
-    uint32_t chg = 0;
-    if (any0) chg |= 1u << S.b0;
-    if (any1) chg |= 1u << S.b1;
-    if (DELTA && (any0 | any1)) {
-        if (S.fast) {
-            const bool mine = lane < 16 ? any0 : any1;
-            if (mine && S.my_x >= 0) atomicOr(&nxt[S.my_x >> 5], 1u << (S.my_x & 31));
-        } else {
-            if (any0) mark_out_range(g, S.o00, S.o01, lane, nxt);
-            if (any1) mark_out_range(g, S.o10, S.o11, lane, nxt);
-        }
-    }
-    return chg;
-}
+// Relaxes the candidate vertices (bits of m) of word w for every slot, in
+// three steps that keep the control work lane-parallel:
+//  A. lane = candidate vertex: walk its in-arcs, test each tail's change bit
+//     (delta pull) and append the changed arcs (u, w) to the lane's slots of
+//     the warp's task queue in shared memory (<= QCAP per vertex, else the
+//     vertex takes the generic path);
+//  B. lane = source slots: for the candidate vertices two at a time, load
+//     their own rows and gather the queued tails' rows (up to four gathers
+//     in flight), min-plus relax, store improved rows, vote;
+//  C. lane = vertex again: every improved vertex marks its out-neighbours in
+//     the next round's candidate bitmap (shared-memory atomicOr).
+// Returns the word's change mask.
+constexpr int QCAP = 16;
 
 template <class Op, bool DELTA, int SPL>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const uint32_t *pchg,
-                                               uint32_t *nxt) {
-    const int vl = (w << 5) + lane;
-    int p_lo = 0, p_hi = 0, q_lo = 0, q_hi = 0;
-    if (vl < g.V) {
-        p_lo = g.in_ptr[vl];
-        p_hi = g.in_ptr[vl + 1];
-        q_lo = g.out_ptr[vl];
-        q_hi = g.out_ptr[vl + 1];
+                                               uint32_t *nxt, int *qu, uint32_t *qw) {
+    constexpr int TSW = 32 * SPL;
+    const int v = (w << 5) + lane;
+    const bool act = (m >> lane) & 1u;
+    int a0 = 0, a1 = 0;
+    if (act) {
+        a0 = g.in_ptr[v];
+        a1 = g.in_ptr[v + 1];
     }
-    uint32_t *Rl = R + lane * SPL;           // this lane's slots of the tile
+    // ---- A: queue this lane's changed in-arcs
+    int c = 0;
+    for (int k = a0; k < a1; ++k) {
+        const int u = g.in_src[k];
+        if (!DELTA || ((pchg[u >> 5] >> (u & 31)) & 1u)) {
+            if (c < QCAP) {
+                qu[lane * QCAP + c] = u;
+                qw[lane * QCAP + c] = g.in_w[k];
+            }
+            ++c;
+        }
+    }
+    relax += (unsigned long long)__reduce_add_sync(FULL, (unsigned)c);
+    __syncwarp();
+    uint32_t todo = __ballot_sync(FULL, c > 0);
+    const uint32_t slow = __ballot_sync(FULL, c > QCAP);
+    uint32_t *Rl = R + lane * SPL;
     uint32_t chg = 0;
-    PairState<SPL> S = load_pair<Op, DELTA, SPL>(g, Rl, w, m, lane, p_lo, p_hi, q_lo, q_hi, pchg);
-    for (;;) {
-        const bool more = m != 0;
-        PairState<SPL> N;
-        if (more) N = load_pair<Op, DELTA, SPL>(g, Rl, w, m, lane, p_lo, p_hi, q_lo, q_hi, pchg);
-        chg |= process_pair<Op, DELTA, SPL>(g, Rl, w, S, lane, relax, pchg, nxt);
-        if (!more) break;
-        S = N;
+    unsigned long long dummy = 0;
+    // ---- B: relax the queued vertices, two per step
+    while (todo) {
+        const int i0 = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const bool two = todo != 0;
+        const int i1 = two ? __ffs(todo) - 1 : i0;
+        if (two) todo &= todo - 1;
+        const int v0 = (w << 5) + i0, v1 = (w << 5) + i1;
+        const Vec<SPL> e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
+        Vec<SPL> e1 = e0;
+        if (two) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
+        Vec<SPL> d0 = e0, d1 = e1;
+        const bool s0 = (slow >> i0) & 1u, s1 = two && ((slow >> i1) & 1u);
+        if (!s0 && !s1) {
+            const int c0 = __shfl_sync(FULL, c, i0);
+            const int c1 = two ? __shfl_sync(FULL, c, i1) : 0;
+            const int *q0 = qu + i0 * QCAP, *q1 = qu + i1 * QCAP;
+            const uint32_t *p0 = qw + i0 * QCAP, *p1 = qw + i1 * QCAP;
+            const int tmax = max(c0, c1);
+            for (int t = 0; t < tmax; t += 2) {
+                Vec<SPL> x00, x01, x10, x11;
+                uint32_t w00 = 0, w01 = 0, w10 = 0, w11 = 0;
+                if (t < c0) { x00 = vload<SPL>(Rl + (size_t)q0[t] * TSW); w00 = p0[t]; }
+                if (t + 1 < c0) { x01 = vload<SPL>(Rl + (size_t)q0[t + 1] * TSW); w01 = p0[t + 1]; }
+                if (t < c1) { x10 = vload<SPL>(Rl + (size_t)q1[t] * TSW); w10 = p1[t]; }
+                if (t + 1 < c1) { x11 = vload<SPL>(Rl + (size_t)q1[t + 1] * TSW); w11 = p1[t + 1]; }
+                if (t < c0) vrelax<Op, SPL>(d0, x00, w00);
+                if (t + 1 < c0) vrelax<Op, SPL>(d0, x01, w01);
+                if (t < c1) vrelax<Op, SPL>(d1, x10, w10);
+                if (t + 1 < c1) vrelax<Op, SPL>(d1, x11, w11);
+            }
+        } else {
+            if (s0) d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i0),
+                                                     __shfl_sync(FULL, a1, i0), lane, d0, dummy);
+            else {
+                const int c0 = __shfl_sync(FULL, c, i0);
+                for (int t = 0; t < c0; ++t) vrelax<Op, SPL>(d0, vload<SPL>(Rl + (size_t)qu[i0 * QCAP + t] * TSW), qw[i0 * QCAP + t]);
+            }
+            if (two) {
+                if (s1) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i1),
+                                                         __shfl_sync(FULL, a1, i1), lane, d1, dummy);
+                else {
+                    const int c1 = __shfl_sync(FULL, c, i1);
+                    for (int t = 0; t < c1; ++t) vrelax<Op, SPL>(d1, vload<SPL>(Rl + (size_t)qu[i1 * QCAP + t] * TSW), qw[i1 * QCAP + t]);
+                }
+            }
+        }
+        const bool c0 = vless<Op, SPL>(d0, e0);
+        if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
+        const bool c1 = two && vless<Op, SPL>(d1, e1);
+        if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
+        if (__any_sync(FULL, c0)) chg |= 1u << i0;
+        if (__any_sync(FULL, c1)) chg |= 1u << i1;
     }
+    // ---- C: improved vertices mark their out-neighbours, lane-parallel
+    if (DELTA && ((chg >> lane) & 1u)) {
+        const int o1 = g.out_ptr[v + 1];
+        for (int e = g.out_ptr[v]; e < o1; ++e) {
+            const int x = g.out_dst[e];
+            atomicOr(&nxt[x >> 5], 1u << (x & 31));
+        }
+    }
+    __syncwarp();   // the queue is reused by the warp's next word
     return chg;
 }
 
@@ -388,6 +337,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         if (tile >= ntiles) break;
         uint32_t *R = rows + (size_t)tile * V * TSW;
         uint32_t *cur = smem, *nxt = smem + NW, *pchg = smem + 2 * NW, *cchg = smem + 3 * NW;
+        int *qu = reinterpret_cast<int *>(smem + 4 * NW) + warp * (32 * QCAP * 2);
+        uint32_t *qw = reinterpret_cast<uint32_t *>(qu + 32 * QCAP);
 
         // init: every row INF, bitmaps empty
         {
@@ -431,7 +382,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 if (m) {
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt);
+                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt, qu, qw);
                     any |= c != 0;
                 }
                 if (!DENSE && lane == 0 && cchg[w] != c) cchg[w] = c;   // also clears stale words
@@ -461,6 +412,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 template <class Op, bool DENSE, int NT, int MINB, int SPL>
 static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
     auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL>;
+    smem += (size_t)(NT / 32) * 32 * QCAP * 2 * sizeof(int);   // task queues (u, w) per warp
     WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, nsm = 0;
     WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
@@ -500,10 +452,11 @@ template <class Op>
 static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
     const int V = g->V;
     const int NW = (V + 31) / 32;
+    // 4 bitmaps; launch_shape adds the per-warp task queues
     const size_t smem = (size_t)4 * NW * sizeof(uint32_t);
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    if (smem + 1024 > (size_t)max_optin)
+    if (smem + (size_t)16 * 32 * QCAP * 2 * sizeof(int) + 1024 > (size_t)max_optin)
         WR_THROW(WR_ETOOLARGE, "bf: V too large for the shared-memory frontier bitmaps");
     const bool dense = run.variant == WR_BF_DENSE;
     switch (run.spl) {
