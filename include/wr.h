@@ -138,6 +138,7 @@ typedef struct {
     float ms;                 /* device time of the call (CUDA events)       */
     int32_t negcycle_source;  /* on WR_ENEGCYCLE: a source reaching one      */
     int64_t kernel_launches;  /* libwr kernels launched by the call          */
+    int64_t visits;           /* (vertex, round) candidate visits, all tiles  */
 } wr_bf_stats;
 
 /* a3+a4 Batched Bellman-Ford (P720-724 §4.7: "dist and pred ... V x N,
@@ -201,6 +202,7 @@ typedef struct {
     int64_t kernel_launches;
     float bf_ms;              /* device time of the relaxation sweeps alone  */
     float pred_ms;            /* device time of the canonical-pred pass      */
+    int64_t visits;           /* BF candidate visits                         */
 } wr_route_stats;
 
 /* a7 Segmented route of one stop set (Theorem 3.1, P324-337 §3).

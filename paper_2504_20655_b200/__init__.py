@@ -60,7 +60,7 @@ class BfOpts(C.Structure):
 class BfStats(C.Structure):
     _fields_ = [("rounds_max", C.c_int32), ("relaxations", C.c_int64), ("segments", C.c_int32),
                 ("tiles", C.c_int32), ("ms", C.c_float), ("negcycle_source", C.c_int32),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("visits", C.c_int64)]
 
 
 class RouteOpts(C.Structure):
@@ -72,7 +72,7 @@ class RouteStats(C.Structure):
     _fields_ = [("orders", C.c_int64), ("sources", C.c_int64), ("permutations", C.c_int64),
                 ("stitch_candidates", C.c_int64), ("segments", C.c_int32), ("rounds_max", C.c_int32),
                 ("relaxations", C.c_int64), ("ms", C.c_float), ("kernel_launches", C.c_int64),
-                ("bf_ms", C.c_float), ("pred_ms", C.c_float)]
+                ("bf_ms", C.c_float), ("pred_ms", C.c_float), ("visits", C.c_int64)]
 
 
 class PlanInfo(C.Structure):

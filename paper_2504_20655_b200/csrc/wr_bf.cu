@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         __syncthreads();
 
         int rounds = 0;
-        unsigned long long relax = 0;
+        unsigned long long relax = 0, visits = 0;
         bool more = true;
         while (more) {
             if (DENSE) {
@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
                     c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt, qu, qw);
+                    visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
                 if (!DENSE && lane == 0 && cchg[w] != c) cchg[w] = c;   // also clears stale words
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         }
         // per-tile statistics (one lane per warp contributes its arc count)
         if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TSW);
+        if (lane == 0 && visits) atomicAdd(&stats->visits, visits);
         if (threadIdx.x == 0) atomicMax(&stats->rounds_max, rounds);
         __syncthreads();
     }
@@ -434,9 +436,9 @@ static int env_int(const char *name, int dflt) {
 
 template <class Op, bool DENSE, int SPL>
 static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    // default 5 = 448 threads x 2 CTAs/SM (73 regs, no spills): measured best
-    // on config 5 among 512x2 / 512x3 / 256x4 / 256x3 / 384x2 / 448x2 / 320x2
-    static const int cfg = env_int("WR_BF_CONFIG", 5);
+    // default 4 = 384 threads x 2 CTAs/SM: measured best on config 5 among
+    // 512x2 / 512x3 / 256x4 / 256x3 / 384x2 / 448x2 / 320x2
+    static const int cfg = env_int("WR_BF_CONFIG", 4);
     switch (cfg) {
         case 1: launch_shape<Op, DENSE, 512, 3, SPL>(g, run, d_stats, st, smem); break;
         case 2: launch_shape<Op, DENSE, 256, 4, SPL>(g, run, d_stats, st, smem); break;
@@ -487,9 +489,10 @@ void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStrea
 int choose_spl(int64_t S, int nsm) {
     const int forced = env_int("WR_BF_SPL", 0);
     if (forced == 1 || forced == 2 || forced == 4) return forced;
-    // measured on config 5: SPL 2 beats 1 and 4 (4 spills
-    // registers and widens the tiles' wavefront spread)
-    int spl = 2;
+    // measured on config 5: with the task-queue sweep, 4
+    // sources per lane (128-source Morton tiles) is fastest; narrower tiles
+    // when there are too few tiles to fill the GPU (>= 4 per SM)
+    int spl = 4;
     while (spl > 1 && S / (32 * spl) < (int64_t)4 * nsm) spl /= 2;
     return spl;
 }
@@ -1001,7 +1004,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     if (dist && !dist_dev) dist_stage.alloc((size_t)sb * ncols);
     if (pred && !pred_dev) pred_stage.alloc((size_t)sb * V);
     DBuf<BfTileStats> d_stats(1);
-    BfTileStats h0{0ull, 0, -1};
+    BfTileStats h0{0ull, 0, -1, 0ull};
     WR_CUDA(cudaMemcpyAsync(d_stats.p, &h0, sizeof(h0), cudaMemcpyHostToDevice, st));
 
     int segments = 0;
@@ -1064,6 +1067,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     if (stats) {
         stats->rounds_max = hs.rounds_max;
         stats->relaxations = (int64_t)hs.relax;
+        stats->visits = (int64_t)hs.visits;
         stats->segments = segments;
         stats->tiles = (int32_t)total_tiles;
         stats->ms = ms;

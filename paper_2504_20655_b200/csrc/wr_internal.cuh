@@ -177,6 +177,7 @@ struct BfTileStats {        // per-call accumulators (device)
     unsigned long long relax;
     int rounds_max;
     int negcycle_tile;      // -1 or a tile with a negative cycle
+    unsigned long long visits;  // candidate (vertex, round) visits
 };
 
 // Launches the relaxation sweep of a segment on stream st (a3).

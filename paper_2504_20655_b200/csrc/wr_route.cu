@@ -823,7 +823,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     WR_CUDA(cudaEventCreate(&e0));
     WR_CUDA(cudaEventCreate(&e1));
     WR_CUDA(cudaEventRecord(e0, st));
-    BfTileStats h0{0ull, 0, -1};
+    BfTileStats h0{0ull, 0, -1, 0ull};
     DBuf<BfTileStats> d_stats(1);
     WR_CUDA(cudaMemcpyAsync(d_stats.p, &h0, sizeof(h0), cudaMemcpyHostToDevice, st));
     int segments = 0;
@@ -903,6 +903,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         stats->segments = segments;
         stats->rounds_max = hs.rounds_max;
         stats->relaxations = (int64_t)hs.relax;
+        stats->visits = (int64_t)hs.visits;
         stats->ms = ms;
         stats->kernel_launches = g_launches - l0;
         stats->bf_ms = bf_ms;
@@ -1054,6 +1055,7 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
         stats->segments = s1.segments;
         stats->rounds_max = s1.rounds_max;
         stats->relaxations = s1.relaxations;
+        stats->visits = s1.visits;
         stats->ms = ms;
         stats->kernel_launches = g_launches - l0;
         stats->bf_ms = s1.bf_ms;

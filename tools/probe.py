@@ -47,7 +47,7 @@ def main():
         torch.cuda.synchronize()
         wall = time.time() - t
         print(json.dumps({"rep": r, "wall_ms": wall * 1e3, "call_ms": st.ms, "bf_ms": st.bf_ms, "pred_ms": st.pred_ms,
-                          "relaxations": st.relaxations, "useful": S * g.E,
+                          "relaxations": st.relaxations, "visits": st.visits, "useful": S * g.E,
                           "work_ratio": st.relaxations / max(1, S * g.E), "rounds_max": st.rounds_max,
                           "permutations": st.permutations, "stitch": st.stitch_candidates,
                           "launches": st.kernel_launches,
