@@ -308,12 +308,21 @@ def main():
     E = g.E
     useful = S * E                                    # graph500 convention: each arc once per source
     # roofline of the dominant kernel (the relaxation sweep): algorithmic bytes
-    # per launch = per-source compulsory traffic:
-    # write the source's V distances once (4V) + read each arc (u, w) once per
-    # 32-source tile (8E/32) + CSR out-arc read once per tile (4E/32).
-    alg_bytes = S * (4 * g.V) + (S / 32.0) * (12 * E)
+    # per launch = compulsory traffic: write each
+    # source's V distances once (4V per source) + read the graph (in-arcs
+    # (u, w) 8E, out-arcs 4E, offsets 8V) once per 128-source tile.
+    alg_bytes = S * (4 * g.V) + (S / 128.0) * (12 * E + 8 * g.V)
     bf_s = bf_step_ms / 1e3
     achieved = alg_bytes / bf_s / 1e9 if bf_s > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):   # DRAM bytes per launch from the committed ncu --set full capture
+        traffic = json.load(open(tpath)).get("bf_frontier_kernel", {}).get("dram_bytes")
+    # ALU view: one DPX add+min (VIADDMNMX, ALU pipe: 64 lanes/clk/SM) per
+    # useful relaxation, at the clock seen under load
+    clk = (ck.get("sm_mhz") or 1965.0) * 1e6
+    alu_peak = 148 * 64 * clk
+    alu_ach = useful / bf_s if bf_s > 0 else None
     line = {
         "metric": METRIC, "value": B / (ms / 1e3), "unit": "orders/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -326,8 +335,14 @@ def main():
                                   "unit": "edges/s", "convention": "useful = S*E (one traversal of every arc per source)"},
         "bf_ms_per_step": bf_step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak if achieved else None, "traffic": None,
-                     "kernel": "bf_frontier_kernel", "peak_kind": peak_kind},
+                     "frac": achieved / hbm_peak if achieved else None,
+                     "traffic": traffic / 1e9 if traffic else None, "traffic_unit": "GB per launch",
+                     "algorithmic_gb_per_launch": alg_bytes / 1e9,
+                     "kernel": "bf_frontier_kernel", "peak_kind": peak_kind,
+                     "note": "latency-bound frontier sweep; see DESIGN.md section 9"},
+        "roofline_alu": {"bound": "alu", "achieved": alu_ach / 1e12 if alu_ach else None,
+                         "peak": alu_peak / 1e12, "unit": "T relaxations/s",
+                         "frac": alu_ach / alu_peak if alu_ach else None},
         "gpu_launches": int(launches[0]),
         "clocks": ck,
         "e2e": e2e,

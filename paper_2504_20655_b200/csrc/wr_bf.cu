@@ -214,7 +214,7 @@ constexpr int QCAP = 16;
 template <class Op, bool DELTA, int SPL>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const uint32_t *pchg,
-                                               uint32_t *nxt, int *qu, uint32_t *qw) {
+                                               uint32_t *nxt, int *qu, uint32_t *qw, uint32_t *touched) {
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
@@ -238,6 +238,12 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     relax += (unsigned long long)__reduce_add_sync(FULL, (unsigned)c);
     __syncwarp();
     uint32_t todo = __ballot_sync(FULL, c > 0);
+    // rows are written lazily: a vertex never improved so far holds no row
+    // yet and reads as INF (its first improvement writes the whole row)
+    const uint32_t tw = DELTA ? touched[w] : FULL;
+    Vec<SPL> infv;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) infv.x[j] = Op::INF;
     const uint32_t slow = __ballot_sync(FULL, c > QCAP);
     uint32_t *Rl = R + lane * SPL;
     uint32_t chg = 0;
@@ -250,9 +256,9 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         const int i1 = two ? __ffs(todo) - 1 : i0;
         if (two) todo &= todo - 1;
         const int v0 = (w << 5) + i0, v1 = (w << 5) + i1;
-        const Vec<SPL> e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
-        Vec<SPL> e1 = e0;
-        if (two) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
+        Vec<SPL> e0 = infv, e1 = infv;
+        if ((tw >> i0) & 1u) e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
+        if (two && ((tw >> i1) & 1u)) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
         Vec<SPL> d0 = e0, d1 = e1;
         const bool s0 = (slow >> i0) & 1u, s1 = two && ((slow >> i1) & 1u);
         if (!s0 && !s1) {
@@ -289,13 +295,16 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
                 }
             }
         }
+        // first write of a row covers every slot (untouched slots stay INF)
+        const bool f0 = !((tw >> i0) & 1u), f1 = two && !((tw >> i1) & 1u);
         const bool c0 = vless<Op, SPL>(d0, e0);
-        if (c0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
+        if (c0 || f0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
         const bool c1 = two && vless<Op, SPL>(d1, e1);
-        if (c1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
+        if (c1 || f1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
         if (__any_sync(FULL, c0)) chg |= 1u << i0;
         if (__any_sync(FULL, c1)) chg |= 1u << i1;
     }
+    if (DELTA && lane == 0 && (chg & ~tw)) touched[w] = tw | chg;   // this warp owns word w
     // ---- C: improved vertices mark their out-neighbours, lane-parallel
     if (DELTA && ((chg >> lane) & 1u)) {
         const int o1 = g.out_ptr[v + 1];
@@ -337,19 +346,34 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         if (tile >= ntiles) break;
         uint32_t *R = rows + (size_t)tile * V * TSW;
         uint32_t *cur = smem, *nxt = smem + NW, *pchg = smem + 2 * NW, *cchg = smem + 3 * NW;
-        int *qu = reinterpret_cast<int *>(smem + 4 * NW) + warp * (32 * QCAP * 2);
+        uint32_t *touched = smem + 4 * NW;   // vertices whose row has been written
+        int *qu = reinterpret_cast<int *>(smem + 5 * NW) + warp * (32 * QCAP * 2);
         uint32_t *qw = reinterpret_cast<uint32_t *>(qu + 32 * QCAP);
 
-        // init: every row INF, bitmaps empty
+        // init: bitmaps empty; rows INF (dense) or written lazily (frontier:
+        // a row is written whole on its vertex's first improvement, and the
+        // rows of vertices never reached are filled with INF at the end)
+        const uint4 inf4 = make_uint4(Op::INF, Op::INF, Op::INF, Op::INF);
         {
-            uint4 inf4 = make_uint4(Op::INF, Op::INF, Op::INF, Op::INF);
-            uint4 *R4 = reinterpret_cast<uint4 *>(R);
-            const size_t n4 = (size_t)V * (TSW / 4);
-            for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
-            for (int w = threadIdx.x; w < 4 * NW; w += NT) smem[w] = 0u;
+            if (DENSE) {
+                uint4 *R4 = reinterpret_cast<uint4 *>(R);
+                const size_t n4 = (size_t)V * (TSW / 4);
+                for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
+            }
+            for (int w = threadIdx.x; w < 5 * NW; w += NT) smem[w] = 0u;
         }
         __syncthreads();
         if (warp == 0) {   // seed: d[s][slot] = 0; the sources "changed" in round 0
+            if (!DENSE) {  // the seed vertices' rows: INF everywhere first
+                for (int k = 0; k < TSW; ++k) {
+                    const int s = tile_src[tile * TSW + k];
+                    if (s >= 0) {
+                        uint32_t *row = R + (size_t)s * TSW;
+                        for (int q = lane; q < TSW / 4; q += 32) reinterpret_cast<uint4 *>(row)[q] = inf4;
+                    }
+                }
+                __syncwarp();
+            }
 #pragma unroll
             for (int j = 0; j < SPL; ++j) {
                 const int slot = lane * SPL + j;
@@ -357,6 +381,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 if (s >= 0) {
                     R[(size_t)s * TSW + slot] = Op::ZERO;
                     atomicOr(&pchg[s >> 5], 1u << (s & 31));
+                    atomicOr(&touched[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
                         const int x = g.out_dst[e];
                         atomicOr(&cur[x >> 5], 1u << (x & 31));
@@ -382,7 +407,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 if (m) {
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt, qu, qw);
+                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt, qu, qw, touched);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
@@ -399,6 +424,17 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             if (more && rounds >= max_rounds) {
                 if (threadIdx.x == 0) atomicMax(&stats->negcycle_tile, tile);
                 more = false;
+            }
+        }
+        if (!DENSE) {   // vertices never reached: their rows read INF
+            for (int w = warp; w < NW; w += NWARPS) {
+                uint32_t um = ~touched[w] & (w == NW - 1 ? last_mask : FULL);
+                while (um) {
+                    const int b = __ffs(um) - 1;
+                    um &= um - 1;
+                    uint4 *row = reinterpret_cast<uint4 *>(R + (size_t)((w << 5) + b) * TSW);
+                    for (int q = lane; q < TSW / 4; q += 32) row[q] = inf4;
+                }
             }
         }
         // per-tile statistics (one lane per warp contributes its arc count)
@@ -455,7 +491,7 @@ static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     const int V = g->V;
     const int NW = (V + 31) / 32;
     // 4 bitmaps; launch_shape adds the per-warp task queues
-    const size_t smem = (size_t)4 * NW * sizeof(uint32_t);
+    const size_t smem = (size_t)5 * NW * sizeof(uint32_t);
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem + (size_t)16 * 32 * QCAP * 2 * sizeof(int) + 1024 > (size_t)max_optin)
@@ -582,37 +618,38 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
-// a4 canonical pred, vectorised over the tile: warp per (tile, 32 vertices),
+// a4 canonical pred, vectorised over the tile: warp per (tile, 8 vertices),
 // lane = SPL source slots. In-arcs are sorted by tail, so the first steep
 // tight in-arc met is the smallest-tail one: the arc loop stops as soon as
 // every slot that needs a predecessor has one. Results are staged in shared
-// memory and written as one 128-B segment per source row.
-template <int SPL>
+// memory and written as one full 32-B sector per source row (8 vertices x
+// 4 B), 4 rows per store instruction.
 struct PredShape {
-    static constexpr int WARPS = SPL == 4 ? 2 : 4;   // static smem staging <= 48 KB
+    static constexpr int WARPS = 8;
+    static constexpr int PV = 8;     // vertices per warp job
 };
 
 template <class Op, int SPL>
-__global__ void __launch_bounds__(PredShape<SPL>::WARPS * 32) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
+__global__ void __launch_bounds__(PredShape::WARPS * 32) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
                                                       const uint32_t *__restrict__ rows,
                                                       const int *__restrict__ slot_row, int64_t out_row0,
                                                       int32_t *pred_out, int *flat_tiles) {
     constexpr int TSW = 32 * SPL;
-    constexpr int PW = PredShape<SPL>::WARPS;
-    __shared__ int32_t sp[PW][32][TSW + 1];
+    constexpr int PW = PredShape::WARPS, PV = PredShape::PV;
+    __shared__ int32_t sp[PW][PV][TSW + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int V = g.V;
-    const int chunks = (V + 31) / 32;
+    const int chunks = (V + PV - 1) / PV;
     const int64_t job = (int64_t)blockIdx.x * PW + warp;
     if (job >= (int64_t)ntiles * chunks) return;
     const int tile = (int)(job / chunks);
-    const int c0 = (int)(job % chunks) * 32;
+    const int c0 = (int)(job % chunks) * PV;
     const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
     int src[SPL];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) src[j] = tile_src[tile * TSW + lane * SPL + j];
     bool flat = false;
-    const int nv = min(32, V - c0);
+    const int nv = min(PV, V - c0);
     int p_lo = 0, p_hi = 0;
     if (lane < nv) {
         p_lo = g.in_ptr[c0 + lane];
@@ -707,11 +744,13 @@ __global__ void __launch_bounds__(PredShape<SPL>::WARPS * 32) bf_pred_kernel(Dev
         }
     }
     __syncwarp();
-    for (int s = 0; s < TSW; ++s) {
-        const int sl = tile * TSW + s;
-        if (tile_src[sl] < 0) break;
-        const int64_t row = out_row0 + (slot_row ? slot_row[sl] : sl);
-        if (lane < nv) pred_out[row * (int64_t)V + c0 + lane] = sp[warp][lane][s];
+    for (int s0 = 0; s0 < TSW; s0 += 32 / PV) {
+        const int sl_in = s0 + lane / PV, jv = lane % PV;
+        const int sl = tile * TSW + sl_in;
+        if (jv < nv && tile_src[sl] >= 0) {
+            const int64_t row = out_row0 + (slot_row ? slot_row[sl] : sl);
+            pred_out[row * (int64_t)V + c0 + jv] = sp[warp][jv][sl_in];
+        }
     }
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
@@ -719,16 +758,18 @@ __global__ void __launch_bounds__(PredShape<SPL>::WARPS * 32) bf_pred_kernel(Dev
 template <class Op>
 static void launch_pred(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
                         cudaStream_t st) {
-    const int64_t jobs = (int64_t)run.ntiles * ((g->V + 31) / 32);
+    const int64_t jobs = (int64_t)run.ntiles * ((g->V + PredShape::PV - 1) / PredShape::PV);
+    const unsigned grid = (unsigned)((jobs + PredShape::WARPS - 1) / PredShape::WARPS);
+    const int nt = PredShape::WARPS * 32;
     if (run.spl == 2)
-        bf_pred_kernel<Op, 2><<<(unsigned)((jobs + 3) / 4), 128, 0, st>>>(
-            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+        bf_pred_kernel<Op, 2><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
+                                                   out_row0, pred_out, flat);
     else if (run.spl == 4)
-        bf_pred_kernel<Op, 4><<<(unsigned)((jobs + 1) / 2), 64, 0, st>>>(
-            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+        bf_pred_kernel<Op, 4><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
+                                                   out_row0, pred_out, flat);
     else
-        bf_pred_kernel<Op, 1><<<(unsigned)((jobs + 3) / 4), 128, 0, st>>>(
-            g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+        bf_pred_kernel<Op, 1><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
+                                                   out_row0, pred_out, flat);
     count_launch();
     WR_LAUNCH_CHECK();
 }
