@@ -210,7 +210,7 @@ def main():
     d_res = torch.empty((max(n_my, 1), wr.RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
     pred_buf = None
     if not a.no_pred:
-        pred_buf = torch.empty((max(int(info.src_hi), 1), g.V), dtype=torch.int32, device=dev)
+        pred_buf = torch.empty((max(int(info.src_hi - info.src_lo), 1), g.V), dtype=torch.int32, device=dev)
     send = torch.empty(info.max_send, dtype=torch.int32, device=dev)
     gathered = torch.empty(world * info.max_send, dtype=torch.int32, device=dev) if world > 1 else send
     plan0.close()

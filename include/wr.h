@@ -174,11 +174,12 @@ typedef struct {
                              /* K = m O8 clusters when labels are not given */
     int64_t chunk;           /* permutations per chunk (O6); 0 = 2,903,040  */
     int64_t hbm_budget;      /* as in wr_bf_opts                            */
-    int32_t *pred_out;       /* optional DEVICE S x V int32: canonical pred
-                                (O3) of every BF source, row = index of the
-                                source in the ascending distinct-stop list;
-                                a sharded rank writes its own block of rows */
-    int64_t pred_rows;       /* rows available in pred_out (>= S)           */
+    int32_t *pred_out;       /* optional DEVICE int32 rows of V: canonical
+                                pred (O3) of this call's BF sources, row =
+                                index of the source in the ascending
+                                distinct-stop list minus the rank's src_lo
+                                (world 1: 0..S-1; rank r: its own block)    */
+    int64_t pred_rows;       /* rows available in pred_out (>= src_hi-src_lo) */
 } wr_route_opts;
 
 typedef struct {

@@ -294,7 +294,8 @@ def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, r
     """a2..a7: route every order. Returns (results, stats); results is a
     RESULT_DTYPE numpy array unless a device buffer is passed. pred_out: an
     optional device int32 tensor (>= S rows x V) receiving the canonical
-    predecessor rows (a4) of the distinct stops in ascending order."""
+    predecessor rows (a4) of the distinct stops in ascending order
+    (OrdersPlan: the rank's own block of sources, row 0 = its src_lo)."""
     ptr = _arr(order_ptr, np.int64)
     nodes = _arr(order_nodes, np.int32)
     B = int(ptr.shape[0]) - 1

@@ -828,8 +828,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     WR_CUDA(cudaMemcpyAsync(d_stats.p, &h0, sizeof(h0), cudaMemcpyHostToDevice, st));
     int segments = 0;
     float bf_ms = 0.f, pred_ms = 0.f;
-    if (o.pred_out && (!is_device_ptr(o.pred_out) || o.pred_rows < P->src_hi))
-        return fail(WR_EINVAL, "wr_orders_local: pred_out must be device memory with >= S rows");
+    if (o.pred_out && (!is_device_ptr(o.pred_out) || o.pred_rows < P->src_hi - P->src_lo))
+        return fail(WR_EINVAL, "wr_orders_local: pred_out must be device memory with >= src_hi-src_lo rows");
     if (nsrc > 0) {
         wr_graph_info_t gi;
         wr_graph_info(g, &gi);
@@ -860,14 +860,14 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventRecord(b1, st));
             if (o.pred_out) {   // a4 canonical pred of this segment's sources
                 WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
-                bf_write_outputs(g, run, lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
+                bf_write_outputs(g, run, lo - P->src_lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
                 std::vector<int> hflat(ntiles);
                 WR_CUDA(cudaMemcpyAsync(hflat.data(), flat.p, sizeof(int) * ntiles, cudaMemcpyDeviceToHost, st));
                 WR_CUDA(cudaStreamSynchronize(st));
                 std::vector<int> todo;
                 for (int t = 0; t < ntiles; ++t)
                     if (hflat[t] || g->has_negative) todo.push_back(t);
-                bf_resolve_flat(g, run, todo, lo, o.pred_out, st);
+                bf_resolve_flat(g, run, todo, lo - P->src_lo, o.pred_out, st);
             }
             WR_CUDA(cudaEventRecord(b2, st));
             WR_CUDA(cudaEventSynchronize(b2));

@@ -273,6 +273,32 @@ def G_disconnected():
     return G(4, [0, 1, 2, 3], [1, 0, 3, 2], np.array([1, 1, 1, 1], np.int32))
 
 
+def test_route_orders_pred_rows():
+    """a4 inside the orders path: pred rows of the distinct stops (ascending)
+    equal the oracle's canonical predecessor; sharded ranks fill their own
+    blocks and concatenate to the same matrix."""
+    g, orders, _ = gen.config(3, wtype="f32", B=600)
+    G = wr.Graph.from_gen(g)
+    stops = np.unique(orders.order_nodes)
+    pred = torch.full((stops.size, g.V), -7, dtype=torch.int32, device="cuda")
+    wr.route_orders(G, orders.order_ptr, orders.order_nodes, pred_out=pred)
+    P = pred.cpu().numpy()
+    rows = oracle.bf_many(g, stops[::50])
+    for k, i in enumerate(range(0, stops.size, 50)):
+        assert np.array_equal(P[i], oracle.pred(g, int(stops[i]), rows[k]))
+    world = 3
+    parts = []
+    for r in range(world):
+        plan = wr.OrdersPlan(G, orders.order_ptr, orders.order_nodes, r, world)
+        n = plan.info.src_hi - plan.info.src_lo
+        pr = torch.full((max(n, 1), g.V), -7, dtype=torch.int32, device="cuda")
+        plan = wr.OrdersPlan(G, orders.order_ptr, orders.order_nodes, r, world, pred_out=pr)
+        send = torch.zeros(plan.info.max_send, dtype=torch.int32, device="cuda")
+        plan.local(send)
+        parts.append(pr.cpu().numpy()[:n])
+    assert np.array_equal(np.concatenate(parts), P)
+
+
 def test_route_orders_budget_and_chunk_invariance():
     g, orders, _ = gen.config(3, B=2048)
     G = wr.Graph.from_gen(g)
