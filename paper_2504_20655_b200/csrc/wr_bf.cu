@@ -209,12 +209,19 @@ __device__ __forceinline__ void mark_out_range(const DevGraph &g, int o0, int o1
 //  C. lane = vertex again: every improved vertex marks its out-neighbours in
 //     the next round's candidate bitmap (shared-memory atomicOr).
 // Returns the word's change mask.
+// Task-queue capacity per vertex: per-warp queues of 32 x QCAP packed
+// (u, w) pairs, either after the bitmaps in dynamic shared memory or in a
+// static array (compile-time address; capacity limited by the 48 KB static
+// budget: qcap_for(NT)).
 constexpr int QCAP = 16;
+__host__ __device__ constexpr int qcap_for(int nt) {
+    return ((46 * 1024) / (nt * 8)) >= 16 ? 16 : (((46 * 1024) / (nt * 8)) & ~1);
+}
 
-template <class Op, bool DELTA, int SPL>
+template <class Op, bool DELTA, int SPL, int QC>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const uint32_t *pchg,
-                                               uint32_t *nxt, int *qu, uint32_t *qw, uint32_t *touched) {
+                                               uint32_t *nxt, int2 *q, uint32_t *touched) {
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
@@ -228,10 +235,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     for (int k = a0; k < a1; ++k) {
         const int u = g.in_src[k];
         if (!DELTA || ((pchg[u >> 5] >> (u & 31)) & 1u)) {
-            if (c < QCAP) {
-                qu[lane * QCAP + c] = u;
-                qw[lane * QCAP + c] = g.in_w[k];
-            }
+            if (c < QC) q[lane * QC + c] = make_int2(u, (int)g.in_w[k]);
             ++c;
         }
     }
@@ -244,7 +248,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     Vec<SPL> infv;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) infv.x[j] = Op::INF;
-    const uint32_t slow = __ballot_sync(FULL, c > QCAP);
+    const uint32_t slow = __ballot_sync(FULL, c > QC);
     uint32_t *Rl = R + lane * SPL;
     uint32_t chg = 0;
     unsigned long long dummy = 0;
@@ -264,34 +268,43 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         if (!s0 && !s1) {
             const int c0 = __shfl_sync(FULL, c, i0);
             const int c1 = two ? __shfl_sync(FULL, c, i1) : 0;
-            const int *q0 = qu + i0 * QCAP, *q1 = qu + i1 * QCAP;
-            const uint32_t *p0 = qw + i0 * QCAP, *p1 = qw + i1 * QCAP;
+            const int2 *q0 = q + i0 * QC, *q1 = q + i1 * QC;
             const int tmax = max(c0, c1);
             for (int t = 0; t < tmax; t += 2) {
                 Vec<SPL> x00, x01, x10, x11;
-                uint32_t w00 = 0, w01 = 0, w10 = 0, w11 = 0;
-                if (t < c0) { x00 = vload<SPL>(Rl + (size_t)q0[t] * TSW); w00 = p0[t]; }
-                if (t + 1 < c0) { x01 = vload<SPL>(Rl + (size_t)q0[t + 1] * TSW); w01 = p0[t + 1]; }
-                if (t < c1) { x10 = vload<SPL>(Rl + (size_t)q1[t] * TSW); w10 = p1[t]; }
-                if (t + 1 < c1) { x11 = vload<SPL>(Rl + (size_t)q1[t + 1] * TSW); w11 = p1[t + 1]; }
-                if (t < c0) vrelax<Op, SPL>(d0, x00, w00);
-                if (t + 1 < c0) vrelax<Op, SPL>(d0, x01, w01);
-                if (t < c1) vrelax<Op, SPL>(d1, x10, w10);
-                if (t + 1 < c1) vrelax<Op, SPL>(d1, x11, w11);
+                int2 t00 = make_int2(0, 0), t01 = t00, t10 = t00, t11 = t00;
+                if (t < c0) t00 = q0[t];
+                if (t + 1 < c0) t01 = q0[t + 1];
+                if (t < c1) t10 = q1[t];
+                if (t + 1 < c1) t11 = q1[t + 1];
+                if (t < c0) x00 = vload<SPL>(Rl + (size_t)t00.x * TSW);
+                if (t + 1 < c0) x01 = vload<SPL>(Rl + (size_t)t01.x * TSW);
+                if (t < c1) x10 = vload<SPL>(Rl + (size_t)t10.x * TSW);
+                if (t + 1 < c1) x11 = vload<SPL>(Rl + (size_t)t11.x * TSW);
+                if (t < c0) vrelax<Op, SPL>(d0, x00, (uint32_t)t00.y);
+                if (t + 1 < c0) vrelax<Op, SPL>(d0, x01, (uint32_t)t01.y);
+                if (t < c1) vrelax<Op, SPL>(d1, x10, (uint32_t)t10.y);
+                if (t + 1 < c1) vrelax<Op, SPL>(d1, x11, (uint32_t)t11.y);
             }
         } else {
             if (s0) d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i0),
                                                      __shfl_sync(FULL, a1, i0), lane, d0, dummy);
             else {
                 const int c0 = __shfl_sync(FULL, c, i0);
-                for (int t = 0; t < c0; ++t) vrelax<Op, SPL>(d0, vload<SPL>(Rl + (size_t)qu[i0 * QCAP + t] * TSW), qw[i0 * QCAP + t]);
+                for (int t = 0; t < c0; ++t) {
+                    const int2 tk = q[i0 * QC + t];
+                    vrelax<Op, SPL>(d0, vload<SPL>(Rl + (size_t)tk.x * TSW), (uint32_t)tk.y);
+                }
             }
             if (two) {
                 if (s1) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i1),
                                                          __shfl_sync(FULL, a1, i1), lane, d1, dummy);
                 else {
                     const int c1 = __shfl_sync(FULL, c, i1);
-                    for (int t = 0; t < c1; ++t) vrelax<Op, SPL>(d1, vload<SPL>(Rl + (size_t)qu[i1 * QCAP + t] * TSW), qw[i1 * QCAP + t]);
+                    for (int t = 0; t < c1; ++t) {
+                        const int2 tk = q[i1 * QC + t];
+                        vrelax<Op, SPL>(d1, vload<SPL>(Rl + (size_t)tk.x * TSW), (uint32_t)tk.y);
+                    }
                 }
             }
         }
@@ -325,13 +338,15 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 // barrier. Word w of every bitmap is written by one warp only (w mod warps).
 // Dense variant: every vertex is a candidate every round, all arcs pulled
 // (the paper's edge-parallel class of work).
-template <class Op, bool DENSE, int NT, int MINB, int SPL>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
                                                                BfTileStats *stats) {
     constexpr int TSW = 32 * SPL;
+    constexpr int QC = SQ ? qcap_for(NT) : QCAP;
     extern __shared__ uint32_t smem[];
+    __shared__ int2 s_queue[SQ ? NT / 32 : 1][SQ ? 32 * QC : 1];
     const int V = g.V;
     const int NW = (V + 31) >> 5;
     __shared__ int s_tile;
@@ -347,8 +362,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         uint32_t *R = rows + (size_t)tile * V * TSW;
         uint32_t *cur = smem, *nxt = smem + NW, *pchg = smem + 2 * NW, *cchg = smem + 3 * NW;
         uint32_t *touched = smem + 4 * NW;   // vertices whose row has been written
-        int *qu = reinterpret_cast<int *>(smem + 5 * NW) + warp * (32 * QCAP * 2);
-        uint32_t *qw = reinterpret_cast<uint32_t *>(qu + 32 * QCAP);
+        int2 *q = SQ ? &s_queue[warp][0]
+                     : reinterpret_cast<int2 *>(smem + ((5 * NW + 1) & ~1)) + warp * (32 * QC);   // 8-B aligned
 
         // init: bitmaps empty; rows INF (dense) or written lazily (frontier:
         // a row is written whole on its vertex's first improvement, and the
@@ -407,7 +422,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 if (m) {
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    c = relax_word<Op, !DENSE, SPL>(g, R, w, m, lane, relax, pchg, nxt, qu, qw, touched);
+                    c = relax_word<Op, !DENSE, SPL, QC>(g, R, w, m, lane, relax, pchg, nxt, q, touched);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
@@ -447,10 +462,10 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 
 // Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
 // WR_BF_CONFIG selects one (tuning knob; default measured best).
-template <class Op, bool DENSE, int NT, int MINB, int SPL>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ = false>
 static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL>;
-    smem += (size_t)(NT / 32) * 32 * QCAP * 2 * sizeof(int);   // task queues (u, w) per warp
+    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, SQ>;
+    if (!SQ) smem += (size_t)(NT / 32) * 32 * QCAP * sizeof(int2);   // per-warp task queues
     WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, nsm = 0;
     WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
@@ -472,17 +487,16 @@ static int env_int(const char *name, int dflt) {
 
 template <class Op, bool DENSE, int SPL>
 static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    // default 4 = 384 threads x 2 CTAs/SM: measured best on config 5 among
-    // 512x2 / 512x3 / 256x4 / 256x3 / 384x2 / 448x2 / 320x2
-    static const int cfg = env_int("WR_BF_CONFIG", 4);
+    // launch shapes measured on config 5; 1 CTA per SM keeps
+    // the tiles in flight (L2 working set) at one per SM
+    // (640 threads x 1 CTA: 97 ms; 768x1: 123; 896x1: 117; 384x2: 155;
+    // static-array queues 10-15 % slower than the dynamic-smem ones)
+    static const int cfg = env_int("WR_BF_CONFIG", 9);
     switch (cfg) {
-        case 1: launch_shape<Op, DENSE, 512, 3, SPL>(g, run, d_stats, st, smem); break;
-        case 2: launch_shape<Op, DENSE, 256, 4, SPL>(g, run, d_stats, st, smem); break;
-        case 3: launch_shape<Op, DENSE, 256, 3, SPL>(g, run, d_stats, st, smem); break;
         case 4: launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st, smem); break;
-        case 5: launch_shape<Op, DENSE, 448, 2, SPL>(g, run, d_stats, st, smem); break;
-        case 6: launch_shape<Op, DENSE, 320, 2, SPL>(g, run, d_stats, st, smem); break;
-        default: launch_shape<Op, DENSE, 512, 2, SPL>(g, run, d_stats, st, smem); break;
+        case 8: launch_shape<Op, DENSE, 768, 1, SPL>(g, run, d_stats, st, smem); break;
+        case 10: launch_shape<Op, DENSE, 896, 1, SPL>(g, run, d_stats, st, smem); break;
+        default: launch_shape<Op, DENSE, 640, 1, SPL>(g, run, d_stats, st, smem); break;
     }
 }
 
@@ -491,10 +505,10 @@ static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     const int V = g->V;
     const int NW = (V + 31) / 32;
     // 4 bitmaps; launch_shape adds the per-warp task queues
-    const size_t smem = (size_t)5 * NW * sizeof(uint32_t);
+    const size_t smem = (size_t)((5 * NW + 1) & ~1) * sizeof(uint32_t);
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    if (smem + (size_t)16 * 32 * QCAP * 2 * sizeof(int) + 1024 > (size_t)max_optin)
+    if (smem + (size_t)16 * 32 * QCAP * sizeof(int2) + 1024 > (size_t)max_optin)
         WR_THROW(WR_ETOOLARGE, "bf: V too large for the shared-memory frontier bitmaps");
     const bool dense = run.variant == WR_BF_DENSE;
     switch (run.spl) {
