@@ -643,8 +643,8 @@ struct PredShape {
     static constexpr int PV = 8;     // vertices per warp job
 };
 
-template <class Op, int SPL>
-__global__ void __launch_bounds__(PredShape::WARPS * 32) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
+template <class Op, int SPL, int MINB>
+__global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
                                                       const uint32_t *__restrict__ rows,
                                                       const int *__restrict__ slot_row, int64_t out_row0,
                                                       int32_t *pred_out, int *flat_tiles) {
@@ -769,23 +769,34 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32) bf_pred_kernel(DevGraph
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
+template <class Op, int SPL, int MINB>
+static void launch_pred_shape(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
+                              cudaStream_t st) {
+    const int64_t jobs = (int64_t)run.ntiles * ((g->V + PredShape::PV - 1) / PredShape::PV);
+    const unsigned grid = (unsigned)((jobs + PredShape::WARPS - 1) / PredShape::WARPS);
+    bf_pred_kernel<Op, SPL, MINB><<<grid, PredShape::WARPS * 32, 0, st>>>(
+        g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
+    count_launch();
+    WR_LAUNCH_CHECK();
+}
+
+template <class Op, int SPL>
+static void launch_pred_spl(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
+                            cudaStream_t st) {
+    // 256 threads x >= 4 CTAs/SM (64 regs): 45 ms on config 5 vs 61 (no
+    // bound) and 77 (5 CTAs, spills)
+    static const int cfg = env_int("WR_PRED_CONFIG", 1);
+    if (cfg == 1) launch_pred_shape<Op, SPL, 4>(g, run, out_row0, pred_out, flat, st);
+    else if (cfg == 2) launch_pred_shape<Op, SPL, 5>(g, run, out_row0, pred_out, flat, st);
+    else launch_pred_shape<Op, SPL, 1>(g, run, out_row0, pred_out, flat, st);
+}
+
 template <class Op>
 static void launch_pred(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
                         cudaStream_t st) {
-    const int64_t jobs = (int64_t)run.ntiles * ((g->V + PredShape::PV - 1) / PredShape::PV);
-    const unsigned grid = (unsigned)((jobs + PredShape::WARPS - 1) / PredShape::WARPS);
-    const int nt = PredShape::WARPS * 32;
-    if (run.spl == 2)
-        bf_pred_kernel<Op, 2><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
-                                                   out_row0, pred_out, flat);
-    else if (run.spl == 4)
-        bf_pred_kernel<Op, 4><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
-                                                   out_row0, pred_out, flat);
-    else
-        bf_pred_kernel<Op, 1><<<grid, nt, 0, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row,
-                                                   out_row0, pred_out, flat);
-    count_launch();
-    WR_LAUNCH_CHECK();
+    if (run.spl == 2) launch_pred_spl<Op, 2>(g, run, out_row0, pred_out, flat, st);
+    else if (run.spl == 4) launch_pred_spl<Op, 4>(g, run, out_row0, pred_out, flat, st);
+    else launch_pred_spl<Op, 1>(g, run, out_row0, pred_out, flat, st);
 }
 
 void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t, const int *targets, int T,
