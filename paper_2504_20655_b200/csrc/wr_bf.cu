@@ -218,7 +218,7 @@ __host__ __device__ constexpr int qcap_for(int nt) {
     return ((46 * 1024) / (nt * 8)) >= 16 ? 16 : (((46 * 1024) / (nt * 8)) & ~1);
 }
 
-template <class Op, bool DELTA, int SPL, int QC>
+template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const uint32_t *pchg,
                                                uint32_t *nxt, int2 *q, uint32_t *touched) {
@@ -252,70 +252,77 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     uint32_t *Rl = R + lane * SPL;
     uint32_t chg = 0;
     unsigned long long dummy = 0;
-    // ---- B: relax the queued vertices, two per step
+    // ---- B: relax the queued vertices, VB per step, TPS tasks each per
+    // step (VB*TPS row gathers in flight)
     while (todo) {
-        const int i0 = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const bool two = todo != 0;
-        const int i1 = two ? __ffs(todo) - 1 : i0;
-        if (two) todo &= todo - 1;
-        const int v0 = (w << 5) + i0, v1 = (w << 5) + i1;
-        Vec<SPL> e0 = infv, e1 = infv;
-        if ((tw >> i0) & 1u) e0 = vload<SPL>(Rl + (size_t)v0 * TSW);
-        if (two && ((tw >> i1) & 1u)) e1 = vload<SPL>(Rl + (size_t)v1 * TSW);
-        Vec<SPL> d0 = e0, d1 = e1;
-        const bool s0 = (slow >> i0) & 1u, s1 = two && ((slow >> i1) & 1u);
-        if (!s0 && !s1) {
-            const int c0 = __shfl_sync(FULL, c, i0);
-            const int c1 = two ? __shfl_sync(FULL, c, i1) : 0;
-            const int2 *q0 = q + i0 * QC, *q1 = q + i1 * QC;
-            const int tmax = max(c0, c1);
-            for (int t = 0; t < tmax; t += 2) {
-                Vec<SPL> x00, x01, x10, x11;
-                int2 t00 = make_int2(0, 0), t01 = t00, t10 = t00, t11 = t00;
-                if (t < c0) t00 = q0[t];
-                if (t + 1 < c0) t01 = q0[t + 1];
-                if (t < c1) t10 = q1[t];
-                if (t + 1 < c1) t11 = q1[t + 1];
-                if (t < c0) x00 = vload<SPL>(Rl + (size_t)t00.x * TSW);
-                if (t + 1 < c0) x01 = vload<SPL>(Rl + (size_t)t01.x * TSW);
-                if (t < c1) x10 = vload<SPL>(Rl + (size_t)t10.x * TSW);
-                if (t + 1 < c1) x11 = vload<SPL>(Rl + (size_t)t11.x * TSW);
-                if (t < c0) vrelax<Op, SPL>(d0, x00, (uint32_t)t00.y);
-                if (t + 1 < c0) vrelax<Op, SPL>(d0, x01, (uint32_t)t01.y);
-                if (t < c1) vrelax<Op, SPL>(d1, x10, (uint32_t)t10.y);
-                if (t + 1 < c1) vrelax<Op, SPL>(d1, x11, (uint32_t)t11.y);
+        int iv[VB];
+        bool ok[VB];
+#pragma unroll
+        for (int k = 0; k < VB; ++k) {
+            ok[k] = todo != 0;
+            iv[k] = ok[k] ? __ffs(todo) - 1 : 0;
+            if (ok[k]) todo &= todo - 1;
+        }
+        Vec<SPL> e[VB], d[VB];
+        int cc[VB];
+        bool anyslow = false;
+#pragma unroll
+        for (int k = 0; k < VB; ++k) {
+            e[k] = infv;
+            if (ok[k] && ((tw >> iv[k]) & 1u)) e[k] = vload<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW);
+            d[k] = e[k];
+            cc[k] = __shfl_sync(FULL, c, iv[k]);
+            if (!ok[k]) cc[k] = 0;
+            anyslow |= ok[k] && ((slow >> iv[k]) & 1u);
+        }
+        if (!anyslow) {
+            int tmax = 0;
+#pragma unroll
+            for (int k = 0; k < VB; ++k) tmax = max(tmax, cc[k]);
+            for (int t = 0; t < tmax; t += TPS) {
+                int2 tk[VB][TPS];
+                Vec<SPL> x[VB][TPS];
+#pragma unroll
+                for (int k = 0; k < VB; ++k)
+#pragma unroll
+                    for (int j = 0; j < TPS; ++j) {
+                        tk[k][j] = make_int2(0, 0);
+                        if (t + j < cc[k]) tk[k][j] = q[iv[k] * QC + t + j];
+                    }
+#pragma unroll
+                for (int k = 0; k < VB; ++k)
+#pragma unroll
+                    for (int j = 0; j < TPS; ++j)
+                        if (t + j < cc[k]) x[k][j] = vload<SPL>(Rl + (size_t)tk[k][j].x * TSW);
+#pragma unroll
+                for (int k = 0; k < VB; ++k)
+#pragma unroll
+                    for (int j = 0; j < TPS; ++j)
+                        if (t + j < cc[k]) vrelax<Op, SPL>(d[k], x[k][j], (uint32_t)tk[k][j].y);
             }
         } else {
-            if (s0) d0 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i0),
-                                                     __shfl_sync(FULL, a1, i0), lane, d0, dummy);
-            else {
-                const int c0 = __shfl_sync(FULL, c, i0);
-                for (int t = 0; t < c0; ++t) {
-                    const int2 tk = q[i0 * QC + t];
-                    vrelax<Op, SPL>(d0, vload<SPL>(Rl + (size_t)tk.x * TSW), (uint32_t)tk.y);
-                }
-            }
-            if (two) {
-                if (s1) d1 = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, i1),
-                                                         __shfl_sync(FULL, a1, i1), lane, d1, dummy);
-                else {
-                    const int c1 = __shfl_sync(FULL, c, i1);
-                    for (int t = 0; t < c1; ++t) {
-                        const int2 tk = q[i1 * QC + t];
-                        vrelax<Op, SPL>(d1, vload<SPL>(Rl + (size_t)tk.x * TSW), (uint32_t)tk.y);
+#pragma unroll
+            for (int k = 0; k < VB; ++k) {
+                if (!ok[k]) continue;
+                if ((slow >> iv[k]) & 1u) {
+                    d[k] = relax_vertex<Op, DELTA, SPL>(g, Rl, pchg, __shfl_sync(FULL, a0, iv[k]),
+                                                        __shfl_sync(FULL, a1, iv[k]), lane, d[k], dummy);
+                } else {
+                    for (int t = 0; t < cc[k]; ++t) {
+                        const int2 tq = q[iv[k] * QC + t];
+                        vrelax<Op, SPL>(d[k], vload<SPL>(Rl + (size_t)tq.x * TSW), (uint32_t)tq.y);
                     }
                 }
             }
         }
-        // first write of a row covers every slot (untouched slots stay INF)
-        const bool f0 = !((tw >> i0) & 1u), f1 = two && !((tw >> i1) & 1u);
-        const bool c0 = vless<Op, SPL>(d0, e0);
-        if (c0 || f0) vstore<SPL>(Rl + (size_t)v0 * TSW, d0);
-        const bool c1 = two && vless<Op, SPL>(d1, e1);
-        if (c1 || f1) vstore<SPL>(Rl + (size_t)v1 * TSW, d1);
-        if (__any_sync(FULL, c0)) chg |= 1u << i0;
-        if (__any_sync(FULL, c1)) chg |= 1u << i1;
+#pragma unroll
+        for (int k = 0; k < VB; ++k) {
+            // first write of a row covers every slot (untouched slots stay INF)
+            const bool f = ok[k] && !((tw >> iv[k]) & 1u);
+            const bool ch = ok[k] && vless<Op, SPL>(d[k], e[k]);
+            if (ch || f) vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, d[k]);
+            if (__any_sync(FULL, ch)) chg |= 1u << iv[k];
+        }
     }
     if (DELTA && lane == 0 && (chg & ~tw)) touched[w] = tw | chg;   // this warp owns word w
     // ---- C: improved vertices mark their out-neighbours, lane-parallel
@@ -338,7 +345,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 // barrier. Word w of every bitmap is written by one warp only (w mod warps).
 // Dense variant: every vertex is a candidate every round, all arcs pulled
 // (the paper's edge-parallel class of work).
-template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ, int VB, int TPS>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
@@ -422,7 +429,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 if (m) {
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    c = relax_word<Op, !DENSE, SPL, QC>(g, R, w, m, lane, relax, pchg, nxt, q, touched);
+                    c = relax_word<Op, !DENSE, SPL, QC, VB, TPS>(g, R, w, m, lane, relax, pchg, nxt, q, touched);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
@@ -462,9 +469,9 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 
 // Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
 // WR_BF_CONFIG selects one (tuning knob; default measured best).
-template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ = false>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ = false, int VB = 2, int TPS = 2>
 static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, SQ>;
+    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, SQ, VB, TPS>;
     if (!SQ) smem += (size_t)(NT / 32) * 32 * QCAP * sizeof(int2);   // per-warp task queues
     WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, nsm = 0;
