@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include "wr_internal.cuh"
@@ -123,6 +124,13 @@ __device__ __forceinline__ void vrelax(Vec<SPL> &d, const Vec<SPL> &x, uint32_t 
     for (int j = 0; j < SPL; ++j) d.x[j] = Op::relax(d.x[j], x.x[j], w);
 }
 template <class Op, int SPL>
+__device__ __forceinline__ Vec<SPL> vmin(const Vec<SPL> &a, const Vec<SPL> &b) {
+    Vec<SPL> r;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) r.x[j] = Op::less(a.x[j], b.x[j]) ? a.x[j] : b.x[j];
+    return r;
+}
+template <class Op, int SPL>
 __device__ __forceinline__ bool vless(const Vec<SPL> &a, const Vec<SPL> &b) {
     bool r = false;
 #pragma unroll
@@ -154,10 +162,23 @@ void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_ti
 // The tails' change bits are tested lane-parallel (one bitmap probe per
 // arc, ballot), and only the set arcs are gathered. Dense mode tests nothing.
 
+// The change sets are round-stamped words (bits, round) in shared memory,
+// double-buffered by round parity: a word written in round r is only read
+// as "changed in round r" (stamp check), so stale words from earlier rounds
+// never need clearing, and a word is written only when something changed.
+struct ChgView {
+    const uint2 *p;
+    uint32_t r;   // the round whose changes are wanted
+    __device__ __forceinline__ bool test(int u) const {
+        const uint2 e = p[u >> 5];
+        return e.y == r && ((e.x >> (u & 31)) & 1u);
+    }
+};
+
 // Generic-degree pull of one vertex. Rl = this lane's first slot.
 template <class Op, bool DELTA, int SPL>
 __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32_t *__restrict__ Rl,
-                                                 const uint32_t *pchg, int a0, int a1, int lane, Vec<SPL> d,
+                                                 const ChgView pchg, int a0, int a1, int lane, Vec<SPL> d,
                                                  unsigned long long &relax) {
     constexpr int TSW = 32 * SPL;
     for (int base = a0; base < a1; base += 32) {
@@ -168,7 +189,7 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
         if (lane < cnt) {
             my_u = g.in_src[base + lane];
             my_w = g.in_w[base + lane];
-            take = !DELTA || ((pchg[my_u >> 5] >> (my_u & 31)) & 1u);
+            take = !DELTA || pchg.test(my_u);
         }
         uint32_t m = __ballot_sync(FULL, take);
         relax += (unsigned long long)__popc(m);
@@ -190,13 +211,6 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
     return d;
 }
 
-__device__ __forceinline__ void mark_out_range(const DevGraph &g, int o0, int o1, int lane, uint32_t *nxt) {
-    for (int e = o0 + lane; e < o1; e += 32) {
-        const int x = g.out_dst[e];
-        atomicOr(&nxt[x >> 5], 1u << (x & 31));
-    }
-}
-
 // Relaxes the candidate vertices (bits of m) of word w for every slot, in
 // three steps that keep the control work lane-parallel:
 //  A. lane = candidate vertex: walk its in-arcs, test each tail's change bit
@@ -207,21 +221,18 @@ __device__ __forceinline__ void mark_out_range(const DevGraph &g, int o0, int o1
 //     their own rows and gather the queued tails' rows (up to four gathers
 //     in flight), min-plus relax, store improved rows, vote;
 //  C. lane = vertex again: every improved vertex marks its out-neighbours in
-//     the next round's candidate bitmap (shared-memory atomicOr).
+//     the next round's candidate bitmap (shared-memory atomicOr); the lane
+//     that turns a word non-zero appends it to the next round's word list.
 // Returns the word's change mask.
-// Task-queue capacity per vertex: per-warp queues of 32 x QCAP packed
-// (u, w) pairs, either after the bitmaps in dynamic shared memory or in a
-// static array (compile-time address; capacity limited by the 48 KB static
-// budget: qcap_for(NT)).
+// Task-queue capacity per vertex: per-warp queues of 32 x QC packed (u, w)
+// pairs after the bitmaps in dynamic shared memory.
 constexpr int QCAP = 16;
-__host__ __device__ constexpr int qcap_for(int nt) {
-    return ((46 * 1024) / (nt * 8)) >= 16 ? 16 : (((46 * 1024) / (nt * 8)) & ~1);
-}
 
-template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS>
+template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
-                                               int lane, unsigned long long &relax, const uint32_t *pchg,
-                                               uint32_t *nxt, int2 *q, uint32_t *touched) {
+                                               int lane, unsigned long long &relax, const ChgView pchg,
+                                               uint32_t *nxt, int *nlist, int *nlen, int2 *q,
+                                               uint32_t *touched) {
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
@@ -230,13 +241,20 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         a0 = g.in_ptr[v];
         a1 = g.in_ptr[v + 1];
     }
-    // ---- A: queue this lane's changed in-arcs
+    // ---- A: queue this lane's changed in-arcs; the packed (u, w) arcs are
+    // loaded AQ at a time (independent loads in flight, no branch between
+    // them) before their tails' change bits are tested
+    constexpr int AQ = 8;
     int c = 0;
-    for (int k = a0; k < a1; ++k) {
-        const int u = g.in_src[k];
-        if (!DELTA || ((pchg[u >> 5] >> (u & 31)) & 1u)) {
-            if (c < QC) q[lane * QC + c] = make_int2(u, (int)g.in_w[k]);
-            ++c;
+    for (int k0 = a0; k0 < a1; k0 += AQ) {
+        int2 arc[AQ];
+#pragma unroll
+        for (int j = 0; j < AQ; ++j) arc[j] = (k0 + j < a1) ? g.in_arc[k0 + j] : make_int2(-1, 0);
+#pragma unroll
+        for (int j = 0; j < AQ; ++j) {
+            const bool take = arc[j].x >= 0 && (!DELTA || pchg.test(arc[j].x));
+            if (take && c < QC) q[lane * QC + c] = arc[j];
+            c += take ? 1 : 0;
         }
     }
     relax += (unsigned long long)__reduce_add_sync(FULL, (unsigned)c);
@@ -268,9 +286,11 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         bool anyslow = false;
 #pragma unroll
         for (int k = 0; k < VB; ++k) {
+            // the own row is only needed at the end: d starts at INF so the
+            // row loads overlap the tails' gathers instead of preceding them
             e[k] = infv;
             if (ok[k] && ((tw >> iv[k]) & 1u)) e[k] = vload<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW);
-            d[k] = e[k];
+            d[k] = infv;
             cc[k] = __shfl_sync(FULL, c, iv[k]);
             if (!ok[k]) cc[k] = 0;
             anyslow |= ok[k] && ((slow >> iv[k]) & 1u);
@@ -320,7 +340,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
             // first write of a row covers every slot (untouched slots stay INF)
             const bool f = ok[k] && !((tw >> iv[k]) & 1u);
             const bool ch = ok[k] && vless<Op, SPL>(d[k], e[k]);
-            if (ch || f) vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, d[k]);
+            if (ch || f) vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, vmin<Op, SPL>(d[k], e[k]));
             if (__any_sync(FULL, ch)) chg |= 1u << iv[k];
         }
     }
@@ -330,7 +350,11 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         const int o1 = g.out_ptr[v + 1];
         for (int e = g.out_ptr[v]; e < o1; ++e) {
             const int x = g.out_dst[e];
-            atomicOr(&nxt[x >> 5], 1u << (x & 31));
+            if (LIST) {
+                if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u) nlist[atomicAdd(nlen, 1)] = x >> 5;
+            } else {
+                atomicOr(&nxt[x >> 5], 1u << (x & 31));
+            }
         }
     }
     __syncwarp();   // the queue is reused by the warp's next word
@@ -338,28 +362,53 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 }
 
 // ------------------------------------------------------ the sweep kernel --
-// One CTA per tile at a time. Shared memory: four V-bit bitmaps - the
-// candidate sets cur (relaxed this round) and nxt (out-neighbours of this
-// round's improvements), and the change sets pchg (improved last round,
-// read-only now) and cchg (improved this round) - swapped after each round's
-// barrier. Word w of every bitmap is written by one warp only (w mod warps).
+// One CTA per tile at a time. Shared memory (frontier variant):
+//   cur, nxt   V-bit candidate bitmaps (relaxed this round / out-neighbours
+//              of this round's improvements), swapped each round;
+//   touched    vertices whose row has been written (lazy rows);
+//   chg[2]     round-stamped change words (ChgView), by round parity;
+//   list[2]    the non-zero words of cur / nxt, so a round visits only its
+//              candidate words, handed out to warps dynamically (one shared
+//              counter per round) - no scan over all V/32 words and no
+//              static word-to-warp split that leaves warps idle at the
+//              round barrier;
+//   queues     per-warp task queues (relax_word).
 // Dense variant: every vertex is a candidate every round, all arcs pulled
-// (the paper's edge-parallel class of work).
-template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ, int VB, int TPS>
+// (the paper's edge-parallel class of work), words split statically.
+struct FrontierSmem {
+    size_t cur, nxt, touched, chg, list, queue, words;
+};
+__host__ __device__ constexpr FrontierSmem frontier_smem(int NW, int nwarps, int QC) {
+    // offsets in 32-bit words; uint2 / int2 regions 8-B aligned
+    return FrontierSmem{0,
+                        (size_t)NW,
+                        (size_t)2 * NW,
+                        ((size_t)3 * NW + 1) & ~(size_t)1,
+                        (((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)4 * NW,
+                        ((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 1) & ~(size_t)1,
+                        (((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 1) & ~(size_t)1) +
+                            (size_t)nwarps * 32 * QC * 2};
+}
+
+template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
                                                                BfTileStats *stats) {
     constexpr int TSW = 32 * SPL;
-    constexpr int QC = SQ ? qcap_for(NT) : QCAP;
-    extern __shared__ uint32_t smem[];
-    __shared__ int2 s_queue[SQ ? NT / 32 : 1][SQ ? 32 * QC : 1];
+    constexpr int NWARPS = NT / 32;
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ int s_tile;
+    __shared__ int s_len[3], s_head[3];
     const int V = g.V;
     const int NW = (V + 31) >> 5;
-    __shared__ int s_tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NWARPS = NT / 32;
     const uint32_t last_mask = (V & 31) ? ((1u << (V & 31)) - 1u) : 0xffffffffu;
+    const FrontierSmem L = frontier_smem(NW, NWARPS, QC);
+    uint32_t *const touched = smem + L.touched;
+    uint2 *const chg = reinterpret_cast<uint2 *>(smem + L.chg);
+    int *const list = reinterpret_cast<int *>(smem + L.list);
+    int2 *const q = reinterpret_cast<int2 *>(smem + L.queue) + warp * (32 * QC);
 
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
@@ -367,23 +416,20 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         const int tile = s_tile;
         if (tile >= ntiles) break;
         uint32_t *R = rows + (size_t)tile * V * TSW;
-        uint32_t *cur = smem, *nxt = smem + NW, *pchg = smem + 2 * NW, *cchg = smem + 3 * NW;
-        uint32_t *touched = smem + 4 * NW;   // vertices whose row has been written
-        int2 *q = SQ ? &s_queue[warp][0]
-                     : reinterpret_cast<int2 *>(smem + ((5 * NW + 1) & ~1)) + warp * (32 * QC);   // 8-B aligned
+        uint32_t *cur = smem + L.cur, *nxt = smem + L.nxt;
 
-        // init: bitmaps empty; rows INF (dense) or written lazily (frontier:
-        // a row is written whole on its vertex's first improvement, and the
-        // rows of vertices never reached are filled with INF at the end)
+        // init: bitmaps and stamps zero (round 0 = the seeds); rows INF
+        // (dense) or written lazily (frontier: a row is written whole on its
+        // vertex's first improvement, and the rows of vertices never reached
+        // are filled with INF at the end)
         const uint4 inf4 = make_uint4(Op::INF, Op::INF, Op::INF, Op::INF);
-        {
-            if (DENSE) {
-                uint4 *R4 = reinterpret_cast<uint4 *>(R);
-                const size_t n4 = (size_t)V * (TSW / 4);
-                for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
-            }
-            for (int w = threadIdx.x; w < 5 * NW; w += NT) smem[w] = 0u;
+        if (DENSE) {
+            uint4 *R4 = reinterpret_cast<uint4 *>(R);
+            const size_t n4 = (size_t)V * (TSW / 4);
+            for (size_t i = threadIdx.x; i < n4; i += NT) R4[i] = inf4;
         }
+        for (size_t i = threadIdx.x; i < L.list; i += NT) smem[i] = 0u;
+        if (threadIdx.x < 3) s_len[threadIdx.x] = s_head[threadIdx.x] = 0;
         __syncthreads();
         if (warp == 0) {   // seed: d[s][slot] = 0; the sources "changed" in round 0
             if (!DENSE) {  // the seed vertices' rows: INF everywhere first
@@ -391,7 +437,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     const int s = tile_src[tile * TSW + k];
                     if (s >= 0) {
                         uint32_t *row = R + (size_t)s * TSW;
-                        for (int q = lane; q < TSW / 4; q += 32) reinterpret_cast<uint4 *>(row)[q] = inf4;
+                        for (int c = lane; c < TSW / 4; c += 32) reinterpret_cast<uint4 *>(row)[c] = inf4;
                     }
                 }
                 __syncwarp();
@@ -402,11 +448,11 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 const int s = tile_src[tile * TSW + slot];
                 if (s >= 0) {
                     R[(size_t)s * TSW + slot] = Op::ZERO;
-                    atomicOr(&pchg[s >> 5], 1u << (s & 31));
+                    atomicOr(&chg[s >> 5].x, 1u << (s & 31));   // stamp 0 = round 0
                     atomicOr(&touched[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
                         const int x = g.out_dst[e];
-                        atomicOr(&cur[x >> 5], 1u << (x & 31));
+                        if (atomicOr(&cur[x >> 5], 1u << (x & 31)) == 0u) list[NW + atomicAdd(&s_len[1], 1)] = x >> 5;
                     }
                 }
             }
@@ -416,33 +462,64 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         int rounds = 0;
         unsigned long long relax = 0, visits = 0;
         bool more = true;
-        while (more) {
+        for (int r = 1; more; ++r) {
+            int any = 0;
             if (DENSE) {
                 for (int w = threadIdx.x; w < NW; w += NT) cur[w] = (w == NW - 1) ? last_mask : 0xffffffffu;
                 __syncthreads();
-            }
-            // ---- relax: warp per candidate word, lane = SPL source slots
-            int any = 0;
-            for (int w = warp; w < NW; w += NWARPS) {
-                const uint32_t m = cur[w];
-                uint32_t c = 0;
-                if (m) {
-                    __syncwarp();
-                    if (lane == 0) cur[w] = 0u;
-                    c = relax_word<Op, !DENSE, SPL, QC, VB, TPS>(g, R, w, m, lane, relax, pchg, nxt, q, touched);
+                for (int w = warp; w < NW; w += NWARPS) {
+                    const uint32_t m = cur[w];
+                    const uint32_t c = relax_word<Op, false, SPL, QC, VB, TPS, false>(
+                        g, R, w, m, lane, relax, ChgView{chg, 0u}, nxt, list, &s_len[0], q, touched);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
-                if (!DENSE && lane == 0 && cchg[w] != c) cchg[w] = c;   // also clears stale words
+            } else if (!LIST) {
+                // ---- static split: warp k scans words k, k + NWARPS, ...
+                const ChgView pc{chg + ((r - 1) & 1) * NW, (uint32_t)(r - 1)};
+                uint2 *cc = chg + (r & 1) * NW;
+                for (int w = warp; w < NW; w += NWARPS) {
+                    const uint32_t m = cur[w];
+                    if (!m) continue;
+                    __syncwarp();
+                    if (lane == 0) cur[w] = 0u;
+                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, false>(g, R, w, m, lane, relax, pc, nxt,
+                                                                                     nullptr, nullptr, q, touched);
+                    if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
+                    visits += (unsigned long long)__popc(m);
+                    any |= c != 0;
+                }
+            } else {
+                // ---- relax the candidate words of list r&1, claimed one at a
+                // time; improvements append to list (r+1)&1
+                const int *lc = list + (r & 1) * NW;
+                int *ln = list + ((r + 1) & 1) * NW;
+                const int len = s_len[r % 3];
+                int *const nlen = &s_len[(r + 1) % 3];
+                if (threadIdx.x == 0) s_len[(r + 2) % 3] = s_head[(r + 2) % 3] = 0;   // used in round r-1
+                const ChgView pc{chg + ((r - 1) & 1) * NW, (uint32_t)(r - 1)};
+                uint2 *cc = chg + (r & 1) * NW;
+                for (;;) {
+                    int i = 0;
+                    if (lane == 0) i = atomicAdd(&s_head[r % 3], 1);
+                    i = __shfl_sync(FULL, i, 0);
+                    if (i >= len) break;
+                    const int w = lc[i];
+                    const uint32_t m = cur[w];
+                    __syncwarp();
+                    if (lane == 0) cur[w] = 0u;
+                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, true>(g, R, w, m, lane, relax, pc, nxt,
+                                                                                    ln, nlen, q, touched);
+                    if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
+                    visits += (unsigned long long)__popc(m);
+                    any |= c != 0;
+                }
             }
             ++rounds;
             more = __syncthreads_or(any) != 0;
             uint32_t *t = cur;
             cur = nxt;
             nxt = t;
-            t = pchg;
-            pchg = cchg;
-            cchg = t;
             if (more && rounds >= max_rounds) {
                 if (threadIdx.x == 0) atomicMax(&stats->negcycle_tile, tile);
                 more = false;
@@ -455,7 +532,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     const int b = __ffs(um) - 1;
                     um &= um - 1;
                     uint4 *row = reinterpret_cast<uint4 *>(R + (size_t)((w << 5) + b) * TSW);
-                    for (int q = lane; q < TSW / 4; q += 32) row[q] = inf4;
+                    for (int c = lane; c < TSW / 4; c += 32) row[c] = inf4;
                 }
             }
         }
@@ -469,10 +546,14 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 
 // Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
 // WR_BF_CONFIG selects one (tuning knob; default measured best).
-template <class Op, bool DENSE, int NT, int MINB, int SPL, bool SQ = false, int VB = 2, int TPS = 2>
-static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
-    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, SQ, VB, TPS>;
-    if (!SQ) smem += (size_t)(NT / 32) * 32 * QCAP * sizeof(int2);   // per-warp task queues
+template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool LIST = false, int VB = 2, int TPS = 2>
+static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
+    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, QC, VB, TPS, LIST && !DENSE>;
+    const int NW = (g->V + 31) / 32;
+    const size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
+    int max_optin = 0;
+    WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+    if (smem > (size_t)max_optin) return false;
     WR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, nsm = 0;
     WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
@@ -485,6 +566,7 @@ static void launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     count_launch();
     WR_LAUNCH_CHECK();
     WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
+    return true;
 }
 
 static int env_int(const char *name, int dflt) {
@@ -493,43 +575,43 @@ static int env_int(const char *name, int dflt) {
 }
 
 template <class Op, bool DENSE, int SPL>
-static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st, size_t smem) {
+static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
     // launch shapes measured on config 5; 1 CTA per SM keeps
-    // the tiles in flight (L2 working set) at one per SM
-    // (640 threads x 1 CTA: 97 ms; 768x1: 123; 896x1: 117; 384x2: 155;
-    // static-array queues 10-15 % slower than the dynamic-smem ones)
-    static const int cfg = env_int("WR_BF_CONFIG", 9);
+    // the tiles in flight (L2 working set) at one per SM. int32 sweep:
+    // 768 threads + word lists (14) 77.6 ms, 768 static (8) 80.6, 640 lists
+    // (11) 84.4, 640 static (9) 94.4, 896 static (10) 104; fp32: 768 static
+    // 232 ms, 640 static 240, 768 lists 254 (the list order lets more
+    // suboptimal values propagate: 4.4 vs 3.6 x S*E relaxations).
+    static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 14);
+    bool ok = false;
     switch (cfg) {
-        case 4: launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st, smem); break;
-        case 8: launch_shape<Op, DENSE, 768, 1, SPL>(g, run, d_stats, st, smem); break;
-        case 10: launch_shape<Op, DENSE, 896, 1, SPL>(g, run, d_stats, st, smem); break;
-        default: launch_shape<Op, DENSE, 640, 1, SPL>(g, run, d_stats, st, smem); break;
+        case 4: ok = launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st); break;
+        case 8: ok = launch_shape<Op, DENSE, 768, 1, SPL>(g, run, d_stats, st); break;
+        case 10: ok = launch_shape<Op, DENSE, 896, 1, SPL>(g, run, d_stats, st); break;
+        case 11: ok = launch_shape<Op, DENSE, 640, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
+        case 14: ok = launch_shape<Op, DENSE, 768, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
+        default: break;
     }
+    if (!ok && !launch_shape<Op, DENSE, 640, 1, SPL>(g, run, d_stats, st) &&
+        !launch_shape<Op, DENSE, 256, 1, SPL, 4>(g, run, d_stats, st))
+        WR_THROW(WR_ETOOLARGE, "bf: V too large for the shared-memory frontier bitmaps");
 }
 
 template <class Op>
 static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
-    const int V = g->V;
-    const int NW = (V + 31) / 32;
-    // 4 bitmaps; launch_shape adds the per-warp task queues
-    const size_t smem = (size_t)((5 * NW + 1) & ~1) * sizeof(uint32_t);
-    int max_optin = 0;
-    WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    if (smem + (size_t)16 * 32 * QCAP * sizeof(int2) + 1024 > (size_t)max_optin)
-        WR_THROW(WR_ETOOLARGE, "bf: V too large for the shared-memory frontier bitmaps");
     const bool dense = run.variant == WR_BF_DENSE;
     switch (run.spl) {
         case 4:
-            if (dense) launch_dispatch<Op, true, 4>(g, run, d_stats, st, smem);
-            else launch_dispatch<Op, false, 4>(g, run, d_stats, st, smem);
+            if (dense) launch_dispatch<Op, true, 4>(g, run, d_stats, st);
+            else launch_dispatch<Op, false, 4>(g, run, d_stats, st);
             break;
         case 2:
-            if (dense) launch_dispatch<Op, true, 2>(g, run, d_stats, st, smem);
-            else launch_dispatch<Op, false, 2>(g, run, d_stats, st, smem);
+            if (dense) launch_dispatch<Op, true, 2>(g, run, d_stats, st);
+            else launch_dispatch<Op, false, 2>(g, run, d_stats, st);
             break;
         default:
-            if (dense) launch_dispatch<Op, true, 1>(g, run, d_stats, st, smem);
-            else launch_dispatch<Op, false, 1>(g, run, d_stats, st, smem);
+            if (dense) launch_dispatch<Op, true, 1>(g, run, d_stats, st);
+            else launch_dispatch<Op, false, 1>(g, run, d_stats, st);
             break;
     }
 }
@@ -541,17 +623,18 @@ void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStrea
     else launch_sweep<OpU32>(g, run, d_stats, st);
 }
 
-// Sources per lane for S sources: as wide as possible while the tile count
-// still fills the GPU (>= 2 tiles per CTA slot); WR_BF_SPL forces a width.
+// Sources per lane for S sources; WR_BF_SPL forces a width.
 int choose_spl(int64_t S, int nsm) {
+    (void)S;
+    (void)nsm;
     const int forced = env_int("WR_BF_SPL", 0);
     if (forced == 1 || forced == 2 || forced == 4) return forced;
-    // measured on config 5: with the task-queue sweep, 4
-    // sources per lane (128-source Morton tiles) is fastest; narrower tiles
-    // when there are too few tiles to fill the GPU (>= 4 per SM)
-    int spl = 4;
-    while (spl > 1 && S / (32 * spl) < (int64_t)4 * nsm) spl /= 2;
-    return spl;
+    // Always the widest tile (measured): a tile's time is
+    // set by its chain of ~100 latency-bound rounds, almost independent of
+    // its width, so 128 sources per tile finish in the same time as 32 and
+    // the wave count ceil(tiles / SMs) is smallest at SPL 4 (per-rank shard
+    // of config 5 at W = 4: SPL 4 47 ms vs the narrow-tile 124 ms).
+    return 4;
 }
 
 // --------------------------------------------------- a4 + output layout --

@@ -248,6 +248,11 @@ __global__ void scatter_kernel(const int *src, const int *dst, const uint32_t *w
 
 // Deterministic order: in-arcs of v sorted by (tail, weight bits); out-arcs
 // of u sorted by head. Insertion sort per vertex (warehouse degrees <= ~10).
+__global__ void pack_arcs_kernel(const int *in_src, const uint32_t *in_w, int2 *in_arc, int64_t E) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < E) in_arc[i] = make_int2(in_src[i], (int)in_w[i]);
+}
+
 __global__ void sort_adj_kernel(const int *in_ptr, int *in_src, uint32_t *in_w, const int *out_ptr,
                                 int *out_dst, int V) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -388,6 +393,10 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
                                                          g->out_ptr.p, g->out_dst.p, V);
         count_launch();
         WR_LAUNCH_CHECK();
+        g->in_arc.alloc(E);
+        pack_arcs_kernel<<<grid_for(E, 256), 256, 0, st>>>(g->in_src.p, g->in_w.p, g->in_arc.p, E);
+        count_launch();
+        WR_LAUNCH_CHECK();
         WR_CUDA(cudaStreamSynchronize(st));
     }
     WR_CUDA(cudaStreamSynchronize(st));
@@ -432,7 +441,7 @@ wr_status wr_graph_info(const wr_graph *g, wr_graph_info_t *info) {
     info->has_negative = g->has_negative;
     info->has_xy = g->xy.p != nullptr;
     info->device = g->device;
-    info->device_bytes = (int64_t)(g->in_ptr.bytes() + g->in_src.bytes() + g->in_w.bytes() +
+    info->device_bytes = (int64_t)(g->in_ptr.bytes() + g->in_src.bytes() + g->in_w.bytes() + g->in_arc.bytes() +
                                    g->out_ptr.bytes() + g->out_dst.bytes() + g->xy.bytes());
     info->max_abs_weight = g->wtype == WR_I32 ? g->max_abs_w : 0;
     return WR_OK;

@@ -125,6 +125,7 @@ struct DevGraph {           // kernel view (POD)
     const int *in_ptr;      // [V+1] CSC offsets (in-arcs of v)
     const int *in_src;      // [E]   tail u of each in-arc, sorted by (v, u)
     const uint32_t *in_w;   // [E]   weight bits
+    const int2 *in_arc;     // [E]   (in_src, in_w) packed: one 8-B load per in-arc
     const int *out_ptr;     // [V+1] CSR offsets (out-arcs of u)
     const int *out_dst;     // [E]   head of each out-arc
 };
@@ -140,11 +141,12 @@ struct wr_graph {
     int32_t max_abs_w = 0;
     wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
     wr::DBuf<uint32_t> in_w;
+    wr::DBuf<int2> in_arc;
     wr::DBuf<int> xy;       // [V*2] or empty
     wr::DBuf<int> z;        // [V] rack level or empty
     int bbox[6] = {0, 0, 0, 0, 0, 0};   // xmin, xmax, ymin, ymax, zmin, zmax
     wr::DevGraph view() const {
-        return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, out_ptr.p, out_dst.p};
+        return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, in_arc.p, out_ptr.p, out_dst.p};
     }
 };
 
