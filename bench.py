@@ -282,11 +282,12 @@ def main():
             p.finish(gathered, results=h_res)
             p.close()
 
-        e2e_step()
+        for _ in range(2):
+            e2e_step()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        k2 = max(1, min(a.steps, 3))
+        k2 = max(1, a.steps)
         for _ in range(k2):
             e2e_step()
         f1.record(stream)

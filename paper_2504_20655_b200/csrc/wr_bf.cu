@@ -877,7 +877,7 @@ static void launch_pred_spl(const wr_graph *g, const BfRun &run, int64_t out_row
     // bound) and 77 (5 CTAs, spills)
     static const int cfg = env_int("WR_PRED_CONFIG", 1);
     if (cfg == 1) launch_pred_shape<Op, SPL, 4>(g, run, out_row0, pred_out, flat, st);
-    else if (cfg == 2) launch_pred_shape<Op, SPL, 5>(g, run, out_row0, pred_out, flat, st);
+    else if (cfg == 2) launch_pred_shape<Op, SPL, 3>(g, run, out_row0, pred_out, flat, st);
     else launch_pred_shape<Op, SPL, 1>(g, run, out_row0, pred_out, flat, st);
 }
 

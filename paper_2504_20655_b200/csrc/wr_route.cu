@@ -17,6 +17,9 @@
 // permutation, so the paper's memory limit disappears; the chunk only bounds
 // the work of one warp.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -841,6 +844,14 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         const int tsw = 32 * spl;
         const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc, tsw);
         const int64_t max_tiles = sb / tsw;
+        static const bool trace = getenv("WR_TRACE") != nullptr;
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (trace) {
+            WR_CUDA(cudaEventCreate(&t0));
+            WR_CUDA(cudaEventCreate(&t1));
+            WR_CUDA(cudaEventRecord(t0, st));
+        }
+        const auto h0 = std::chrono::steady_clock::now();
         DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
         DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
         DBuf<int> flat(o.pred_out ? max_tiles : 0);
@@ -856,6 +867,14 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             make_tiles_ordered(g, P->sources.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
             WR_CUDA(cudaEventRecord(b0, st));
+            if (trace) {
+                WR_CUDA(cudaEventSynchronize(b0));
+                float a = 0.f;
+                WR_CUDA(cudaEventElapsedTime(&a, t0, b0));
+                fprintf(stderr, "[wr] local: alloc+tiles %.2f ms device, %.2f ms host (segment %d, %d tiles)\n", a,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(),
+                        segments, ntiles);
+            }
             bf_run(g, run, d_stats.p, st);
             WR_CUDA(cudaEventRecord(b1, st));
             if (o.pred_out) {   // a4 canonical pred of this segment's sources
@@ -884,6 +903,17 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
                 WR_LAUNCH_CHECK();
             }
             ++segments;
+            if (trace) {
+                WR_CUDA(cudaEventRecord(t1, st));
+                WR_CUDA(cudaEventSynchronize(t1));
+                float a = 0.f;
+                WR_CUDA(cudaEventElapsedTime(&a, b2, t1));
+                fprintf(stderr, "[wr] local: gather_send %.2f ms\n", a);
+            }
+        }
+        if (trace) {
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
         }
         cudaEventDestroy(b0);
         cudaEventDestroy(b1);
@@ -1048,6 +1078,10 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
     WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    static const bool trace = getenv("WR_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "[wr] route_orders %.2f ms: local %.2f (bf %.2f, pred %.2f), finish %.2f, plan+rest %.2f\n", ms,
+                s1.ms, s1.bf_ms, s1.pred_ms, s2.ms, ms - s1.ms - s2.ms);
     if (stats) {
         *stats = s2;
         stats->orders = B;
