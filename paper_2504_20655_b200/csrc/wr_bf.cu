@@ -51,6 +51,11 @@ struct OpU32 {
     __device__ __forceinline__ static bool tight(uint32_t du, uint32_t w, uint32_t dv) {
         return du != INF && du + w == dv;
     }
+    // tight and d[u] < d[v], for a finite dv: w > 0 and du + w == dv (an INF
+    // du gives du + w > INF > dv, no wrap for w < 2^31)
+    __device__ __forceinline__ static bool steep_tight(uint32_t du, uint32_t w, uint32_t dv) {
+        return w != 0u && du + w == dv;
+    }
 };
 // fp32 (weights finite, >= 0): one IEEE binary32 RN add, then min. +inf
 // tails give +inf, which never wins.
@@ -68,6 +73,9 @@ struct OpF32 {
     __device__ __forceinline__ static bool tight(uint32_t du, uint32_t w, uint32_t dv) {
         return du != INF && __fadd_rn(__uint_as_float(du), __uint_as_float(w)) == __uint_as_float(dv);
     }
+    __device__ __forceinline__ static bool steep_tight(uint32_t du, uint32_t w, uint32_t dv) {
+        return tight(du, w, dv) && less(du, dv);
+    }
 };
 // int32 with negative weights: exact 64-bit candidate, INF tails skipped.
 struct OpI32N {
@@ -82,6 +90,9 @@ struct OpI32N {
     __device__ __forceinline__ static bool finite(uint32_t x) { return x != INF; }
     __device__ __forceinline__ static bool tight(uint32_t du, uint32_t w, uint32_t dv) {
         return du != INF && (int64_t)(int)du + (int64_t)(int)w == (int64_t)(int)dv;
+    }
+    __device__ __forceinline__ static bool steep_tight(uint32_t du, uint32_t w, uint32_t dv) {
+        return tight(du, w, dv) && less(du, dv);
     }
 };
 
@@ -759,15 +770,14 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
         p_lo = g.in_ptr[c0 + lane];
         p_hi = g.in_ptr[c0 + lane + 1];
     }
-    // steep-tight test of one gathered in-neighbour row for all slots
-    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, bool (&need)[SPL], int (&best)[SPL]) {
+    // steep-tight test of one gathered in-neighbour row for all slots; best
+    // = NEED (-1) while a slot still looks for its pred, SKIP (-2) for slots
+    // that need none (empty, the source itself, unreachable)
+    constexpr int NEED = -1, SKIP = -2;
+    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, int (&best)[SPL]) {
 #pragma unroll
-        for (int j = 0; j < SPL; ++j) {
-            if (need[j] && Op::tight(x.x[j], w, d.x[j]) && Op::less(x.x[j], d.x[j])) {
-                best[j] = u;
-                need[j] = false;
-            }
-        }
+        for (int j = 0; j < SPL; ++j)
+            if (best[j] == NEED && Op::steep_tight(x.x[j], w, d.x[j])) best[j] = u;
     };
     // two vertices per step (lanes 0-15 / 16-31 hold their in-arcs), up to
     // four row gathers in flight; stop when no slot still needs a pred
@@ -781,15 +791,13 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
         const Vec<SPL> d0 = vload<SPL>(Rl + (size_t)v0 * TSW);
         Vec<SPL> d1 = d0;
         if (two) d1 = vload<SPL>(Rl + (size_t)v1 * TSW);
-        bool need0[SPL], need1[SPL];
         int best0[SPL], best1[SPL];
         bool anyn = false;
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
-            need0[j] = src[j] >= 0 && v0 != src[j] && Op::finite(d0.x[j]);
-            need1[j] = two && src[j] >= 0 && v1 != src[j] && Op::finite(d1.x[j]);
-            best0[j] = best1[j] = -1;
-            anyn |= need0[j] | need1[j];
+            best0[j] = (src[j] >= 0 && v0 != src[j] && Op::finite(d0.x[j])) ? NEED : SKIP;
+            best1[j] = (two && src[j] >= 0 && v1 != src[j] && Op::finite(d1.x[j])) ? NEED : SKIP;
+            anyn |= (best0[j] == NEED) | (best1[j] == NEED);
         }
         if (n0 <= 16 && n1 <= 16) {
             const int sub = lane & 15;
@@ -812,16 +820,16 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                 if (k + 1 < n0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
                 if (k < n1) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
                 if (k + 1 < n1) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
-                if (k < n0) test(x00, w00, u00, d0, need0, best0);
-                if (k + 1 < n0) test(x01, w01, u01, d0, need0, best0);
-                if (k < n1) test(x10, w10, u10, d1, need1, best1);
-                if (k + 1 < n1) test(x11, w11, u11, d1, need1, best1);
+                if (k < n0) test(x00, w00, u00, d0, best0);
+                if (k + 1 < n0) test(x01, w01, u01, d0, best0);
+                if (k < n1) test(x10, w10, u10, d1, best1);
+                if (k + 1 < n1) test(x11, w11, u11, d1, best1);
                 anyn = false;
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) anyn |= need0[j] | need1[j];
+                for (int j = 0; j < SPL; ++j) anyn |= (best0[j] == NEED) | (best1[j] == NEED);
             }
         } else {
-            auto slow = [&](int lo, int hi, const Vec<SPL> &d, bool (&need)[SPL], int (&best)[SPL]) {
+            auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[SPL]) {
                 for (int base = lo; base < hi; base += 32) {
                     const int cnt = min(32, hi - base);
                     int my_u = 0;
@@ -833,18 +841,18 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                     for (int k = 0; k < cnt; ++k) {
                         const int u = __shfl_sync(FULL, my_u, k);
                         const uint32_t w = __shfl_sync(FULL, my_w, k);
-                        test(vload<SPL>(Rl + (size_t)u * TSW), w, u, d, need, best);
+                        test(vload<SPL>(Rl + (size_t)u * TSW), w, u, d, best);
                     }
                 }
             };
-            slow(a00, a01, d0, need0, best0);
-            if (two) slow(a10, a11, d1, need1, best1);
+            slow(a00, a01, d0, best0);
+            if (two) slow(a10, a11, d1, best1);
         }
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
-            flat |= need0[j] | need1[j];      // reachable, no steep tight in-arc: flat
-            sp[warp][jv][lane * SPL + j] = need0[j] ? -1 : best0[j];
-            if (two) sp[warp][jv1][lane * SPL + j] = need1[j] ? -1 : best1[j];
+            flat |= (best0[j] == NEED) | (best1[j] == NEED);   // reachable, no steep tight in-arc: flat
+            sp[warp][jv][lane * SPL + j] = max(best0[j], -1);
+            if (two) sp[warp][jv1][lane * SPL + j] = max(best1[j], -1);
         }
     }
     __syncwarp();
