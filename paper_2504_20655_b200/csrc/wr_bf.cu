@@ -744,7 +744,7 @@ struct PredShape {
     static constexpr int PV = 8;     // vertices per warp job
 };
 
-template <class Op, int SPL, int MINB>
+template <class Op, int SPL, int MINB, int PA>
 __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
                                                       const uint32_t *__restrict__ rows,
                                                       const int *__restrict__ slot_row, int64_t out_row0,
@@ -792,13 +792,15 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
         Vec<SPL> d1 = d0;
         if (two) d1 = vload<SPL>(Rl + (size_t)v1 * TSW);
         int best0[SPL], best1[SPL];
-        bool anyn = false;
+        bool m0 = false, m1 = false;
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
             best0[j] = (src[j] >= 0 && v0 != src[j] && Op::finite(d0.x[j])) ? NEED : SKIP;
             best1[j] = (two && src[j] >= 0 && v1 != src[j] && Op::finite(d1.x[j])) ? NEED : SKIP;
-            anyn |= (best0[j] == NEED) | (best1[j] == NEED);
+            m0 |= best0[j] == NEED;
+            m1 |= best1[j] == NEED;
         }
+        const bool need0 = __any_sync(FULL, m0), need1 = __any_sync(FULL, m1);
         if (n0 <= 16 && n1 <= 16) {
             const int sub = lane & 15;
             const int base = lane < 16 ? a00 : a10;
@@ -809,24 +811,38 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                 my_u = g.in_src[base + sub];
                 my_w = g.in_w[base + sub];
             }
-            const int kmax = max(n0, n1);
-            for (int k = 0; k < kmax && __any_sync(FULL, anyn); k += 2) {
-                const int u00 = __shfl_sync(FULL, my_u, k), u01 = __shfl_sync(FULL, my_u, k + 1);
-                const int u10 = __shfl_sync(FULL, my_u, 16 + k), u11 = __shfl_sync(FULL, my_u, 17 + k);
-                const uint32_t w00 = __shfl_sync(FULL, my_w, k), w01 = __shfl_sync(FULL, my_w, k + 1);
-                const uint32_t w10 = __shfl_sync(FULL, my_w, 16 + k), w11 = __shfl_sync(FULL, my_w, 17 + k);
-                Vec<SPL> x00, x01, x10, x11;
-                if (k < n0) x00 = vload<SPL>(Rl + (size_t)u00 * TSW);
-                if (k + 1 < n0) x01 = vload<SPL>(Rl + (size_t)u01 * TSW);
-                if (k < n1) x10 = vload<SPL>(Rl + (size_t)u10 * TSW);
-                if (k + 1 < n1) x11 = vload<SPL>(Rl + (size_t)u11 * TSW);
-                if (k < n0) test(x00, w00, u00, d0, best0);
-                if (k + 1 < n0) test(x01, w01, u01, d0, best0);
-                if (k < n1) test(x10, w10, u10, d1, best1);
-                if (k + 1 < n1) test(x11, w11, u11, d1, best1);
-                anyn = false;
+            // per-vertex early exit: a vertex whose slots all have their
+            // pred stops gathering (its arc count drops to k)
+            int e0 = need0 ? n0 : 0, e1 = need1 ? n1 : 0;
+            for (int k = 0; k < max(e0, e1); k += PA) {
+                int ua[2][PA];
+                uint32_t wa[2][PA];
+                Vec<SPL> x[2][PA];
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) anyn |= (best0[j] == NEED) | (best1[j] == NEED);
+                for (int a = 0; a < PA; ++a) {
+                    ua[0][a] = __shfl_sync(FULL, my_u, (k + a) & 31);
+                    wa[0][a] = __shfl_sync(FULL, my_w, (k + a) & 31);
+                    ua[1][a] = __shfl_sync(FULL, my_u, (16 + k + a) & 31);
+                    wa[1][a] = __shfl_sync(FULL, my_w, (16 + k + a) & 31);
+                }
+#pragma unroll
+                for (int a = 0; a < PA; ++a) {
+                    if (k + a < e0) x[0][a] = vload<SPL>(Rl + (size_t)ua[0][a] * TSW);
+                    if (k + a < e1) x[1][a] = vload<SPL>(Rl + (size_t)ua[1][a] * TSW);
+                }
+#pragma unroll
+                for (int a = 0; a < PA; ++a) {
+                    if (k + a < e0) test(x[0][a], wa[0][a], ua[0][a], d0, best0);
+                    if (k + a < e1) test(x[1][a], wa[1][a], ua[1][a], d1, best1);
+                }
+                m0 = m1 = false;
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) {
+                    m0 |= best0[j] == NEED;
+                    m1 |= best1[j] == NEED;
+                }
+                if (!__any_sync(FULL, m0)) e0 = min(e0, k + PA);
+                if (!__any_sync(FULL, m1)) e1 = min(e1, k + PA);
             }
         } else {
             auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[SPL]) {
@@ -845,8 +861,8 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                     }
                 }
             };
-            slow(a00, a01, d0, best0);
-            if (two) slow(a10, a11, d1, best1);
+            if (need0) slow(a00, a01, d0, best0);
+            if (two && need1) slow(a10, a11, d1, best1);
         }
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
@@ -867,12 +883,12 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
-template <class Op, int SPL, int MINB>
+template <class Op, int SPL, int MINB, int PA>
 static void launch_pred_shape(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
                               cudaStream_t st) {
     const int64_t jobs = (int64_t)run.ntiles * ((g->V + PredShape::PV - 1) / PredShape::PV);
     const unsigned grid = (unsigned)((jobs + PredShape::WARPS - 1) / PredShape::WARPS);
-    bf_pred_kernel<Op, SPL, MINB><<<grid, PredShape::WARPS * 32, 0, st>>>(
+    bf_pred_kernel<Op, SPL, MINB, PA><<<grid, PredShape::WARPS * 32, 0, st>>>(
         g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
     count_launch();
     WR_LAUNCH_CHECK();
@@ -881,12 +897,15 @@ static void launch_pred_shape(const wr_graph *g, const BfRun &run, int64_t out_r
 template <class Op, int SPL>
 static void launch_pred_spl(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
                             cudaStream_t st) {
-    // 256 threads x >= 4 CTAs/SM (64 regs): 45 ms on config 5 vs 61 (no
-    // bound) and 77 (5 CTAs, spills)
-    static const int cfg = env_int("WR_PRED_CONFIG", 1);
-    if (cfg == 1) launch_pred_shape<Op, SPL, 4>(g, run, out_row0, pred_out, flat, st);
-    else if (cfg == 2) launch_pred_shape<Op, SPL, 3>(g, run, out_row0, pred_out, flat, st);
-    else launch_pred_shape<Op, SPL, 1>(g, run, out_row0, pred_out, flat, st);
+    // 256 threads x >= 4 CTAs/SM (64 regs), one arc per vertex per step
+    // with a per-vertex early exit: 34.6 ms on config 5; two arcs per step
+    // (speculative gathers) 40.8; 3 CTAs/SM 40.0; 6-8 CTAs/SM spill (73-83)
+    static const int cfg = env_int("WR_PRED_CONFIG", 5);
+    switch (cfg) {
+        case 1: launch_pred_shape<Op, SPL, 4, 2>(g, run, out_row0, pred_out, flat, st); break;
+        case 8: launch_pred_shape<Op, SPL, 3, 1>(g, run, out_row0, pred_out, flat, st); break;
+        default: launch_pred_shape<Op, SPL, 4, 1>(g, run, out_row0, pred_out, flat, st); break;
+    }
 }
 
 template <class Op>

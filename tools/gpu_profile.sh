@@ -15,6 +15,6 @@ tail -2 gpurun_out/${TAG}_plain.log
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py $ARGS > gpurun_out/${TAG}_ncu_list.log 2>&1
 echo "launch list exit $?"
-ncu --set full --clock-control none --import-source on -k regex:bf_frontier -c 1 \
+ncu --set full --clock-control none --import-source on -k 'regex:bf_frontier|bf_pred' -c 2 \
     -o gpurun_out/${TAG}_bf python bench.py $ARGS > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full exit $?"

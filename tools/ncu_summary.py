@@ -79,19 +79,22 @@ def main():
     # per-kernel DRAM traffic per launch, for bench.py's roofline.traffic
     import json
     import os
-    tj = {}
+    import math
+    tpath = os.path.join(os.path.dirname(outp) or ".", "roofline_traffic.json")
+    tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    tj = {k: v for k, v in tj.items() if math.isfinite(v.get("dram_bytes", float("nan")))}
     for k, t in traffic.items():
         try:
             rd, ru = t["dram__bytes_read.sum"]
             wr, wu = t["dram__bytes_write.sum"]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-            tj[k.replace("void ", "").split("<")[0]] = {
-                "dram_bytes": float(rd) * scale.get(ru, 1) + float(wr) * scale.get(wu, 1),
-                "source": os.path.basename(outp)}
+            b = float(rd) * scale.get(ru, 1) + float(wr) * scale.get(wu, 1)
+            if math.isfinite(b):
+                tj[k.replace("void ", "").split("<")[0]] = {"dram_bytes": b, "source": os.path.basename(outp)}
         except (KeyError, ValueError):
             pass
     if tj:
-        json.dump(tj, open(os.path.join(os.path.dirname(outp) or ".", "roofline_traffic.json"), "w"), indent=1)
+        json.dump(tj, open(tpath, "w"), indent=1)
 
 
 if __name__ == "__main__":
