@@ -1090,14 +1090,21 @@ void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int>
 }
 
 // ------------------------------------------------------ a8 the scheduler --
-int64_t budget_bytes(int64_t requested) {
-    size_t free_b = 0, total_b = 0;
-    WR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+// The HBM budget of one call: the caller's cap (default 180 GB) limited by
+// what the device can still give. `want` = fixed + pooled bytes that cover
+// the whole job in one segment: when libwr's pool already holds that many
+// idle bytes (a repeated call of the same size), no driver query is made -
+// cudaMemGetInfo was measured to stall for up to ~120 ms on the host while
+// another process (nvidia-smi sampling) held the driver.
+int64_t budget_bytes(int64_t requested, int64_t fixed, int64_t want_pooled) {
+    const int64_t cap = requested > 0 ? requested : (int64_t)180e9;
     int dev = 0;
     WR_CUDA(cudaGetDevice(&dev));
-    free_b += pool_idle_bytes(dev);   // reserved by libwr's pool, reusable
-    int64_t b = requested > 0 ? requested : (int64_t)180e9;
-    return std::min<int64_t>(b, (int64_t)(0.9 * (double)free_b));
+    const int64_t idle = (int64_t)pool_idle_bytes(dev);   // reserved by libwr's pool, reusable
+    if (want_pooled > 0 && idle >= want_pooled && fixed + want_pooled <= cap) return fixed + want_pooled;
+    size_t free_b = 0, total_b = 0;
+    WR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    return std::min<int64_t>(cap, (int64_t)(0.9 * (double)(free_b + (size_t)idle)));
 }
 
 // Sources per Bellman-Ford segment: the per-segment working set
@@ -1175,8 +1182,10 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     if (pred && !pred_dev) per_src += 4LL * V;
     wr_graph_info_t gi;
     wr_graph_info(g, &gi);
-    const int64_t budget = budget_bytes(o.hbm_budget);
-    const int64_t sb = sources_per_segment(budget, gi.device_bytes + (64 << 20), per_src, std::max(S, 1), tsw);
+    const int64_t fixed = gi.device_bytes + (64 << 20);
+    const int64_t tiles_all = (std::max(S, 1) + tsw - 1) / tsw;
+    const int64_t budget = budget_bytes(o.hbm_budget, fixed, tiles_all * tsw * per_src);
+    const int64_t sb = sources_per_segment(budget, fixed, per_src, std::max(S, 1), tsw);
     const int64_t max_tiles = sb / tsw;
 
     DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);

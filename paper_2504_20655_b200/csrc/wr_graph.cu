@@ -38,14 +38,69 @@ static cudaMemPool_t pool_for(int dev) {
     return g_pools[dev];
 }
 
+// Block cache in front of the pool: a freed block is kept (not returned to
+// the pool) and handed back to the next request of a fitting size on the
+// same stream - stream order makes the reuse safe - so a repeated call makes
+// no allocation driver calls at all. Those calls were measured to stall the
+// host for up to ~40 ms while another process (nvidia-smi sampling) held
+// the driver. Cached blocks count as idle memory (pool_idle_bytes) and are
+// released on OOM and by wr_release_cached.
+struct CachedBlock {
+    void *p;
+    size_t bytes;
+    cudaStream_t s;
+    int dev;
+};
+static std::mutex g_cache_mu;
+static std::vector<CachedBlock> g_cache;
+static std::vector<std::pair<void *, size_t>> g_live;   // outstanding blocks and their sizes
+constexpr size_t CACHE_MAX_BLOCKS = 256;
+
+static void cache_release(int dev) {   // hand every cached block of dev back to the pool
+    std::vector<CachedBlock> out;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_cache.size();) {
+            if (g_cache[i].dev == dev) {
+                out.push_back(g_cache[i]);
+                g_cache[i] = g_cache.back();
+                g_cache.pop_back();
+            } else {
+                ++i;
+            }
+        }
+    }
+    for (auto &b : out) cudaFreeAsync(b.p, b.s);
+}
+
 void *pool_alloc(size_t bytes, cudaStream_t s) {
     int dev = 0;
     WR_CUDA(cudaGetDevice(&dev));
+    if (bytes == 0) bytes = 1;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        int best = -1;
+        for (int i = 0; i < (int)g_cache.size(); ++i) {
+            const CachedBlock &b = g_cache[i];
+            // fits: at least the request, at most 1/8 (or 1 MB) larger
+            if (b.dev == dev && b.s == s && b.bytes >= bytes && b.bytes - bytes <= std::max<size_t>(bytes / 8, 1 << 20) &&
+                (best < 0 || b.bytes < g_cache[best].bytes))
+                best = i;
+        }
+        if (best >= 0) {
+            CachedBlock b = g_cache[best];
+            g_cache[best] = g_cache.back();
+            g_cache.pop_back();
+            g_live.emplace_back(b.p, b.bytes);
+            return b.p;
+        }
+    }
     void *p = nullptr;
     cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool_for(dev), s);
-    if (e == cudaErrorMemoryAllocation) {   // give idle pool memory back and retry once
+    if (e == cudaErrorMemoryAllocation) {   // give cached and idle pool memory back and retry once
         cudaGetLastError();
-        WR_CUDA(cudaStreamSynchronize(s));
+        cache_release(dev);
+        WR_CUDA(cudaDeviceSynchronize());
         WR_CUDA(cudaMemPoolTrimTo(pool_for(dev), 0));
         e = cudaMallocFromPoolAsync(&p, bytes, pool_for(dev), s);
     }
@@ -54,11 +109,33 @@ void *pool_alloc(size_t bytes, cudaStream_t s) {
         set_error(std::string("device allocation of ") + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
         throw CudaError{e == cudaErrorMemoryAllocation ? WR_ENOMEM : WR_ECUDA};
     }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_live.emplace_back(p, bytes);
     return p;
 }
 
 void pool_free(void *p, cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeAsync(p, s);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t bytes = 0;
+    for (size_t i = 0; i < g_live.size(); ++i)
+        if (g_live[i].first == p) {
+            bytes = g_live[i].second;
+            g_live[i] = g_live.back();
+            g_live.pop_back();
+            break;
+        }
+    if (bytes == 0 || g_cache.size() >= CACHE_MAX_BLOCKS) {
+        cudaFreeAsync(p, s);
+        return;
+    }
+    g_cache.push_back(CachedBlock{p, bytes, s, dev});
 }
 
 size_t pool_idle_bytes(int dev) {
@@ -66,7 +143,13 @@ size_t pool_idle_bytes(int dev) {
     uint64_t reserved = 0, used = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    return reserved > used ? (size_t)(reserved - used) : 0;
+    size_t cached = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto &b : g_cache)
+            if (b.dev == dev) cached += b.bytes;
+    }
+    return (reserved > used ? (size_t)(reserved - used) : 0) + cached;
 }
 
 void set_error(const std::string &msg) { g_err = msg; }
@@ -414,6 +497,8 @@ int32_t wr_version(void) { return 1; }
 wr_status wr_release_cached(int32_t device) {
     return wr::guarded([&] {
         WR_CUDA(cudaSetDevice(device));
+        WR_CUDA(cudaDeviceSynchronize());
+        wr::cache_release(device);
         WR_CUDA(cudaDeviceSynchronize());
         WR_CUDA(cudaMemPoolTrimTo(wr::pool_for(device), 0));
         return WR_OK;

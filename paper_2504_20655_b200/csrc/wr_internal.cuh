@@ -159,7 +159,7 @@ void scan_exclusive_i32(const int *in, int *out, int n, cudaStream_t st);
 
 // -------------------------------------------------------- Bellman-Ford --
 // Segment scheduler (a8): sources per BF batch for a per-source byte cost.
-int64_t budget_bytes(int64_t requested);
+int64_t budget_bytes(int64_t requested, int64_t fixed, int64_t want_pooled);
 int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes,
                             int64_t S, int tsw);
 // Sources per lane (1, 2, 4) for S sources on nsm SMs (env WR_BF_SPL forces).

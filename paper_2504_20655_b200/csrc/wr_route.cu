@@ -822,6 +822,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     StreamScope stream_scope(st);
     const int V = g->V;
     const int64_t nsrc = P->src_hi - P->src_lo;
+    const auto hstart = std::chrono::steady_clock::now();
+    auto hms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hstart).count(); };
     cudaEvent_t e0, e1;
     WR_CUDA(cudaEventCreate(&e0));
     WR_CUDA(cudaEventCreate(&e1));
@@ -836,12 +838,14 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     if (nsrc > 0) {
         wr_graph_info_t gi;
         wr_graph_info(g, &gi);
-        const int64_t budget = budget_bytes(o.hbm_budget);
         const int64_t fixed = gi.device_bytes + (128 << 20);
         int nsm = 0;
         WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
         const int spl = choose_spl(nsrc, nsm);
         const int tsw = 32 * spl;
+        const double h_pre = hms();
+        const int64_t budget = budget_bytes(o.hbm_budget, fixed, (nsrc + tsw - 1) / tsw * tsw * 4LL * V);
+        const double h_budget = hms();
         const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc, tsw);
         const int64_t max_tiles = sb / tsw;
         static const bool trace = getenv("WR_TRACE") != nullptr;
@@ -851,7 +855,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventCreate(&t1));
             WR_CUDA(cudaEventRecord(t0, st));
         }
-        const auto h0 = std::chrono::steady_clock::now();
+        const auto hclock0 = std::chrono::steady_clock::now();
         DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
         DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
         DBuf<int> flat(o.pred_out ? max_tiles : 0);
@@ -867,14 +871,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             make_tiles_ordered(g, P->sources.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
             WR_CUDA(cudaEventRecord(b0, st));
-            if (trace) {
-                WR_CUDA(cudaEventSynchronize(b0));
-                float a = 0.f;
-                WR_CUDA(cudaEventElapsedTime(&a, t0, b0));
-                fprintf(stderr, "[wr] local: alloc+tiles %.2f ms device, %.2f ms host (segment %d, %d tiles)\n", a,
-                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(),
-                        segments, ntiles);
-            }
+            const double host_to_b0 =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hclock0).count();
             bf_run(g, run, d_stats.p, st);
             WR_CUDA(cudaEventRecord(b1, st));
             if (o.pred_out) {   // a4 canonical pred of this segment's sources
@@ -906,9 +904,13 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             if (trace) {
                 WR_CUDA(cudaEventRecord(t1, st));
                 WR_CUDA(cudaEventSynchronize(t1));
-                float a = 0.f;
-                WR_CUDA(cudaEventElapsedTime(&a, b2, t1));
-                fprintf(stderr, "[wr] local: gather_send %.2f ms\n", a);
+                float a = 0.f, c = 0.f;
+                WR_CUDA(cudaEventElapsedTime(&a, t0, b0));
+                WR_CUDA(cudaEventElapsedTime(&c, b2, t1));
+                fprintf(stderr,
+                        "[wr] local segment %d (%d tiles): alloc+tiles %.2f ms device (%.2f ms host), "
+                        "gather_send %.2f ms; host: prologue %.2f, budget %.2f\n",
+                        segments, ntiles, a, host_to_b0, c, h_pre, h_budget - h_pre);
             }
         }
         if (trace) {
@@ -919,10 +921,13 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         cudaEventDestroy(b1);
         cudaEventDestroy(b2);
     }
+    const double h_loop = hms();
     WR_CUDA(cudaEventRecord(e1, st));
     BfTileStats hs;
     WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
+    static const bool trace_l = getenv("WR_TRACE") != nullptr;
+    if (trace_l) fprintf(stderr, "[wr] local host: loop done at %.2f ms, synced at %.2f ms\n", h_loop, hms());
     float ms = 0.f;
     WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
