@@ -180,7 +180,15 @@ typedef struct {
                                 distinct-stop list minus the rank's src_lo
                                 (world 1: 0..S-1; rank r: its own block)    */
     int64_t pred_rows;       /* rows available in pred_out (>= src_hi-src_lo) */
+    int32_t flags;           /* WR_ROUTE_* bits, 0 = defaults               */
+    int32_t reserved;        /* must be 0                                   */
 } wr_route_opts;
+
+/* wr_route_opts.flags: keep the Bellman-Ford working rows in 32 bits even
+ * when the graph admits packed 16-bit rows (int32 weights in [1, 0x3fff];
+ * results are identical either way - a packed sweep whose distances could
+ * exceed 0x7ffe is redone with 32-bit rows). */
+#define WR_ROUTE_ROWS32 1
 
 typedef struct {
     int32_t n;               /* stops (distinct nodes, ascending before routing) */

@@ -22,6 +22,7 @@ WR_OK, WR_EINVAL, WR_ENOMEM, WR_ENEGCYCLE, WR_EOVERFLOW, WR_EUNREACHABLE, WR_ETO
 WR_I32, WR_F32 = 0, 1
 WR_COO, WR_CSR = 0, 1
 WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE = 0, 1, 2
+WR_ROUTE_ROWS32 = 1
 MAX_STOPS = 16
 DEFAULT_CHUNK = 2903040
 I32_INF = np.iinfo(np.int32).max
@@ -65,7 +66,8 @@ class BfStats(C.Structure):
 
 class RouteOpts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("async_", C.c_int32), ("m", C.c_int32), ("chunk", C.c_int64),
-                ("hbm_budget", C.c_int64), ("pred_out", C.c_void_p), ("pred_rows", C.c_int64)]
+                ("hbm_budget", C.c_int64), ("pred_out", C.c_void_p), ("pred_rows", C.c_int64),
+                ("flags", C.c_int32), ("reserved", C.c_int32)]
 
 
 class RouteStats(C.Structure):
@@ -290,7 +292,7 @@ def route_segmented(g: Graph, stops, labels=None, m: int = 1, chunk: int = 0, st
 
 
 def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, results=None,
-                 hbm_budget: int = 0, stream=None, pred_out=None):
+                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0):
     """a2..a7: route every order. Returns (results, stats); results is a
     RESULT_DTYPE numpy array unless a device buffer is passed. pred_out: an
     optional device int32 tensor (>= S rows x V) receiving the canonical
@@ -302,7 +304,7 @@ def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, r
     if results is None:
         results = np.zeros(B, dtype=RESULT_DTYPE)
     o = RouteOpts(_stream_ptr(stream), 0, m, chunk, hbm_budget, _ptr(pred_out),
-                  int(pred_out.shape[0]) if pred_out is not None else 0)
+                  int(pred_out.shape[0]) if pred_out is not None else 0, flags)
     st = RouteStats()
     _check(lib.wr_route_orders(g.handle, _ptr(ptr), _ptr(nodes), B, C.byref(o), _ptr(results), C.byref(st)))
     return results, st
@@ -327,12 +329,12 @@ class OrdersPlan:
     (caller, torch.distributed) -> finish (route this rank's order block)."""
 
     def __init__(self, g: Graph, order_ptr, order_nodes, rank: int, world: int, m: int = 1, chunk: int = 0,
-                 hbm_budget: int = 0, stream=None, pred_out=None):
+                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0):
         self.g = g
         ptr = _arr(order_ptr, np.int64)
         nodes = _arr(order_nodes, np.int32)
         self.opts = RouteOpts(_stream_ptr(stream), 0, m, chunk, hbm_budget, _ptr(pred_out),
-                              int(pred_out.shape[0]) if pred_out is not None else 0)
+                              int(pred_out.shape[0]) if pred_out is not None else 0, flags)
         h = C.c_void_p()
         _check(lib.wr_orders_plan(g.handle, _ptr(ptr), _ptr(nodes), int(ptr.shape[0]) - 1, rank, world,
                                   C.byref(self.opts), C.byref(h)))

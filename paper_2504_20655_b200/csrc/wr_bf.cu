@@ -24,6 +24,7 @@
 //   * pred is not written inside the racy sweep: a4 recomputes the
 //     canonical predecessor from the converged dist (O3), deterministic.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -41,6 +42,12 @@ constexpr uint32_t FULL = 0xffffffffu;
 // INF + w (w < 2^31) never wraps and never beats a finite value: an INF tail
 // relaxes nothing, exactly like the oracle's "skip d[u] == INF".
 struct OpU32 {
+    static constexpr int PACK = 1;   // sources per 32-bit word
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
+    __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
+    __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
+    __device__ __forceinline__ static uint32_t half(uint32_t x, int) { return x; }
     static constexpr uint32_t INF = 0x7fffffffu;
     static constexpr uint32_t ZERO = 0u;
     __device__ __forceinline__ static uint32_t relax(uint32_t d, uint32_t du, uint32_t w) {
@@ -60,6 +67,12 @@ struct OpU32 {
 // fp32 (weights finite, >= 0): one IEEE binary32 RN add, then min. +inf
 // tails give +inf, which never wins.
 struct OpF32 {
+    static constexpr int PACK = 1;   // sources per 32-bit word
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
+    __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
+    __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
+    __device__ __forceinline__ static uint32_t half(uint32_t x, int) { return x; }
     static constexpr uint32_t INF = 0x7f800000u;
     static constexpr uint32_t ZERO = 0u;
     __device__ __forceinline__ static uint32_t relax(uint32_t d, uint32_t du, uint32_t w) {
@@ -79,6 +92,12 @@ struct OpF32 {
 };
 // int32 with negative weights: exact 64-bit candidate, INF tails skipped.
 struct OpI32N {
+    static constexpr int PACK = 1;   // sources per 32-bit word
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
+    __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
+    __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
+    __device__ __forceinline__ static uint32_t half(uint32_t x, int) { return x; }
     static constexpr uint32_t INF = 0x7fffffffu;
     static constexpr uint32_t ZERO = 0u;
     __device__ __forceinline__ static uint32_t relax(uint32_t d, uint32_t du, uint32_t w) {
@@ -93,6 +112,38 @@ struct OpI32N {
     }
     __device__ __forceinline__ static bool steep_tight(uint32_t du, uint32_t w, uint32_t dv) {
         return tight(du, w, dv) && less(du, dv);
+    }
+};
+// Nonnegative int32 distances that provably stay below 2^15 - 1, two per
+// 32-bit word (packed u16, DPX VIADDMNMX.U16x2: two relaxations per
+// instruction, half the bytes per source row). INF = 0x7fff per half; with
+// w clamped to <= 0x7fff, du + w <= 0xfffe never wraps and an INF tail
+// never beats a finite value. A path longer than 0x7ffe cannot be
+// represented: the sweep flags a tile whose stored distances reach
+// 0x7fff - max_w (any longer candidate could be clipped) and the caller
+// redoes the segment with 32-bit rows, so results are exact either way.
+struct OpU16 {
+    static constexpr int PACK = 2;
+    static constexpr uint32_t INF = 0x7fff7fffu;
+    static constexpr uint32_t INF1 = 0x7fffu;
+    static constexpr uint32_t ZERO = 0u;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) {
+        w = min(w, 0x7fffu);
+        return w | (w << 16);
+    }
+    __device__ __forceinline__ static uint32_t relax(uint32_t d, uint32_t du, uint32_t w2) {
+        return __viaddmin_u16x2(du, w2, d);
+    }
+    __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+    __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return __vcmpltu2(a, b) != 0u; }
+    __device__ __forceinline__ static bool overflow(uint32_t d, uint32_t thr2) {
+        return (__vcmpgeu2(d, thr2) & ~__vcmpeq2(d, INF)) != 0u;
+    }
+    __device__ __forceinline__ static uint32_t half(uint32_t x, int h) { return (x >> (16 * h)) & 0xffffu; }
+    // per-slot (one half) predicates for the pred pass
+    __device__ __forceinline__ static bool finite(uint32_t x1) { return x1 != INF1; }
+    __device__ __forceinline__ static bool steep_tight(uint32_t du1, uint32_t w, uint32_t dv1) {
+        return w != 0u && du1 + w == dv1;   // w > 0 on every packed graph
     }
 };
 
@@ -138,14 +189,14 @@ template <class Op, int SPL>
 __device__ __forceinline__ Vec<SPL> vmin(const Vec<SPL> &a, const Vec<SPL> &b) {
     Vec<SPL> r;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) r.x[j] = Op::less(a.x[j], b.x[j]) ? a.x[j] : b.x[j];
+    for (int j = 0; j < SPL; ++j) r.x[j] = Op::min_word(a.x[j], b.x[j]);
     return r;
 }
 template <class Op, int SPL>
 __device__ __forceinline__ bool vless(const Vec<SPL> &a, const Vec<SPL> &b) {
     bool r = false;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) r |= Op::less(a.x[j], b.x[j]);
+    for (int j = 0; j < SPL; ++j) r |= Op::any_less(a.x[j], b.x[j]);
     return r;
 }
 
@@ -199,7 +250,7 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
         bool take = false;
         if (lane < cnt) {
             my_u = g.in_src[base + lane];
-            my_w = g.in_w[base + lane];
+            my_w = Op::prep_w(g.in_w[base + lane]);
             take = !DELTA || pchg.test(my_u);
         }
         uint32_t m = __ballot_sync(FULL, take);
@@ -243,7 +294,7 @@ template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const ChgView pchg,
                                                uint32_t *nxt, int *nlist, int *nlen, int2 *q,
-                                               uint32_t *touched) {
+                                               uint32_t *touched, bool &ovf, uint32_t thr2) {
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
@@ -264,7 +315,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 #pragma unroll
         for (int j = 0; j < AQ; ++j) {
             const bool take = arc[j].x >= 0 && (!DELTA || pchg.test(arc[j].x));
-            if (take && c < QC) q[lane * QC + c] = arc[j];
+            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x, (int)Op::prep_w((uint32_t)arc[j].y));
             c += take ? 1 : 0;
         }
     }
@@ -351,7 +402,14 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
             // first write of a row covers every slot (untouched slots stay INF)
             const bool f = ok[k] && !((tw >> iv[k]) & 1u);
             const bool ch = ok[k] && vless<Op, SPL>(d[k], e[k]);
-            if (ch || f) vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, vmin<Op, SPL>(d[k], e[k]));
+            if (ch || f) {
+                const Vec<SPL> nv = vmin<Op, SPL>(d[k], e[k]);
+                vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, nv);
+                if (Op::PACK > 1) {
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) ovf |= Op::overflow(nv.x[j], thr2);
+                }
+            }
             if (__any_sync(FULL, ch)) chg |= 1u << iv[k];
         }
     }
@@ -405,8 +463,10 @@ template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int T
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
-                                                               BfTileStats *stats) {
-    constexpr int TSW = 32 * SPL;
+                                                               BfTileStats *stats, uint32_t thr2,
+                                                               const int *__restrict__ tile_order) {
+    constexpr int TSW = 32 * SPL;              // 32-bit words per row
+    constexpr int TS = TSW * Op::PACK;         // sources per tile
     constexpr int NWARPS = NT / 32;
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ int s_tile;
@@ -422,7 +482,10 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
     int2 *const q = reinterpret_cast<int2 *>(smem + L.queue) + warp * (32 * QC);
 
     for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
+        if (threadIdx.x == 0) {
+            const int k = atomicAdd(tile_counter, 1);
+            s_tile = (k < ntiles && tile_order) ? tile_order[k] : k;
+        }
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
@@ -444,8 +507,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         __syncthreads();
         if (warp == 0) {   // seed: d[s][slot] = 0; the sources "changed" in round 0
             if (!DENSE) {  // the seed vertices' rows: INF everywhere first
-                for (int k = 0; k < TSW; ++k) {
-                    const int s = tile_src[tile * TSW + k];
+                for (int k = 0; k < TS; ++k) {
+                    const int s = tile_src[tile * TS + k];
                     if (s >= 0) {
                         uint32_t *row = R + (size_t)s * TSW;
                         for (int c = lane; c < TSW / 4; c += 32) reinterpret_cast<uint4 *>(row)[c] = inf4;
@@ -454,11 +517,12 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 __syncwarp();
             }
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) {
-                const int slot = lane * SPL + j;
-                const int s = tile_src[tile * TSW + slot];
+            for (int j = 0; j < SPL * Op::PACK; ++j) {
+                const int slot = lane * SPL * Op::PACK + j;
+                const int s = tile_src[tile * TS + slot];
                 if (s >= 0) {
-                    R[(size_t)s * TSW + slot] = Op::ZERO;
+                    if (Op::PACK == 1) R[(size_t)s * TSW + slot] = Op::ZERO;
+                    else reinterpret_cast<uint16_t *>(R)[(size_t)s * TS + slot] = 0;
                     atomicOr(&chg[s >> 5].x, 1u << (s & 31));   // stamp 0 = round 0
                     atomicOr(&touched[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
@@ -472,7 +536,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 
         int rounds = 0;
         unsigned long long relax = 0, visits = 0;
-        bool more = true;
+        bool more = true, ovf = false;
         for (int r = 1; more; ++r) {
             int any = 0;
             if (DENSE) {
@@ -481,7 +545,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 for (int w = warp; w < NW; w += NWARPS) {
                     const uint32_t m = cur[w];
                     const uint32_t c = relax_word<Op, false, SPL, QC, VB, TPS, false>(
-                        g, R, w, m, lane, relax, ChgView{chg, 0u}, nxt, list, &s_len[0], q, touched);
+                        g, R, w, m, lane, relax, ChgView{chg, 0u}, nxt, list, &s_len[0], q, touched, ovf, thr2);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
@@ -495,7 +559,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
                     const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, false>(g, R, w, m, lane, relax, pc, nxt,
-                                                                                     nullptr, nullptr, q, touched);
+                                                                                     nullptr, nullptr, q, touched, ovf,
+                                                                                     thr2);
                     if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
@@ -520,7 +585,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
                     const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, true>(g, R, w, m, lane, relax, pc, nxt,
-                                                                                    ln, nlen, q, touched);
+                                                                                    ln, nlen, q, touched, ovf, thr2);
                     if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
@@ -547,8 +612,9 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 }
             }
         }
+        if (Op::PACK > 1 && __syncthreads_or(ovf) && threadIdx.x == 0) atomicOr(&stats->overflow, 1);
         // per-tile statistics (one lane per warp contributes its arc count)
-        if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TSW);
+        if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TS);
         if (lane == 0 && visits) atomicAdd(&stats->visits, visits);
         if (threadIdx.x == 0) atomicMax(&stats->rounds_max, rounds);
         __syncthreads();
@@ -573,7 +639,8 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     const int grid = (int)std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
     DBuf<int> counter(1);
     WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
-    kern<<<grid, NT, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p, run.max_rounds, d_stats);
+    kern<<<grid, NT, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p, run.max_rounds, d_stats,
+                                 run.ovf_thr * 0x10001u, run.tile_order);
     count_launch();
     WR_LAUNCH_CHECK();
     WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
@@ -627,9 +694,116 @@ static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     }
 }
 
-void bf_run(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
-    if (run.ntiles <= 0) return;
-    if (g->wtype == WR_F32) launch_sweep<OpF32>(g, run, d_stats, st);
+// ----------------------------------------------- tile claim order (LPT) --
+// A tile's sweep time grows with its rounds, i.e. with the eccentricity of
+// its sources; persistent CTAs claiming tiles in Morton order leave SMs idle
+// while the last long tiles finish (C5: SMs active 81 % of the sweep). Tiles
+// are claimed longest-first instead: key = max over the tile's sources of
+// the BFS hop distance from a central vertex (the vertex nearest the centre
+// of the xy/level bounding box, else vertex 0), computed once per graph.
+__global__ void center_pick_kernel(const int *xy, const int *z, int V, int cx2, int cy2, int cz2,
+                                   unsigned long long *best) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const long long d = llabs(2LL * xy[2 * v] - cx2) + llabs(2LL * xy[2 * v + 1] - cy2) +
+                        (z ? llabs(2LL * z[v] - cz2) : 0LL);
+    atomicMin(best, ((unsigned long long)d << 32) | (unsigned)v);
+}
+
+__global__ void bfs_level_kernel(DevGraph g, int *hop, int level, int *changed) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= g.V || hop[v] != level) return;
+    bool any = false;
+    for (int e = g.out_ptr[v]; e < g.out_ptr[v + 1]; ++e) {
+        const int x = g.out_dst[e];
+        if (hop[x] == INT_MAX) {   // racing writers store the same value
+            hop[x] = level + 1;
+            any = true;
+        }
+    }
+    if (any) *changed = 1;
+}
+
+__global__ void tile_key_kernel(const int *tile_src, int ntiles, int ts, const int *hop, long long *key) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    int m = 0;
+    for (int k = 0; k < ts; ++k) {
+        const int s = tile_src[(size_t)t * ts + k];
+        if (s >= 0) m = max(m, hop[s] == INT_MAX ? 0 : hop[s]);
+    }
+    key[t] = ((long long)(INT_MAX - m) << 32) | t;   // ascending sort = longest first, then index
+}
+
+__global__ void fill_i32_kernel(int *p, int n, int v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+static const int *center_hops(const wr_graph *g, cudaStream_t st) {
+    if (g->hop_c.p) return g->hop_c.p;
+    const int V = g->V;
+    DBuf<int> hop;
+    {   // graph-lifetime buffer: allocated (and later freed) on the legacy stream
+        StreamScope s0(0);
+        hop.alloc(V);
+        WR_CUDA(cudaStreamSynchronize(0));
+    }
+    fill_i32_kernel<<<(V + 255) / 256, 256, 0, st>>>(hop.p, V, INT_MAX);
+    count_launch();
+    int c = 0;
+    if (g->xy.p) {
+        DBuf<unsigned long long> best(1);
+        const unsigned long long init = ~0ull;
+        WR_CUDA(cudaMemcpyAsync(best.p, &init, 8, cudaMemcpyHostToDevice, st));
+        center_pick_kernel<<<(V + 255) / 256, 256, 0, st>>>(g->xy.p, g->z.p, V, g->bbox[0] + g->bbox[1],
+                                                            g->bbox[2] + g->bbox[3], g->bbox[4] + g->bbox[5], best.p);
+        count_launch();
+        unsigned long long hb = 0;
+        WR_CUDA(cudaMemcpyAsync(&hb, best.p, 8, cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        c = (int)(hb & 0xffffffffu);
+    }
+    const int zero = 0;
+    WR_CUDA(cudaMemcpyAsync(hop.p + c, &zero, 4, cudaMemcpyHostToDevice, st));
+    DBuf<int> changed(1);
+    for (int level = 0; level < V; ++level) {
+        WR_CUDA(cudaMemsetAsync(changed.p, 0, 4, st));
+        bfs_level_kernel<<<(V + 255) / 256, 256, 0, st>>>(g->view(), hop.p, level, changed.p);
+        count_launch();
+        int h = 0;
+        WR_CUDA(cudaMemcpyAsync(&h, changed.p, 4, cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        if (!h) break;
+    }
+    WR_LAUNCH_CHECK();
+    g->hop_c = std::move(hop);
+    return g->hop_c.p;
+}
+
+void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStream_t st) {
+    if (run0.ntiles <= 0) return;
+    BfRun run = run0;
+    static const bool no_lpt = getenv("WR_NO_LPT") != nullptr;
+    DBuf<int> order;
+    if (!no_lpt && !run.tile_order && run.ntiles > 1) {
+        const int *hop = center_hops(g, st);
+        DBuf<long long> key(run.ntiles);
+        tile_key_kernel<<<(run.ntiles + 127) / 128, 128, 0, st>>>(run.tile_src, run.ntiles, run.tsw(), hop, key.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+        std::vector<long long> hk(run.ntiles);
+        WR_CUDA(cudaMemcpyAsync(hk.data(), key.p, 8 * run.ntiles, cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        std::sort(hk.begin(), hk.end());
+        std::vector<int> ho(run.ntiles);
+        for (int i = 0; i < run.ntiles; ++i) ho[i] = (int)(hk[i] & 0xffffffffll);
+        order.alloc(run.ntiles);
+        WR_CUDA(cudaMemcpyAsync(order.p, ho.data(), 4 * run.ntiles, cudaMemcpyHostToDevice, st));
+        run.tile_order = order.p;
+    }
+    if (run.pack == 2) launch_sweep<OpU16>(g, run, d_stats, st);
+    else if (g->wtype == WR_F32) launch_sweep<OpF32>(g, run, d_stats, st);
     else if (g->has_negative) launch_sweep<OpI32N>(g, run, d_stats, st);
     else launch_sweep<OpU32>(g, run, d_stats, st);
 }
@@ -740,18 +914,23 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
 // memory and written as one full 32-B sector per source row (8 vertices x
 // 4 B), 4 rows per store instruction.
 struct PredShape {
-    static constexpr int WARPS = 8;
-    static constexpr int PV = 8;     // vertices per warp job
+    static constexpr int PV = 8;     // vertices per warp job (full 32-B output sectors)
 };
 
-template <class Op, int SPL, int MINB, int PA>
-__global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
+// PW warps per CTA (8 for 32-bit rows, 4 for packed rows: the output
+// staging sp[PW][PV][TS + 1] stays under the 48 KB static limit).
+template <class Op, int SPL, int MINB, int PA, int PW>
+__global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
                                                       const uint32_t *__restrict__ rows,
                                                       const int *__restrict__ slot_row, int64_t out_row0,
-                                                      int32_t *pred_out, int *flat_tiles) {
-    constexpr int TSW = 32 * SPL;
-    constexpr int PW = PredShape::WARPS, PV = PredShape::PV;
-    __shared__ int32_t sp[PW][PV][TSW + 1];
+                                                      int32_t *__restrict__ pred_out, int *flat_tiles) {
+    constexpr int TSW = 32 * SPL;           // 32-bit words per row
+    static_assert(PredShape::PV == 8, "the output stores write 8 columns per slot");
+    constexpr int P = Op::PACK;
+    constexpr int TS = TSW * P;             // sources (slots) per tile
+    constexpr int NS = SPL * P;             // slots per lane
+    constexpr int PV = PredShape::PV;
+    __shared__ int32_t sp[PW][PV][TS + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int V = g.V;
     const int chunks = (V + PV - 1) / PV;
@@ -760,9 +939,9 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
     const int tile = (int)(job / chunks);
     const int c0 = (int)(job % chunks) * PV;
     const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
-    int src[SPL];
+    int src[NS];
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) src[j] = tile_src[tile * TSW + lane * SPL + j];
+    for (int j = 0; j < NS; ++j) src[j] = tile_src[tile * TS + lane * NS + j];
     bool flat = false;
     const int nv = min(PV, V - c0);
     int p_lo = 0, p_hi = 0;
@@ -772,15 +951,19 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
     }
     // steep-tight test of one gathered in-neighbour row for all slots; best
     // = NEED (-1) while a slot still looks for its pred, SKIP (-2) for slots
-    // that need none (empty, the source itself, unreachable)
+    // that need none (empty, the source itself, unreachable). Slot j*P + h
+    // is half h of the lane's word j.
     constexpr int NEED = -1, SKIP = -2;
-    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, int (&best)[SPL]) {
+    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, int (&best)[NS]) {
 #pragma unroll
         for (int j = 0; j < SPL; ++j)
-            if (best[j] == NEED && Op::steep_tight(x.x[j], w, d.x[j])) best[j] = u;
+#pragma unroll
+            for (int h = 0; h < P; ++h)
+                if (best[j * P + h] == NEED && Op::steep_tight(Op::half(x.x[j], h), w, Op::half(d.x[j], h)))
+                    best[j * P + h] = u;
     };
-    // two vertices per step (lanes 0-15 / 16-31 hold their in-arcs), up to
-    // four row gathers in flight; stop when no slot still needs a pred
+    // two vertices per step (lanes 0-15 / 16-31 hold their in-arcs), PA
+    // in-arcs of each per step; stop when no slot still needs a pred
     for (int jv = 0; jv < nv; jv += 2) {
         const bool two = jv + 1 < nv;
         const int jv1 = two ? jv + 1 : jv;
@@ -791,15 +974,18 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
         const Vec<SPL> d0 = vload<SPL>(Rl + (size_t)v0 * TSW);
         Vec<SPL> d1 = d0;
         if (two) d1 = vload<SPL>(Rl + (size_t)v1 * TSW);
-        int best0[SPL], best1[SPL];
+        int best0[NS], best1[NS];
         bool m0 = false, m1 = false;
 #pragma unroll
-        for (int j = 0; j < SPL; ++j) {
-            best0[j] = (src[j] >= 0 && v0 != src[j] && Op::finite(d0.x[j])) ? NEED : SKIP;
-            best1[j] = (two && src[j] >= 0 && v1 != src[j] && Op::finite(d1.x[j])) ? NEED : SKIP;
-            m0 |= best0[j] == NEED;
-            m1 |= best1[j] == NEED;
-        }
+        for (int j = 0; j < SPL; ++j)
+#pragma unroll
+            for (int h = 0; h < P; ++h) {
+                const int k = j * P + h;
+                best0[k] = (src[k] >= 0 && v0 != src[k] && Op::finite(Op::half(d0.x[j], h))) ? NEED : SKIP;
+                best1[k] = (two && src[k] >= 0 && v1 != src[k] && Op::finite(Op::half(d1.x[j], h))) ? NEED : SKIP;
+                m0 |= best0[k] == NEED;
+                m1 |= best1[k] == NEED;
+            }
         const bool need0 = __any_sync(FULL, m0), need1 = __any_sync(FULL, m1);
         if (n0 <= 16 && n1 <= 16) {
             const int sub = lane & 15;
@@ -837,7 +1023,7 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                 }
                 m0 = m1 = false;
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) {
+                for (int j = 0; j < NS; ++j) {
                     m0 |= best0[j] == NEED;
                     m1 |= best1[j] == NEED;
                 }
@@ -845,7 +1031,7 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
                 if (!__any_sync(FULL, m1)) e1 = min(e1, k + PA);
             }
         } else {
-            auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[SPL]) {
+            auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[NS]) {
                 for (int base = lo; base < hi; base += 32) {
                     const int cnt = min(32, hi - base);
                     int my_u = 0;
@@ -865,30 +1051,46 @@ __global__ void __launch_bounds__(PredShape::WARPS * 32, MINB) bf_pred_kernel(De
             if (two && need1) slow(a10, a11, d1, best1);
         }
 #pragma unroll
-        for (int j = 0; j < SPL; ++j) {
+        for (int j = 0; j < NS; ++j) {
             flat |= (best0[j] == NEED) | (best1[j] == NEED);   // reachable, no steep tight in-arc: flat
-            sp[warp][jv][lane * SPL + j] = max(best0[j], -1);
-            if (two) sp[warp][jv1][lane * SPL + j] = max(best1[j], -1);
+            sp[warp][jv][lane * NS + j] = max(best0[j], -1);
+            if (two) sp[warp][jv1][lane * NS + j] = max(best1[j], -1);
         }
     }
     __syncwarp();
-    for (int s0 = 0; s0 < TSW; s0 += 32 / PV) {
-        const int sl_in = s0 + lane / PV, jv = lane % PV;
-        const int sl = tile * TSW + sl_in;
-        if (jv < nv && tile_src[sl] >= 0) {
-            const int64_t row = out_row0 + (slot_row ? slot_row[sl] : sl);
-            pred_out[row * (int64_t)V + c0 + jv] = sp[warp][jv][sl_in];
+    // lane -> slots lane, lane + 32, ...: each writes its 8 columns of the
+    // source's row as one full 32-B sector (two 16-B stores); the slots'
+    // source and output row are loaded once, all at the same time
+    const bool vec = (V & 3) == 0 && nv == PV;
+    int srow[TS / 32];
+#pragma unroll
+    for (int k = 0; k < TS / 32; ++k) {
+        const int sl = tile * TS + lane + 32 * k;
+        srow[k] = tile_src[sl] < 0 ? -1 : (slot_row ? slot_row[sl] : sl);
+    }
+#pragma unroll
+    for (int k = 0; k < TS / 32; ++k) {
+        if (srow[k] < 0) continue;
+        const int sl_in = lane + 32 * k;
+        int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
+        if (vec) {
+            reinterpret_cast<int4 *>(dst)[0] =
+                make_int4(sp[warp][0][sl_in], sp[warp][1][sl_in], sp[warp][2][sl_in], sp[warp][3][sl_in]);
+            reinterpret_cast<int4 *>(dst)[1] =
+                make_int4(sp[warp][4][sl_in], sp[warp][5][sl_in], sp[warp][6][sl_in], sp[warp][7][sl_in]);
+        } else {
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = sp[warp][jv][sl_in];
         }
     }
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
-template <class Op, int SPL, int MINB, int PA>
+template <class Op, int SPL, int MINB, int PA, int PW = 8 / Op::PACK>
 static void launch_pred_shape(const wr_graph *g, const BfRun &run, int64_t out_row0, int32_t *pred_out, int *flat,
                               cudaStream_t st) {
     const int64_t jobs = (int64_t)run.ntiles * ((g->V + PredShape::PV - 1) / PredShape::PV);
-    const unsigned grid = (unsigned)((jobs + PredShape::WARPS - 1) / PredShape::WARPS);
-    bf_pred_kernel<Op, SPL, MINB, PA><<<grid, PredShape::WARPS * 32, 0, st>>>(
+    const unsigned grid = (unsigned)((jobs + PW - 1) / PW);
+    bf_pred_kernel<Op, SPL, MINB, PA, PW><<<grid, PW * 32, 0, st>>>(
         g->view(), run.tile_src, run.ntiles, run.rows, run.slot_row, out_row0, pred_out, flat);
     count_launch();
     WR_LAUNCH_CHECK();
@@ -900,6 +1102,13 @@ static void launch_pred_spl(const wr_graph *g, const BfRun &run, int64_t out_row
     // 256 threads x >= 4 CTAs/SM (64 regs), one arc per vertex per step
     // with a per-vertex early exit: 34.6 ms on config 5; two arcs per step
     // (speculative gathers) 40.8; 3 CTAs/SM 40.0; 6-8 CTAs/SM spill (73-83)
+    if constexpr (Op::PACK == 2) {   // 128 threads (staging 33 KB) x 6 CTAs/SM
+        static const int cfg16 = env_int("WR_PRED16_CONFIG", 6);
+        if (cfg16 == 4) launch_pred_shape<Op, SPL, 4, 1>(g, run, out_row0, pred_out, flat, st);
+        else if (cfg16 == 8) launch_pred_shape<Op, SPL, 8, 1, 2>(g, run, out_row0, pred_out, flat, st);
+        else launch_pred_shape<Op, SPL, 6, 1>(g, run, out_row0, pred_out, flat, st);
+        return;
+    }
     static const int cfg = env_int("WR_PRED_CONFIG", 5);
     switch (cfg) {
         case 1: launch_pred_shape<Op, SPL, 4, 2>(g, run, out_row0, pred_out, flat, st); break;
@@ -919,6 +1128,11 @@ static void launch_pred(const wr_graph *g, const BfRun &run, int64_t out_row0, i
 void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int64_t, const int *targets, int T,
                       void *dist_out, int32_t *pred_out, int *d_flat_tiles, cudaStream_t st) {
     if (run.ntiles <= 0 || (!dist_out && !pred_out)) return;
+    if (run.pack == 2) {   // packed rows: pred only (no flat vertices: every weight > 0)
+        if (dist_out) WR_THROW(WR_EINTERNAL, "bf_write_outputs: dist output from packed rows");
+        if (pred_out) launch_pred<OpU16>(g, run, out_row0, pred_out, d_flat_tiles, st);
+        return;
+    }
     if (pred_out && !g->has_negative) {     // fast vectorised pred pass (flat vertices flagged)
         if (g->wtype == WR_F32) launch_pred<OpF32>(g, run, out_row0, pred_out, d_flat_tiles, st);
         else launch_pred<OpU32>(g, run, out_row0, pred_out, d_flat_tiles, st);

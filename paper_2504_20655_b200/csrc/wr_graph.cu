@@ -265,7 +265,7 @@ __global__ void csr_to_src_kernel(const int64_t *row_ptr, int V, int *src) {
 }
 
 __global__ void validate_kernel(const int *src, const int *dst, uint32_t *w, int64_t E, int V, int wtype,
-                                int *flags, unsigned *max_abs, int *has_neg, int64_t *in_deg,
+                                int *flags, unsigned *max_abs, int *has_neg, int *has_zero, int64_t *in_deg,
                                 int64_t *out_deg) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
@@ -282,6 +282,7 @@ __global__ void validate_kernel(const int *src, const int *dst, uint32_t *w, int
     } else {
         const int x = (int)bits;
         if (x < 0) atomicOr(has_neg, 1);
+        if (x == 0) atomicOr(has_zero, 1);
         const unsigned a = x < 0 ? (unsigned)(-(int64_t)x) : (unsigned)x;
         atomicMax(max_abs, a);
     }
@@ -410,14 +411,14 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
     }
     DBuf<uint32_t> w = to_device<uint32_t>((const uint32_t *)d->w, E, st);
 
-    DBuf<int> flags(3);          // [0] flags, [1] max_abs, [2] has_neg
+    DBuf<int> flags(4);          // [0] flags, [1] max_abs, [2] has_neg, [3] has_zero (int)
     DBuf<int64_t> in_deg(V + 1), out_deg(V + 1);
-    WR_CUDA(cudaMemsetAsync(flags.p, 0, 12, st));
+    WR_CUDA(cudaMemsetAsync(flags.p, 0, 16, st));
     WR_CUDA(cudaMemsetAsync(in_deg.p, 0, (V + 1) * 8, st));
     WR_CUDA(cudaMemsetAsync(out_deg.p, 0, (V + 1) * 8, st));
     if (E) {
         validate_kernel<<<grid_for(E, 256), 256, 0, st>>>(src.p, dst.p, w.p, E, V, d->wtype, flags.p,
-                                                         (unsigned *)(flags.p + 1), flags.p + 2,
+                                                         (unsigned *)(flags.p + 1), flags.p + 2, flags.p + 3,
                                                          in_deg.p, out_deg.p);
         count_launch();
         WR_LAUNCH_CHECK();
@@ -440,13 +441,14 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
         WR_LAUNCH_CHECK();
         WR_CUDA(cudaMemcpyAsync(g->bbox, bbox.p, sizeof(g->bbox), cudaMemcpyDeviceToHost, st));
     }
-    int hf[3];
-    WR_CUDA(cudaMemcpyAsync(hf, flags.p, 12, cudaMemcpyDeviceToHost, st));
+    int hf[4];
+    WR_CUDA(cudaMemcpyAsync(hf, flags.p, 16, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
     if (hf[0] & BAD_INDEX) return fail(WR_EINVAL, "wr_graph_load: arc endpoint outside [0, V)");
     if (hf[0] & BAD_WEIGHT) return fail(WR_EINVAL, "wr_graph_load: fp32 weight NaN, infinite or negative");
     if (hf[0] & BAD_XY) return fail(WR_EINVAL, "wr_graph_load: |xy| >= 2^20");
     g->has_negative = hf[2];
+    g->has_zero = hf[3];
     g->max_abs_w = hf[1];
     if (d->wtype == WR_I32 && (int64_t)(V - 1) * (int64_t)(uint32_t)hf[1] >= (int64_t)INT32_MAX)
         return fail(WR_EOVERFLOW, "wr_graph_load: (V-1)*max|w| >= INT32_MAX (reading A7)");

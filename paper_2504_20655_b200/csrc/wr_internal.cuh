@@ -138,12 +138,14 @@ struct wr_graph {
     int64_t E = 0;
     int wtype = WR_I32;
     int has_negative = 0;
+    int has_zero = 0;       // an int32 arc of weight 0
     int32_t max_abs_w = 0;
     wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
     wr::DBuf<uint32_t> in_w;
     wr::DBuf<int2> in_arc;
     wr::DBuf<int> xy;       // [V*2] or empty
     wr::DBuf<int> z;        // [V] rack level or empty
+    mutable wr::DBuf<int> hop_c;  // [V] BFS hops from a central vertex (tile cost key), built on first use
     int bbox[6] = {0, 0, 0, 0, 0, 0};   // xmin, xmax, ymin, ymax, zmin, zmax
     wr::DevGraph view() const {
         return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, in_arc.p, out_ptr.p, out_dst.p};
@@ -171,8 +173,12 @@ struct BfRun {              // one BF segment over tiles of 32*spl sources
     uint32_t *rows;         // [ntiles][V][tsw] working distances (output)
     int variant;
     int max_rounds;
-    int spl;                // sources per lane; tsw = 32*spl slots per tile
+    int spl;                // 32-bit words per lane; a row has 32*spl words
     const int *slot_row = nullptr;  // [ntiles*tsw] output row offset per slot (null = identity)
+    int pack = 1;           // sources per 32-bit word: 1, or 2 (packed u16 distances)
+    const int *tile_order = nullptr;  // [ntiles] claim order of the tiles (null = 0..ntiles-1)
+    uint32_t ovf_thr = 0;   // pack 2: a stored distance >= ovf_thr flags a possible u16 overflow
+    int tsw() const { return 32 * spl * pack; }   // sources (slots) per tile
 };
 
 struct BfTileStats {        // per-call accumulators (device)
@@ -180,6 +186,7 @@ struct BfTileStats {        // per-call accumulators (device)
     int rounds_max;
     int negcycle_tile;      // -1 or a tile with a negative cycle
     unsigned long long visits;  // candidate (vertex, round) visits
+    int overflow;           // pack 2: a stored distance reached ovf_thr (redo with 32-bit rows)
 };
 
 // Launches the relaxation sweep of a segment on stream st (a3).

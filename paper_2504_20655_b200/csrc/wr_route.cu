@@ -372,7 +372,7 @@ __global__ void owned_count_kernel(const int *stops, const int *n_arr, const int
 __global__ void gather_send_kernel(const int *stops, const int *n_arr, const int *status, int64_t B,
                                    const int *src_row, int64_t own_lo, int64_t own_hi, int64_t seg_lo,
                                    int64_t seg_hi, const int64_t *off, const uint32_t *rows, int V, int tsw,
-                                   const int *pos_of, uint32_t *send) {
+                                   int pack, const int *pos_of, uint32_t *send) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= B * MS) return;
     const int64_t o = t / MS;
@@ -386,8 +386,16 @@ __global__ void gather_send_kernel(const int *stops, const int *n_arr, const int
     int i_lo, i_hi;
     owned_range(s, n, src_row, own_lo, own_hi, i_lo, i_hi);
     const int64_t rr = pos_of[r - seg_lo];   // slot position of the source in the segment's tiles
-    const uint32_t *R = rows + (size_t)(rr / tsw) * V * tsw + (rr % tsw);
     uint32_t *dst = send + off[o] + (int64_t)(i - i_lo) * n;
+    if (pack == 2) {   // packed u16 rows: widen, INF 0x7fff -> INT32_MAX
+        const uint16_t *R = reinterpret_cast<const uint16_t *>(rows) + (size_t)(rr / tsw) * V * tsw + (rr % tsw);
+        for (int j = 0; j < n; ++j) {
+            const uint32_t x = R[(size_t)s[j] * tsw];
+            dst[j] = x == 0x7fffu ? 0x7fffffffu : x;
+        }
+        return;
+    }
+    const uint32_t *R = rows + (size_t)(rr / tsw) * V * tsw + (rr % tsw);
     for (int j = 0; j < n; ++j) dst[j] = R[(size_t)s[j] * tsw];
 }
 
@@ -835,18 +843,30 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     float bf_ms = 0.f, pred_ms = 0.f;
     if (o.pred_out && (!is_device_ptr(o.pred_out) || o.pred_rows < P->src_hi - P->src_lo))
         return fail(WR_EINVAL, "wr_orders_local: pred_out must be device memory with >= src_hi-src_lo rows");
-    if (nsrc > 0) {
+    // Packed u16 rows (OpU16) when every distance provably fits: int32
+    // weights in [1, 0x3fff] (w > 0 also rules out flat vertices). A tile
+    // whose distances approach 0x7fff raises the overflow flag and the whole
+    // phase is redone with 32-bit rows.
+    static const bool no_pack = getenv("WR_NO_PACK") != nullptr;
+    int pack = (g->wtype == WR_I32 && !g->has_negative && !g->has_zero && g->max_abs_w <= 0x3fff && !no_pack &&
+                !(o.flags & WR_ROUTE_ROWS32))
+                   ? 2
+                   : 1;
+    BfTileStats hs{};
+    auto run_phase = [&](int pk) {
+        if (nsrc <= 0) return;
         wr_graph_info_t gi;
         wr_graph_info(g, &gi);
         const int64_t fixed = gi.device_bytes + (128 << 20);
         int nsm = 0;
         WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
         const int spl = choose_spl(nsrc, nsm);
-        const int tsw = 32 * spl;
+        const int tsw = 32 * spl * pk;            // sources per tile
+        const int64_t src_bytes = 4LL * V / pk;   // row bytes per source
         const double h_pre = hms();
-        const int64_t budget = budget_bytes(o.hbm_budget, fixed, (nsrc + tsw - 1) / tsw * tsw * 4LL * V);
+        const int64_t budget = budget_bytes(o.hbm_budget, fixed, (nsrc + tsw - 1) / tsw * tsw * src_bytes);
         const double h_budget = hms();
-        const int64_t sb = sources_per_segment(budget, fixed, 4LL * V, nsrc, tsw);
+        const int64_t sb = sources_per_segment(budget, fixed, src_bytes, nsrc, tsw);
         const int64_t max_tiles = sb / tsw;
         static const bool trace = getenv("WR_TRACE") != nullptr;
         cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -856,7 +876,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventRecord(t0, st));
         }
         const auto hclock0 = std::chrono::steady_clock::now();
-        DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
+        DBuf<uint32_t> rows((size_t)max_tiles * V * 32 * spl);
         DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
         DBuf<int> flat(o.pred_out ? max_tiles : 0);
         int max_rounds = g->has_negative ? std::max(1, V - 1) : V;
@@ -870,6 +890,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             const int ntiles = (int)((hi - lo + tsw - 1) / tsw);
             make_tiles_ordered(g, P->sources.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
+            run.pack = pk;
+            run.ovf_thr = pk == 2 ? 0x7fffu - (uint32_t)g->max_abs_w : 0u;
             WR_CUDA(cudaEventRecord(b0, st));
             const double host_to_b0 =
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hclock0).count();
@@ -884,6 +906,9 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
                 std::vector<int> todo;
                 for (int t = 0; t < ntiles; ++t)
                     if (hflat[t] || g->has_negative) todo.push_back(t);
+                // packed rows: w > 0 admits no flat vertex unless a distance
+                // was clipped, and then the overflow flag forces the redo
+                if (pk == 2) todo.clear();
                 bf_resolve_flat(g, run, todo, lo - P->src_lo, o.pred_out, st);
             }
             WR_CUDA(cudaEventRecord(b2, st));
@@ -896,7 +921,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             if (P->B > 0) {
                 gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, st>>>(
                     P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, lo, hi, off_r,
-                    rows.p, V, tsw, pos_of.p, (uint32_t *)send);
+                    rows.p, V, tsw, pk, pos_of.p, (uint32_t *)send);
                 count_launch();
                 WR_LAUNCH_CHECK();
             }
@@ -920,10 +945,18 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         cudaEventDestroy(b0);
         cudaEventDestroy(b1);
         cudaEventDestroy(b2);
+    };
+    run_phase(pack);
+    WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    if (pack == 2 && hs.overflow) {   // a distance may not fit in 15 bits: redo with 32-bit rows
+        const BfTileStats z{0ull, 0, -1, 0ull};
+        WR_CUDA(cudaMemcpyAsync(d_stats.p, &z, sizeof(z), cudaMemcpyHostToDevice, st));
+        pack = 1;
+        run_phase(1);
     }
     const double h_loop = hms();
     WR_CUDA(cudaEventRecord(e1, st));
-    BfTileStats hs;
     WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
     static const bool trace_l = getenv("WR_TRACE") != nullptr;

@@ -309,6 +309,70 @@ def test_route_orders_budget_and_chunk_invariance():
     assert a.tobytes() == b.tobytes()
 
 
+def _orders_with_pred(G, orders, S, V, flags=0):
+    pred = torch.full((S, V), -7, dtype=torch.int32, device="cuda")
+    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, pred_out=pred, flags=flags)
+    return res, pred.cpu().numpy(), st
+
+
+def test_packed_rows_equal_rows32():
+    """Packed 16-bit working rows (int32 weights in [1, 0x3fff]) give the same
+    routes, costs and pred rows as 32-bit rows (WR_ROUTE_ROWS32)."""
+    g, orders, _ = gen.config(3, B=2048)
+    assert int(np.min(g.w)) >= 1 and int(np.max(g.w)) <= 0x3fff   # the graph qualifies for packing
+    G = wr.Graph.from_gen(g)
+    S = np.unique(orders.order_nodes).size
+    a, pa, _ = _orders_with_pred(G, orders, S, g.V)
+    b, pb, _ = _orders_with_pred(G, orders, S, g.V, flags=wr.WR_ROUTE_ROWS32)
+    assert a.tobytes() == b.tobytes()
+    assert np.array_equal(pa, pb)
+    compare_orders(g, orders, m=1, G=G, results=a)
+
+
+def _long_grid(n=24, w=0x3000):
+    """n x n bidirectional grid with weights near the packed limit: distances
+    reach ~2n*w >> 0x7fff, so a packed sweep must detect the overflow and
+    redo the phase with 32-bit rows."""
+    src, dst = [], []
+    for i in range(n):
+        for j in range(n):
+            v = i * n + j
+            if j + 1 < n:
+                src += [v, v + 1]
+                dst += [v + 1, v]
+            if i + 1 < n:
+                src += [v, v + n]
+                dst += [v + n, v]
+    rng = np.random.default_rng(7)
+    ww = (w + rng.integers(0, 64, len(src))).astype(np.int32)
+    xy = np.array([(v % n, v // n) for v in range(n * n)], np.int32)
+    return G(n * n, src, dst, ww, xy=xy)
+
+
+def test_packed_overflow_falls_back_exact():
+    g = _long_grid()
+    rng = np.random.default_rng(3)
+    B = 64
+    nodes = rng.integers(0, g.V, B * 5).astype(np.int32)
+    ptr = np.arange(0, B * 5 + 1, 5, dtype=np.int64)
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, B
+    G = wr.Graph(g.V, g.src, g.dst, g.w)
+    S = np.unique(nodes).size
+    res, P, _ = _orders_with_pred(G, orders, S, g.V)
+    exp = oracle.route_orders(g, orders, m=1)
+    assert wr.decode_cost(res, G.wtype).tobytes() == exp["cost"].tobytes()
+    assert np.array_equal(res["seq"], exp["seq"])
+    stops = np.unique(nodes)
+    rows = oracle.bf_many(g, stops[::9])
+    assert rows.max() > 0x7fff                       # the case really overflows 15 bits
+    for k, i in enumerate(range(0, S, 9)):
+        assert np.array_equal(P[i], oracle.pred(g, int(stops[i]), rows[k]))
+
+
 # ------------------------------------------------------------------ a9
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_phases_equal_single(world):
@@ -338,8 +402,18 @@ def test_config5_full_size_sampled(wtype):
     orders and sources are recomputed by the oracle one by one."""
     g, orders, _ = gen.config(5, wtype=wtype)
     G = wr.Graph.from_gen(g)
-    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes)
-    assert st.sources == np.unique(orders.order_nodes).size
+    stops_all = np.unique(orders.order_nodes)
+    pred_dev = torch.empty((stops_all.size, g.V), dtype=torch.int32, device="cuda")
+    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, pred_out=pred_dev)
+    assert st.sources == stops_all.size
+    # pred rows of the bench's launch (packed rows for int32): sampled sources
+    rng0 = np.random.default_rng(56)
+    pick = np.sort(rng0.choice(stops_all.size, 6, replace=False))
+    prow = pred_dev[torch.from_numpy(pick).cuda()].cpu().numpy()
+    del pred_dev
+    ref_rows = oracle.bf_many(g, stops_all[pick])
+    for k, i in enumerate(pick):
+        assert np.array_equal(prow[k], oracle.pred(g, int(stops_all[i]), ref_rows[k]))
     assert (res["status"] == 0).all()
     rng = np.random.default_rng(55)
     sample = np.sort(rng.choice(orders.B, 12, replace=False))
