@@ -217,6 +217,7 @@ def main():
     launches = [0]
     bf_ms = [0.0]
     relax = [0]
+    row_bits = [32]
 
     def step():
         if world == 1:
@@ -224,6 +225,7 @@ def main():
             launches[0] += st.kernel_launches
             bf_ms[0] += st.bf_ms
             relax[0] += st.relaxations
+            row_bits[0] = st.row_bits
             return
         p = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, pred_out=pred_buf)
         s1 = p.local(send)
@@ -232,6 +234,7 @@ def main():
         launches[0] += s1.kernel_launches + s2.kernel_launches
         bf_ms[0] += s1.bf_ms
         relax[0] += s1.relaxations
+        row_bits[0] = s1.row_bits
         p.close()
 
     def barrier():
@@ -310,9 +313,11 @@ def main():
     useful = S * E                                    # graph500 convention: each arc once per source
     # roofline of the dominant kernel (the relaxation sweep): algorithmic bytes
     # per launch = compulsory traffic: write each
-    # source's V distances once (4V per source) + read the graph (in-arcs
-    # (u, w) 8E, out-arcs 4E, offsets 8V) once per 128-source tile.
-    alg_bytes = S * (4 * g.V) + (S / 128.0) * (12 * E + 8 * g.V)
+    # source's V distances once (4V per source, 2V with packed 16-bit rows)
+    # + read the graph (in-arcs (u, w) 8E, out-arcs 4E, offsets 8V) once per
+    # tile (128 sources, 256 packed).
+    rb = row_bits[0] or 32
+    alg_bytes = S * (g.V * rb // 8) + (S / (128.0 * 32 / rb)) * (12 * E + 8 * g.V)
     bf_s = bf_step_ms / 1e3
     achieved = alg_bytes / bf_s / 1e9 if bf_s > 0 else None
     traffic = None
@@ -330,6 +335,8 @@ def main():
         "vs_baseline": None, "dtype": a.wtype, "data": "synthetic",
         "config": {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]", "orders": B,
                    "sources": S, "V": g.V, "E": E, "m": a.m, "pred": not a.no_pred,
+                   "bf_rows": ("packed u16x2, exact (15-bit bound checked per tile, else a 32-bit redo); "
+                               "outputs int32") if rb == 16 else "32-bit",
                    "l2": "working set (dist rows 4*V*S = %.1f GB) >> 126 MB L2; no flush needed" % (4 * g.V * S / 1e9)},
         "edges_relaxed_per_sec": {"useful": useful / (ms / 1e3), "useful_bf_only": useful / bf_s if bf_s else None,
                                   "performed_bf_only": (relax[0] / a.steps) / bf_s if bf_s else None,

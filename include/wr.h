@@ -212,6 +212,9 @@ typedef struct {
     float bf_ms;              /* device time of the relaxation sweeps alone  */
     float pred_ms;            /* device time of the canonical-pred pass      */
     int64_t visits;           /* BF candidate visits                         */
+    int32_t row_bits;         /* BF working-row element width: 16 (packed,
+                                 exact) or 32                                */
+    int32_t reserved;
 } wr_route_stats;
 
 /* a7 Segmented route of one stop set (Theorem 3.1, P324-337 §3).

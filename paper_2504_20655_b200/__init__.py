@@ -74,7 +74,8 @@ class RouteStats(C.Structure):
     _fields_ = [("orders", C.c_int64), ("sources", C.c_int64), ("permutations", C.c_int64),
                 ("stitch_candidates", C.c_int64), ("segments", C.c_int32), ("rounds_max", C.c_int32),
                 ("relaxations", C.c_int64), ("ms", C.c_float), ("kernel_launches", C.c_int64),
-                ("bf_ms", C.c_float), ("pred_ms", C.c_float), ("visits", C.c_int64)]
+                ("bf_ms", C.c_float), ("pred_ms", C.c_float), ("visits", C.c_int64),
+                ("row_bits", C.c_int32), ("reserved", C.c_int32)]
 
 
 class PlanInfo(C.Structure):

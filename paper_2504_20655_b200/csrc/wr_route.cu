@@ -976,6 +976,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         stats->kernel_launches = g_launches - l0;
         stats->bf_ms = bf_ms;
         stats->pred_ms = pred_ms;
+        stats->row_bits = pack == 2 ? 16 : 32;
     }
     return WR_OK;
 }
@@ -1132,6 +1133,7 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
         stats->kernel_launches = g_launches - l0;
         stats->bf_ms = s1.bf_ms;
         stats->pred_ms = s1.pred_ms;
+        stats->row_bits = s1.row_bits;
     }
     return WR_OK;
 }

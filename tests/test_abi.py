@@ -44,6 +44,7 @@ def test_result_layout_matches_header():
     # int32 n, status, uint32 cost_bits, int32 m_used, int64 rank, int32 seq[16]
     assert wr.RESULT_DTYPE.itemsize == 88
     assert ctypes.sizeof(wr.GraphDesc) == 88 and ctypes.sizeof(wr.RouteOpts) == 56
+    assert ctypes.sizeof(wr.RouteStats) == 88
 
 
 def test_shard_range_partitions():
