@@ -29,6 +29,7 @@
 #include <cstring>
 #include <memory>
 #include <type_traits>
+#include <string>
 #include <vector>
 
 #include "wr_internal.cuh"
@@ -315,7 +316,8 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 #pragma unroll
         for (int j = 0; j < AQ; ++j) {
             const bool take = arc[j].x >= 0 && (!DELTA || pchg.test(arc[j].x));
-            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x, (int)Op::prep_w((uint32_t)arc[j].y));
+            // queued: the tail row's word offset (u * TSW < 2^31) and the prepared weight
+            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x * TSW, (int)Op::prep_w((uint32_t)arc[j].y));
             c += take ? 1 : 0;
         }
     }
@@ -375,7 +377,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
                 for (int k = 0; k < VB; ++k)
 #pragma unroll
                     for (int j = 0; j < TPS; ++j)
-                        if (t + j < cc[k]) x[k][j] = vload<SPL>(Rl + (size_t)tk[k][j].x * TSW);
+                        if (t + j < cc[k]) x[k][j] = vload<SPL>(Rl + (uint32_t)tk[k][j].x);
 #pragma unroll
                 for (int k = 0; k < VB; ++k)
 #pragma unroll
@@ -392,7 +394,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
                 } else {
                     for (int t = 0; t < cc[k]; ++t) {
                         const int2 tq = q[iv[k] * QC + t];
-                        vrelax<Op, SPL>(d[k], vload<SPL>(Rl + (size_t)tq.x * TSW), (uint32_t)tq.y);
+                        vrelax<Op, SPL>(d[k], vload<SPL>(Rl + (uint32_t)tq.x), (uint32_t)tq.y);
                     }
                 }
             }
@@ -459,6 +461,9 @@ __host__ __device__ constexpr FrontierSmem frontier_smem(int NW, int nwarps, int
                             (size_t)nwarps * 32 * QC * 2};
 }
 
+// Diagnostics (WR_TILE_TRACE): per tile {start ns, end ns, rounds, SM id}.
+__device__ long long *g_tile_trace = nullptr;
+
 template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
@@ -489,6 +494,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
+        long long t_start = 0;
+        if (g_tile_trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         uint32_t *R = rows + (size_t)tile * V * TSW;
         uint32_t *cur = smem + L.cur, *nxt = smem + L.nxt;
 
@@ -617,6 +624,17 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TS);
         if (lane == 0 && visits) atomicAdd(&stats->visits, visits);
         if (threadIdx.x == 0) atomicMax(&stats->rounds_max, rounds);
+        if (g_tile_trace && threadIdx.x == 0) {
+            long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            long long *e = g_tile_trace + 4 * (size_t)tile;
+            e[0] = t_start;
+            e[1] = t_end;
+            e[2] = rounds;
+            e[3] = smid;
+        }
         __syncthreads();
     }
 }
@@ -660,7 +678,7 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
     // (11) 84.4, 640 static (9) 94.4, 896 static (10) 104; fp32: 768 static
     // 232 ms, 640 static 240, 768 lists 254 (the list order lets more
     // suboptimal values propagate: 4.4 vs 3.6 x S*E relaxations).
-    static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 14);
+    static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 11);
     bool ok = false;
     switch (cfg) {
         case 4: ok = launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st); break;
@@ -668,6 +686,7 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
         case 10: ok = launch_shape<Op, DENSE, 896, 1, SPL>(g, run, d_stats, st); break;
         case 11: ok = launch_shape<Op, DENSE, 640, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
         case 14: ok = launch_shape<Op, DENSE, 768, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
+        case 15: ok = launch_shape<Op, DENSE, 704, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
         default: break;
     }
     if (!ok && !launch_shape<Op, DENSE, 640, 1, SPL>(g, run, d_stats, st) &&
@@ -802,10 +821,43 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
         WR_CUDA(cudaMemcpyAsync(order.p, ho.data(), 4 * run.ntiles, cudaMemcpyHostToDevice, st));
         run.tile_order = order.p;
     }
+    static const char *trace_path = getenv("WR_TILE_TRACE");
+    DBuf<long long> ttrace;
+    if (trace_path) {
+        ttrace.alloc((size_t)4 * run.ntiles);
+        WR_CUDA(cudaMemsetAsync(ttrace.p, 0, ttrace.bytes(), st));
+        WR_CUDA(cudaMemcpyToSymbolAsync(g_tile_trace, &ttrace.p, sizeof(void *), 0, cudaMemcpyHostToDevice, st));
+    }
     if (run.pack == 2) launch_sweep<OpU16>(g, run, d_stats, st);
     else if (g->wtype == WR_F32) launch_sweep<OpF32>(g, run, d_stats, st);
     else if (g->has_negative) launch_sweep<OpI32N>(g, run, d_stats, st);
     else launch_sweep<OpU32>(g, run, d_stats, st);
+    if (trace_path) {   // append one line per tile: tile key-order-pos start end rounds sm
+        std::vector<long long> h((size_t)4 * run.ntiles);
+        WR_CUDA(cudaMemcpyAsync(h.data(), ttrace.p, ttrace.bytes(), cudaMemcpyDeviceToHost, st));
+        std::vector<int> ho(run.ntiles);
+        if (run.tile_order)
+            WR_CUDA(cudaMemcpyAsync(ho.data(), run.tile_order, 4 * run.ntiles, cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        void *null = nullptr;
+        WR_CUDA(cudaMemcpyToSymbol(g_tile_trace, &null, sizeof(void *)));
+        std::vector<int> pos(run.ntiles);
+        for (int i = 0; i < run.ntiles; ++i) pos[run.tile_order ? ho[i] : i] = i;
+        if (FILE *f = fopen(trace_path, "a")) {
+            for (int t = 0; t < run.ntiles; ++t)
+                fprintf(f, "%d %d %lld %lld %lld %lld\n", t, pos[t], h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
+            fclose(f);
+        }
+        std::vector<int> ts((size_t)run.ntiles * run.tsw());
+        WR_CUDA(cudaMemcpy(ts.data(), run.tile_src, 4 * ts.size(), cudaMemcpyDeviceToHost));
+        if (FILE *f = fopen((std::string(trace_path) + ".src").c_str(), "a")) {
+            for (int t = 0; t < run.ntiles; ++t) {
+                for (int k = 0; k < run.tsw(); ++k) fprintf(f, "%d ", ts[(size_t)t * run.tsw() + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
 }
 
 // Sources per lane for S sources; WR_BF_SPL forces a width.
@@ -1400,7 +1452,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     const int64_t tiles_all = (std::max(S, 1) + tsw - 1) / tsw;
     const int64_t budget = budget_bytes(o.hbm_budget, fixed, tiles_all * tsw * per_src);
     const int64_t sb = sources_per_segment(budget, fixed, per_src, std::max(S, 1), tsw);
-    const int64_t max_tiles = sb / tsw;
+    const int64_t max_tiles = tiles_to_allocate(sb, tsw, budget - fixed - sb * per_src, 4LL * V * tsw);
 
     DBuf<uint32_t> rows((size_t)max_tiles * V * tsw);
     DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
@@ -1417,8 +1469,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     int64_t total_tiles = 0;
     for (int64_t lo = 0; lo < S; lo += sb) {
         const int64_t hi = std::min<int64_t>(S, lo + sb);
-        const int ntiles = (int)((hi - lo + tsw - 1) / tsw);
-        make_tiles_ordered(g, d_src.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
+        const int ntiles = make_tiles_ordered(g, d_src.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
         BfRun run{tile_src.p, ntiles, rows.p, variant, max_rounds, spl, slot_row.p};
         bf_run(g, run, d_stats.p, st);
         BfTileStats hs;

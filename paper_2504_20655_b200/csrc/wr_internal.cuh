@@ -146,6 +146,7 @@ struct wr_graph {
     wr::DBuf<int> xy;       // [V*2] or empty
     wr::DBuf<int> z;        // [V] rack level or empty
     mutable wr::DBuf<int> hop_c;  // [V] BFS hops from a central vertex (tile cost key), built on first use
+    mutable std::vector<int> h_xy, h_z;  // host copies of xy / z for tile building, on first use
     int bbox[6] = {0, 0, 0, 0, 0, 0};   // xmin, xmax, ymin, ymax, zmin, zmax
     wr::DevGraph view() const {
         return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, in_arc.p, out_ptr.p, out_dst.p};
@@ -203,11 +204,16 @@ void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int>
 
 // Builds tile_src for sources [lo, hi) of a device source list (tsw slots/tile).
 void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_tile_src, cudaStream_t st);
-// Same, with the sources ordered along a Morton curve of the graph's
-// coordinates (when present): slot_row[slot] = source offset in [0, hi-lo)
-// (-1 = empty slot), pos_of[offset] = slot position (wr_tiles.cu).
-void make_tiles_ordered(const wr_graph *g, const int *d_sources, int64_t lo, int64_t hi, int tsw, int *tile_src,
-                        int *slot_row, int *pos_of, cudaStream_t st);
+// Same, with spatially compact tiles (recursive coordinate bisection of the
+// graph's coordinates when present) and a whole number of waves of tiles
+// (<= max_tiles) with the sources spread evenly: slot_row[slot] = source
+// offset in [0, hi-lo) (-1 = empty slot), pos_of[offset] = slot position.
+// Returns the number of tiles (wr_tiles.cu).
+int make_tiles_ordered(const wr_graph *g, const int *d_sources, int64_t lo, int64_t hi, int tsw, int64_t max_tiles,
+                       int *tile_src, int *slot_row, int *pos_of, cudaStream_t st);
+// Tiles to allocate for segments of sb sources: sb/tsw, plus up to one wave
+// of extra (partly filled) tiles if extra_bytes allow (tile_bytes each).
+int64_t tiles_to_allocate(int64_t sb, int tsw, int64_t extra_bytes, int64_t tile_bytes);
 
 // ------------------------------------------------------------- routing --
 struct RouteProblem {       // one exhaustive search (an order or a segment)

@@ -867,7 +867,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         const int64_t budget = budget_bytes(o.hbm_budget, fixed, (nsrc + tsw - 1) / tsw * tsw * src_bytes);
         const double h_budget = hms();
         const int64_t sb = sources_per_segment(budget, fixed, src_bytes, nsrc, tsw);
-        const int64_t max_tiles = sb / tsw;
+        const int64_t tile_bytes = 4LL * V * 32 * spl;
+        const int64_t max_tiles = tiles_to_allocate(sb, tsw, budget - fixed - sb * src_bytes, tile_bytes);
         static const bool trace = getenv("WR_TRACE") != nullptr;
         cudaEvent_t t0 = nullptr, t1 = nullptr;
         if (trace) {
@@ -887,8 +888,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         WR_CUDA(cudaEventCreate(&b2));
         for (int64_t lo = P->src_lo; lo < P->src_hi; lo += sb) {
             const int64_t hi = std::min<int64_t>(P->src_hi, lo + sb);
-            const int ntiles = (int)((hi - lo + tsw - 1) / tsw);
-            make_tiles_ordered(g, P->sources.p, lo, hi, tsw, tile_src.p, slot_row.p, pos_of.p, st);
+            const int ntiles =
+                make_tiles_ordered(g, P->sources.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
             run.pack = pk;
             run.ovf_thr = pk == 2 ? 0x7fffu - (uint32_t)g->max_abs_w : 0u;
