@@ -1005,14 +1005,31 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
     // = NEED (-1) while a slot still looks for its pred, SKIP (-2) for slots
     // that need none (empty, the source itself, unreachable). Slot j*P + h
     // is half h of the lane's word j.
-    constexpr int NEED = -1, SKIP = -2;
-    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, int (&best)[NS]) {
+    // need: bit k set while slot k still looks for its pred (clear for
+    // empty slots, the source itself and unreachable vertices); best[k] =
+    // the pred found (-1 = none). hit bits of one gathered in-neighbour row:
+    // the steep-tight test of all the lane's slots; packed rows test both
+    // halves of a word with one add and one compare.
+    auto test = [&](const Vec<SPL> &x, uint32_t w, int u, const Vec<SPL> &d, int (&best)[NS], uint32_t &need) {
+        uint32_t hit = 0;
+        if constexpr (P == 2) {
+            const uint32_t w2 = w | (w << 16);   // w in [1, 0x3fff]: no half wraps
 #pragma unroll
-        for (int j = 0; j < SPL; ++j)
+            for (int j = 0; j < SPL; ++j) {
+                const uint32_t t2 = __vcmpeq2(__vadd2(x.x[j], w2), d.x[j]);
+                hit |= ((t2 & 1u) | ((t2 >> 15) & 2u)) << (2 * j);
+            }
+        } else {
 #pragma unroll
-            for (int h = 0; h < P; ++h)
-                if (best[j * P + h] == NEED && Op::steep_tight(Op::half(x.x[j], h), w, Op::half(d.x[j], h)))
-                    best[j * P + h] = u;
+            for (int j = 0; j < SPL; ++j) hit |= (Op::steep_tight(x.x[j], w, d.x[j]) ? 1u : 0u) << j;
+        }
+        hit &= need;
+        if (hit) {
+            need &= ~hit;
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if ((hit >> k) & 1u) best[k] = u;
+        }
     };
     // two vertices per step (lanes 0-15 / 16-31 hold their in-arcs), PA
     // in-arcs of each per step; stop when no slot still needs a pred
@@ -1027,18 +1044,17 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
         Vec<SPL> d1 = d0;
         if (two) d1 = vload<SPL>(Rl + (size_t)v1 * TSW);
         int best0[NS], best1[NS];
-        bool m0 = false, m1 = false;
+        uint32_t need0 = 0, need1 = 0;
 #pragma unroll
         for (int j = 0; j < SPL; ++j)
 #pragma unroll
             for (int h = 0; h < P; ++h) {
                 const int k = j * P + h;
-                best0[k] = (src[k] >= 0 && v0 != src[k] && Op::finite(Op::half(d0.x[j], h))) ? NEED : SKIP;
-                best1[k] = (two && src[k] >= 0 && v1 != src[k] && Op::finite(Op::half(d1.x[j], h))) ? NEED : SKIP;
-                m0 |= best0[k] == NEED;
-                m1 |= best1[k] == NEED;
+                best0[k] = best1[k] = -1;
+                need0 |= (src[k] >= 0 && v0 != src[k] && Op::finite(Op::half(d0.x[j], h)) ? 1u : 0u) << k;
+                need1 |= (two && src[k] >= 0 && v1 != src[k] && Op::finite(Op::half(d1.x[j], h)) ? 1u : 0u) << k;
             }
-        const bool need0 = __any_sync(FULL, m0), need1 = __any_sync(FULL, m1);
+        const bool any0 = __any_sync(FULL, need0 != 0), any1 = __any_sync(FULL, need1 != 0);
         if (n0 <= 16 && n1 <= 16) {
             const int sub = lane & 15;
             const int base = lane < 16 ? a00 : a10;
@@ -1051,7 +1067,7 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
             }
             // per-vertex early exit: a vertex whose slots all have their
             // pred stops gathering (its arc count drops to k)
-            int e0 = need0 ? n0 : 0, e1 = need1 ? n1 : 0;
+            int e0 = any0 ? n0 : 0, e1 = any1 ? n1 : 0;
             for (int k = 0; k < max(e0, e1); k += PA) {
                 int ua[2][PA];
                 uint32_t wa[2][PA];
@@ -1065,25 +1081,19 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
                 }
 #pragma unroll
                 for (int a = 0; a < PA; ++a) {
-                    if (k + a < e0) x[0][a] = vload<SPL>(Rl + (size_t)ua[0][a] * TSW);
-                    if (k + a < e1) x[1][a] = vload<SPL>(Rl + (size_t)ua[1][a] * TSW);
+                    if (k + a < e0) x[0][a] = vload<SPL>(Rl + (uint32_t)(ua[0][a] * TSW));
+                    if (k + a < e1) x[1][a] = vload<SPL>(Rl + (uint32_t)(ua[1][a] * TSW));
                 }
 #pragma unroll
                 for (int a = 0; a < PA; ++a) {
-                    if (k + a < e0) test(x[0][a], wa[0][a], ua[0][a], d0, best0);
-                    if (k + a < e1) test(x[1][a], wa[1][a], ua[1][a], d1, best1);
+                    if (k + a < e0) test(x[0][a], wa[0][a], ua[0][a], d0, best0, need0);
+                    if (k + a < e1) test(x[1][a], wa[1][a], ua[1][a], d1, best1, need1);
                 }
-                m0 = m1 = false;
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    m0 |= best0[j] == NEED;
-                    m1 |= best1[j] == NEED;
-                }
-                if (!__any_sync(FULL, m0)) e0 = min(e0, k + PA);
-                if (!__any_sync(FULL, m1)) e1 = min(e1, k + PA);
+                if (!__any_sync(FULL, need0 != 0)) e0 = min(e0, k + PA);
+                if (!__any_sync(FULL, need1 != 0)) e1 = min(e1, k + PA);
             }
         } else {
-            auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[NS]) {
+            auto slow = [&](int lo, int hi, const Vec<SPL> &d, int (&best)[NS], uint32_t &need) {
                 for (int base = lo; base < hi; base += 32) {
                     const int cnt = min(32, hi - base);
                     int my_u = 0;
@@ -1095,18 +1105,18 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
                     for (int k = 0; k < cnt; ++k) {
                         const int u = __shfl_sync(FULL, my_u, k);
                         const uint32_t w = __shfl_sync(FULL, my_w, k);
-                        test(vload<SPL>(Rl + (size_t)u * TSW), w, u, d, best);
+                        test(vload<SPL>(Rl + (uint32_t)(u * TSW)), w, u, d, best, need);
                     }
                 }
             };
-            if (need0) slow(a00, a01, d0, best0);
-            if (two && need1) slow(a10, a11, d1, best1);
+            if (any0) slow(a00, a01, d0, best0, need0);
+            if (two && any1) slow(a10, a11, d1, best1, need1);
         }
+        flat |= (need0 | need1) != 0;   // reachable, no steep tight in-arc: flat
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            flat |= (best0[j] == NEED) | (best1[j] == NEED);   // reachable, no steep tight in-arc: flat
-            sp[warp][jv][lane * NS + j] = max(best0[j], -1);
-            if (two) sp[warp][jv1][lane * NS + j] = max(best1[j], -1);
+            sp[warp][jv][lane * NS + j] = best0[j];
+            if (two) sp[warp][jv1][lane * NS + j] = best1[j];
         }
     }
     __syncwarp();
