@@ -182,11 +182,12 @@ static bool rcb_perm(const wr_graph *g, const int *d_sources, int64_t lo, int n,
     return true;
 }
 
-// Tile count: a whole number of waves over the SMs (one tile per SM at a
-// time), as few waves as ceil(n / tsw) full tiles need, the sources spread
-// evenly (fill per tile). C5 packed: 331 full tiles are 2.24 waves - the
-// third wave of 35 tiles ran alone for ~20 ms; 444 tiles of 191 sources are
-// exactly 3 waves. Also keeps every SM busy when a rank has few sources.
+// Tile count: by default ceil(n / tsw) full tiles. WR_TILE_BALANCE=1 spreads
+// the sources over a whole number of waves instead (one tile per SM at a
+// time; fill sources per tile). Measured on C5 packed: the sweep does not
+// gain (a tile's time is latency-bound, nearly independent of its fill: 331
+// full tiles 61 ms, 444 tiles of 191 sources 62 ms) and the pred pass, whose
+// cost is per (tile, vertex) job, loses 20 % (32 -> 39.7 ms).
 int balanced_tiles(int64_t n, int tsw, int64_t max_tiles, int &fill) {
     static int nsm = 0;
     if (!nsm) {
@@ -194,7 +195,7 @@ int balanced_tiles(int64_t n, int tsw, int64_t max_tiles, int &fill) {
         WR_CUDA(cudaGetDevice(&dev));
         WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
-    static const bool off = getenv("WR_NO_TILE_BALANCE") != nullptr;
+    static const bool off = getenv("WR_TILE_BALANCE") == nullptr;
     const int64_t base = (n + tsw - 1) / tsw;
     int64_t nt = base;
     if (!off) {
