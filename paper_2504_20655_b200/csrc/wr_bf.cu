@@ -1080,14 +1080,14 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
                     wa[1][a] = __shfl_sync(FULL, my_w, (16 + k + a) & 31);
                 }
 #pragma unroll
-                for (int a = 0; a < PA; ++a) {
-                    if (k + a < e0) x[0][a] = vload<SPL>(Rl + (uint32_t)(ua[0][a] * TSW));
-                    if (k + a < e1) x[1][a] = vload<SPL>(Rl + (uint32_t)(ua[1][a] * TSW));
+                for (int a = 0; a < PA; ++a) {   // lanes whose slots are all done load nothing
+                    if (k + a < e0 && need0) x[0][a] = vload<SPL>(Rl + (uint32_t)(ua[0][a] * TSW));
+                    if (k + a < e1 && need1) x[1][a] = vload<SPL>(Rl + (uint32_t)(ua[1][a] * TSW));
                 }
 #pragma unroll
                 for (int a = 0; a < PA; ++a) {
-                    if (k + a < e0) test(x[0][a], wa[0][a], ua[0][a], d0, best0, need0);
-                    if (k + a < e1) test(x[1][a], wa[1][a], ua[1][a], d1, best1, need1);
+                    if (k + a < e0 && need0) test(x[0][a], wa[0][a], ua[0][a], d0, best0, need0);
+                    if (k + a < e1 && need1) test(x[1][a], wa[1][a], ua[1][a], d1, best1, need1);
                 }
                 if (!__any_sync(FULL, need0 != 0)) e0 = min(e0, k + PA);
                 if (!__any_sync(FULL, need1 != 0)) e1 = min(e1, k + PA);
