@@ -461,6 +461,15 @@ __host__ __device__ constexpr FrontierSmem frontier_smem(int NW, int nwarps, int
                             (size_t)nwarps * 32 * QC * 2};
 }
 
+struct PredShape {
+    static constexpr int PV = 8;     // vertices per warp job (full 32-B output sectors)
+};
+template <class Op, int SPL, int PA>
+__device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restrict__ tile_src,
+                                         const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
+                                         int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
+                                         int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane);
+
 // Diagnostics (WR_TILE_TRACE): per tile {start ns, end ns, rounds, SM id}.
 __device__ long long *g_tile_trace = nullptr;
 
@@ -469,7 +478,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
                                                                BfTileStats *stats, uint32_t thr2,
-                                                               const int *__restrict__ tile_order) {
+                                                               const int *__restrict__ tile_order, PredFuse fuse,
+                                                               const int *__restrict__ slot_row) {
     constexpr int TSW = 32 * SPL;              // 32-bit words per row
     constexpr int TS = TSW * Op::PACK;         // sources per tile
     constexpr int NWARPS = NT / 32;
@@ -635,7 +645,42 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             e[2] = rounds;
             e[3] = smid;
         }
+        if (fuse.pred_out) {   // publish the finished tile: rows visible GPU-wide, then its list entry
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int k = atomicAdd(&fuse.counters[0], 1);
+                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(fuse.done_list + k), "r"(tile) : "memory");
+            }
+        }
         __syncthreads();
+    }
+    if (fuse.pred_out && !DENSE) {
+        // no tile left to claim: take pred jobs (tile in completion order k,
+        // 8-vertex chunk) - a job waits only for a tile that a running CTA
+        // is still relaxing; the shared memory is free for the staging rows
+        constexpr int PV = PredShape::PV;
+        int32_t(*spw)[TS + 1] = reinterpret_cast<int32_t(*)[TS + 1]>(smem) + warp * PV;
+        const int chunks = (V + PV - 1) / PV;
+        const long long njobs = (long long)ntiles * chunks;
+        for (;;) {
+            long long j = 0;
+            if (lane == 0) j = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(fuse.counters + 2), 1ull);
+            j = __shfl_sync(FULL, j, 0);
+            if (j >= njobs) break;
+            const int k = (int)(j / chunks);
+            int t = -1;
+            if (lane == 0) {
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(t) : "l"(fuse.done_list + k) : "memory");
+                    if (t >= 0) break;
+                    __nanosleep(256);
+                }
+            }
+            t = __shfl_sync(FULL, t, 0);
+            pred_job<Op, SPL, 1>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
+                                 (int)(j % chunks) * PV, spw, lane);
+        }
     }
 }
 
@@ -645,7 +690,9 @@ template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool L
 static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
     auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, QC, VB, TPS, LIST && !DENSE>;
     const int NW = (g->V + 31) / 32;
-    const size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
+    size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
+    if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
+        smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV * (32 * SPL * Op::PACK + 1) * sizeof(int32_t));
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem > (size_t)max_optin) return false;
@@ -658,7 +705,7 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     DBuf<int> counter(1);
     WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
     kern<<<grid, NT, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p, run.max_rounds, d_stats,
-                                 run.ovf_thr * 0x10001u, run.tile_order);
+                                 run.ovf_thr * 0x10001u, run.tile_order, run.fuse, run.slot_row);
     count_launch();
     WR_LAUNCH_CHECK();
     WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
@@ -965,31 +1012,22 @@ __global__ void __launch_bounds__(OUT_WARPS * 32) bf_outputs_kernel(DevGraph g, 
 // every slot that needs a predecessor has one. Results are staged in shared
 // memory and written as one full 32-B sector per source row (8 vertices x
 // 4 B), 4 rows per store instruction.
-struct PredShape {
-    static constexpr int PV = 8;     // vertices per warp job (full 32-B output sectors)
-};
-
 // PW warps per CTA (8 for 32-bit rows, 4 for packed rows: the output
 // staging sp[PW][PV][TS + 1] stays under the 48 KB static limit).
-template <class Op, int SPL, int MINB, int PA, int PW>
-__global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
-                                                      const uint32_t *__restrict__ rows,
-                                                      const int *__restrict__ slot_row, int64_t out_row0,
-                                                      int32_t *__restrict__ pred_out, int *flat_tiles) {
+// One pred job: (tile, vertices c0 .. c0+7) for all the tile's slots, by
+// one warp; spw = the warp's [PV][TS + 1] shared staging.
+template <class Op, int SPL, int PA>
+__device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restrict__ tile_src,
+                                         const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
+                                         int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
+                                         int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane) {
     constexpr int TSW = 32 * SPL;           // 32-bit words per row
     static_assert(PredShape::PV == 8, "the output stores write 8 columns per slot");
     constexpr int P = Op::PACK;
     constexpr int TS = TSW * P;             // sources (slots) per tile
     constexpr int NS = SPL * P;             // slots per lane
     constexpr int PV = PredShape::PV;
-    __shared__ int32_t sp[PW][PV][TS + 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int V = g.V;
-    const int chunks = (V + PV - 1) / PV;
-    const int64_t job = (int64_t)blockIdx.x * PW + warp;
-    if (job >= (int64_t)ntiles * chunks) return;
-    const int tile = (int)(job / chunks);
-    const int c0 = (int)(job % chunks) * PV;
     const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
     int src[NS];
 #pragma unroll
@@ -1115,8 +1153,8 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
         flat |= (need0 | need1) != 0;   // reachable, no steep tight in-arc: flat
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            sp[warp][jv][lane * NS + j] = best0[j];
-            if (two) sp[warp][jv1][lane * NS + j] = best1[j];
+            spw[jv][lane * NS + j] = best0[j];
+            if (two) spw[jv1][lane * NS + j] = best1[j];
         }
     }
     __syncwarp();
@@ -1137,14 +1175,30 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
         int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
         if (vec) {
             reinterpret_cast<int4 *>(dst)[0] =
-                make_int4(sp[warp][0][sl_in], sp[warp][1][sl_in], sp[warp][2][sl_in], sp[warp][3][sl_in]);
+                make_int4(spw[0][sl_in], spw[1][sl_in], spw[2][sl_in], spw[3][sl_in]);
             reinterpret_cast<int4 *>(dst)[1] =
-                make_int4(sp[warp][4][sl_in], sp[warp][5][sl_in], sp[warp][6][sl_in], sp[warp][7][sl_in]);
+                make_int4(spw[4][sl_in], spw[5][sl_in], spw[6][sl_in], spw[7][sl_in]);
         } else {
-            for (int jv = 0; jv < nv; ++jv) dst[jv] = sp[warp][jv][sl_in];
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv][sl_in];
         }
     }
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
+}
+
+template <class Op, int SPL, int MINB, int PA, int PW>
+__global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
+                                                      const uint32_t *__restrict__ rows,
+                                                      const int *__restrict__ slot_row, int64_t out_row0,
+                                                      int32_t *__restrict__ pred_out, int *flat_tiles) {
+    constexpr int TS = 32 * SPL * Op::PACK;
+    constexpr int PV = PredShape::PV;
+    __shared__ int32_t sp[PW][PV][TS + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int chunks = (g.V + PV - 1) / PV;
+    const int64_t job = (int64_t)blockIdx.x * PW + warp;
+    if (job >= (int64_t)ntiles * chunks) return;
+    pred_job<Op, SPL, PA>(g, tile_src, rows, slot_row, out_row0, pred_out, flat_tiles, (int)(job / chunks),
+                          (int)(job % chunks) * PV, sp[warp], lane);
 }
 
 template <class Op, int SPL, int MINB, int PA, int PW = 8 / Op::PACK>

@@ -168,6 +168,17 @@ int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_sou
 // Sources per lane (1, 2, 4) for S sources on nsm SMs (env WR_BF_SPL forces).
 int choose_spl(int64_t S, int nsm);
 
+// The canonical-pred pass fused into the sweep: CTAs whose tile claims have
+// run out take pred jobs of finished tiles (in completion order) while the
+// last tiles are still relaxing (a4 overlapped with the a3 tail).
+struct PredFuse {
+    int32_t *pred_out = nullptr;    // null = no fused pred
+    int64_t out_row0 = 0;
+    int *flat_tiles = nullptr;      // [ntiles] set if a tile has a flat vertex
+    int *done_list = nullptr;       // [ntiles] finished tiles in completion order, -1 = not yet
+    int *counters = nullptr;        // [4] zeroed: [0] done slots, [2..3] u64 pred jobs claimed
+};
+
 struct BfRun {              // one BF segment over tiles of 32*spl sources
     const int *tile_src;    // [ntiles*tsw] source vertex per slot, -1 = empty
     int ntiles;
@@ -179,6 +190,7 @@ struct BfRun {              // one BF segment over tiles of 32*spl sources
     int pack = 1;           // sources per 32-bit word: 1, or 2 (packed u16 distances)
     const int *tile_order = nullptr;  // [ntiles] claim order of the tiles (null = 0..ntiles-1)
     uint32_t ovf_thr = 0;   // pack 2: a stored distance >= ovf_thr flags a possible u16 overflow
+    PredFuse fuse;
     int tsw() const { return 32 * spl * pack; }   // sources (slots) per tile
 };
 

@@ -880,6 +880,10 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         DBuf<uint32_t> rows((size_t)max_tiles * V * 32 * spl);
         DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
         DBuf<int> flat(o.pred_out ? max_tiles : 0);
+        // a4 fused into the sweep (non-negative weights): done list + counters
+        static const bool no_fuse = getenv("WR_NO_FUSED_PRED") != nullptr;
+        const bool fused = o.pred_out && !g->has_negative && !no_fuse;
+        DBuf<int> done_list(fused ? max_tiles : 0), fuse_ctr(fused ? 4 : 0);
         int max_rounds = g->has_negative ? std::max(1, V - 1) : V;
         const int64_t *off_r = P->off_all.p + (int64_t)P->rank * (P->B + 1);
         cudaEvent_t b0, b1, b2;
@@ -893,14 +897,26 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
             run.pack = pk;
             run.ovf_thr = pk == 2 ? 0x7fffu - (uint32_t)g->max_abs_w : 0u;
+            if (fused) {
+                WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
+                WR_CUDA(cudaMemsetAsync(done_list.p, 0xff, sizeof(int) * ntiles, st));
+                WR_CUDA(cudaMemsetAsync(fuse_ctr.p, 0, sizeof(int) * 4, st));
+                run.fuse.pred_out = o.pred_out;
+                run.fuse.out_row0 = lo - P->src_lo;
+                run.fuse.flat_tiles = flat.p;
+                run.fuse.done_list = done_list.p;
+                run.fuse.counters = fuse_ctr.p;
+            }
             WR_CUDA(cudaEventRecord(b0, st));
             const double host_to_b0 =
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hclock0).count();
             bf_run(g, run, d_stats.p, st);
             WR_CUDA(cudaEventRecord(b1, st));
             if (o.pred_out) {   // a4 canonical pred of this segment's sources
-                WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
-                bf_write_outputs(g, run, lo - P->src_lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
+                if (!fused) {
+                    WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
+                    bf_write_outputs(g, run, lo - P->src_lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
+                }
                 std::vector<int> hflat(ntiles);
                 WR_CUDA(cudaMemcpyAsync(hflat.data(), flat.p, sizeof(int) * ntiles, cudaMemcpyDeviceToHost, st));
                 WR_CUDA(cudaStreamSynchronize(st));
