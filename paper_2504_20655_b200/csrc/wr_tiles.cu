@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include <climits>
+#include <thread>
 #include <vector>
 #include <cstdlib>
 #include "wr_internal.cuh"
@@ -137,7 +138,7 @@ __global__ void tiles_from_perm_kernel(const int *sources, int64_t lo, const int
 // some tiles straddle a curve jump (span 31-63 cells instead of 7), and a
 // tile's sweep time follows its spatial spread (corr 0.69; 17 ms compact
 // vs 40-52 ms straddling), not its rounds.
-static void rcb(int *idx, int n, int tsw, const int *cx, const int *cy, const int *cz) {
+static void rcb(int *idx, int n, int tsw, const int *cx, const int *cy, const int *cz, int depth = 0) {
     if (n <= tsw) return;
     int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
     for (int i = 0; i < n; ++i) {
@@ -154,8 +155,14 @@ static void rcb(int *idx, int n, int tsw, const int *cx, const int *cy, const in
     const int k = (n + tsw - 1) / tsw;
     const int nl = (k / 2) * tsw;
     std::nth_element(idx, idx + nl, idx + n, [&](int a, int b) { return key[a] < key[b] || (key[a] == key[b] && a < b); });
-    rcb(idx, nl, tsw, cx, cy, cz);
-    rcb(idx + nl, n - nl, tsw, cx, cy, cz);
+    if (depth < 4 && n > 8192) {   // the two halves are independent: top levels on host threads
+        std::thread left([=] { rcb(idx, nl, tsw, cx, cy, cz, depth + 1); });
+        rcb(idx + nl, n - nl, tsw, cx, cy, cz, depth + 1);
+        left.join();
+    } else {
+        rcb(idx, nl, tsw, cx, cy, cz, depth + 1);
+        rcb(idx + nl, n - nl, tsw, cx, cy, cz, depth + 1);
+    }
 }
 
 static bool rcb_perm(const wr_graph *g, const int *d_sources, int64_t lo, int n, int tsw, int *d_perm,
