@@ -299,10 +299,14 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
-    int a0 = 0, a1 = 0;
-    if (act) {
+    int a0 = 0, a1 = 0, o0 = 0, o1 = 0;
+    if (act) {   // out-arc range loaded now: step C then needs one dependent load less
         a0 = g.in_ptr[v];
         a1 = g.in_ptr[v + 1];
+        if (DELTA) {
+            o0 = g.out_ptr[v];
+            o1 = g.out_ptr[v + 1];
+        }
     }
     // ---- A: queue this lane's changed in-arcs; the packed (u, w) arcs are
     // loaded AQ at a time (independent loads in flight, no branch between
@@ -418,8 +422,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     if (DELTA && lane == 0 && (chg & ~tw)) touched[w] = tw | chg;   // this warp owns word w
     // ---- C: improved vertices mark their out-neighbours, lane-parallel
     if (DELTA && ((chg >> lane) & 1u)) {
-        const int o1 = g.out_ptr[v + 1];
-        for (int e = g.out_ptr[v]; e < o1; ++e) {
+        for (int e = o0; e < o1; ++e) {
             const int x = g.out_dst[e];
             if (LIST) {
                 if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u) nlist[atomicAdd(nlen, 1)] = x >> 5;
