@@ -318,6 +318,10 @@ def main():
     # tile (128 sources, 256 packed).
     rb = row_bits[0] or 32
     alg_bytes = S * (g.V * rb // 8) + (S / (128.0 * 32 / rb)) * (12 * E + 8 * g.V)
+    if not a.no_pred:
+        # the canonical-pred pass (a4) runs fused inside the same kernel: it
+        # reads every distance once more and writes every int32 pred once
+        alg_bytes += S * g.V * (rb // 8 + 4)
     bf_s = bf_step_ms / 1e3
     achieved = alg_bytes / bf_s / 1e9 if bf_s > 0 else None
     traffic = None
@@ -346,7 +350,8 @@ def main():
                      "frac": achieved / hbm_peak if achieved else None,
                      "traffic": traffic / 1e9 if traffic else None, "traffic_unit": "GB per launch",
                      "algorithmic_gb_per_launch": alg_bytes / 1e9,
-                     "kernel": "bf_frontier_kernel", "peak_kind": peak_kind,
+                     "kernel": "bf_frontier_kernel" + (" (a3 sweep + fused a4 pred pass)" if not a.no_pred else ""),
+                     "peak_kind": peak_kind,
                      "note": "latency-bound frontier sweep; see DESIGN.md section 9"},
         "roofline_alu": {"bound": "alu", "achieved": alu_ach / 1e12 if alu_ach else None,
                          "peak": alu_peak / 1e12, "unit": "T relaxations/s",
