@@ -329,6 +329,30 @@ def test_packed_rows_equal_rows32():
     compare_orders(g, orders, m=1, G=G, results=a)
 
 
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_fused_pred_segments_and_budget(wtype):
+    """The pred pass fused into the sweep (CTAs out of tiles take pred jobs
+    of finished tiles) gives the same rows with one segment and with many
+    (small HBM budget), and the same rows as the standalone pred kernel of
+    wr_bf_batch; spot rows equal the oracle's canonical pred."""
+    g, orders, _ = gen.config(3, wtype=wtype, B=1024)
+    G = wr.Graph.from_gen(g)
+    stops = np.unique(orders.order_nodes)
+    S = stops.size
+    a, pa, sa = _orders_with_pred(G, orders, S, g.V)
+    pred = torch.full((S, g.V), -7, dtype=torch.int32, device="cuda")
+    budget = G.info().device_bytes + (128 << 20) + 256 * 4 * g.V
+    b, sb = wr.route_orders(G, orders.order_ptr, orders.order_nodes, pred_out=pred, hbm_budget=budget)
+    assert sb.segments > 1
+    assert a.tobytes() == b.tobytes()
+    assert np.array_equal(pa, pred.cpu().numpy())
+    _, pb, _ = wr.bf_batch(G, stops[::37], pred=True)
+    assert np.array_equal(pa[::37], pb)
+    rows = oracle.bf_many(g, stops[::97])
+    for k, i in enumerate(range(0, S, 97)):
+        assert np.array_equal(pa[i], oracle.pred(g, int(stops[i]), rows[k]))
+
+
 def _long_grid(n=24, w=0x3000):
     """n x n bidirectional grid with weights near the packed limit: distances
     reach ~2n*w >> 0x7fff, so a packed sweep must detect the overflow and
