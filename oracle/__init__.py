@@ -51,6 +51,7 @@ def lib():
         L.orc_exact_route_range.argtypes = [C.c_int, vp, C.c_int, C.c_longlong, C.c_longlong, vp, vp, lp]
         L.orc_exact_route_chunked.argtypes = [C.c_int, vp, C.c_int, C.c_longlong, vp, vp, lp, lp]
         L.orc_segmented_route.argtypes = [C.c_int, vp, C.c_int, vp, vp, vp, vp]
+        L.orc_segmented_pairs_route.argtypes = [C.c_int, vp, C.c_int, vp, vp, vp, vp]
         L.orc_kmeans.argtypes = [vp, C.c_int, C.c_int, vp]
         L.orc_order_stops.argtypes = [vp, C.c_int, vp]
         L.orc_perm_rank.argtypes = [vp, C.c_int]
@@ -58,7 +59,7 @@ def lib():
         L.orc_route_count_reduction.argtypes = [C.c_int, vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]
         L.orc_bf_many.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int]
         L.orc_route_orders.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, vp, C.c_longlong,
-                                       C.c_int, vp, C.c_int, vp, vp, vp, vp, vp]
+                                       C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int]
         L.orc_certificate.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
         L.orc_certificate.restype = C.c_longlong
     return _lib
@@ -204,6 +205,20 @@ def segmented_route(D, labels):
     return cost[0], seq, (int(counts[0]), int(counts[1]))
 
 
+def segmented_pairs_route(D, labels):
+    """NEXT-1 boundary-pair stitch: (cost, seq, (segment orders evaluated,
+    stitch candidates))."""
+    D, wt, n = _D(D)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    seq = np.zeros(n, dtype=np.int32)
+    cost = np.zeros(1, dtype=_vdt(wt))
+    counts = np.zeros(2, dtype=np.int64)
+    rc = lib().orc_segmented_pairs_route(wt, _p(D), n, _p(labels), _p(seq), _p(cost), _p(counts))
+    if rc:
+        raise OracleError(rc, "segmented_pairs_route")
+    return cost[0], seq, (int(counts[0]), int(counts[1]))
+
+
 def kmeans(xy, K: int):
     xy = np.ascontiguousarray(xy, dtype=np.int32).reshape(-1, 2)
     labels = np.zeros(xy.shape[0], dtype=np.int32)
@@ -232,7 +247,7 @@ def route_count_reduction(n_j):
     return red.value, brute.value
 
 
-def route_orders(g, orders, m: int = 1, nthreads: int = None):
+def route_orders(g, orders, m: int = 1, nthreads: int = None, pairs: bool = False):
     """a2..a7 composed. Returns dict(n, seq [B,16] node ids, cost, rank, rc)."""
     V, src, dst, w = _graph(g)
     wt = _wt(w)
@@ -247,7 +262,7 @@ def route_orders(g, orders, m: int = 1, nthreads: int = None):
     out_rc = np.zeros(B, dtype=np.int32)
     rc = lib().orc_route_orders(V, src.size, _p(src), _p(dst), _p(w), wt, _p(ptr), _p(nodes), B, m,
                                 _p(xy), nthreads or os.cpu_count(), _p(out_n), _p(out_seq),
-                                _p(out_cost), _p(out_rank), _p(out_rc))
+                                _p(out_cost), _p(out_rank), _p(out_rc), 1 if pairs else 0)
     return dict(rc=rc, n=out_n, seq=out_seq, cost=out_cost, rank=out_rank, order_rc=out_rc)
 
 

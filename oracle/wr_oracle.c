@@ -31,6 +31,10 @@
  *   orc_segmented_route  O7 Theorem 3.1 stitch (P324-337 §3) pinned: worked
  *                     example labelings, m=1 == exact, singletons == exact,
  *                     segmented >= exact, candidate counts vs Thm 3.1.
+ *   orc_segmented_pairs_route  NEXT-1 boundary-pair stitch:
+ *                     pinned: m=1 == exact, singletons == exact, and for int
+ *                     weights == (min cost, lex-smallest) over ALL segment-
+ *                     contiguous orders by brute force; int cost <= O7's.
  *   orc_kmeans        O8 deterministic integer K-means   pinned: hand-made
  *                     separated clusters, brute-force Lloyd fixpoint check.
  *   orc_order_stops   a2 stop projection (P226-238 §2.4) pinned: numpy unique.
@@ -449,6 +453,113 @@ int orc_segmented_route(int wtype, const void *D, int n, const int *labels,
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-1 boundary-pair segmented route (reading R1 in  */
+/* DESIGN.md). The paper stitches one fixed best route per segment in both  */
+/* orientations (O7, P324-337 §3). This variant keeps, per segment, the best */
+/* open path for every ordered endpoint pair (first a, last b):             */
+/*  1. relabel segments by first appearance (as O7);                         */
+/*  2. per segment j (n_j <= 9 stops): enumerate all n_j! orders of its stops */
+/*     lexicographically, cost each left to right (O4), and keep for its    */
+/*     (first, last) pair the first strictly cheaper order (ties -> the     */
+/*     lexicographically smallest); a single stop is its own path;          */
+/*  3. stitch: for every segment order (m! of them, lexicographic) and every */
+/*     choice of one endpoint pair per segment, concatenate the kept paths, */
+/*     cost the full n-stop sequence left to right, keep the minimum, ties  */
+/*     -> the lexicographically smallest sequence.                          */
+/* Candidates m! * prod_j pairs_j <= 2^26, else ETOOLARGE (as the GPU).      */
+/* counts_out = {segment orders evaluated, stitch candidates}.               */
+/* ------------------------------------------------------------------------ */
+int orc_segmented_pairs_route(int wtype, const void *D, int n, const int *labels,
+                              int *seq_out, void *cost_out, long long *counts_out)
+{
+    if (n < 1 || n > 16) return ORC_EINVAL;
+    int seg_of[16], nseg = 0, map_lab[16], map_id[16], nmap = 0;
+    for (int i = 0; i < n; ++i) {
+        int id = -1;
+        for (int k = 0; k < nmap; ++k) if (map_lab[k] == labels[i]) id = map_id[k];
+        if (id < 0) { map_lab[nmap] = labels[i]; map_id[nmap] = nseg; id = nseg++; ++nmap; }
+        seg_of[i] = id;
+    }
+    if (nseg > 6) return ORC_ETOOLARGE;
+    int seg_len[6] = {0}, seg_stops[6][16];
+    for (int i = 0; i < n; ++i) seg_stops[seg_of[i]][seg_len[seg_of[i]]++] = i;
+    /* step 2: best path per (segment, first, last); path[j][a][b][0..nj) */
+    static __thread int path[6][9][9][9];
+    static __thread char pcost[6][9][9][4];
+    static __thread int have[6][9][9];
+    long long seg_evals = 0;
+    int npairs[6], pair_a[6][81], pair_b[6][81];
+    for (int j = 0; j < nseg; ++j) {
+        const int nj = seg_len[j];
+        if (nj > 9) return ORC_ETOOLARGE;
+        memset(have[j], 0, sizeof(have[j]));
+        int loc[9], g[9];
+        for (int a = 0; a < nj; ++a) loc[a] = a;
+        do {
+            for (int a = 0; a < nj; ++a) g[a] = seg_stops[j][loc[a]];
+            char c[4] = {0};
+            if (nj >= 2) {
+                int rc = orc_route_cost(wtype, D, n, g, nj, c);
+                if (rc) return rc;
+            }
+            ++seg_evals;
+            const int fa = loc[0], lb = loc[nj - 1];
+            if (!have[j][fa][lb] || cost_less(wtype, c, pcost[j][fa][lb])) {
+                have[j][fa][lb] = 1;
+                memcpy(pcost[j][fa][lb], c, 4);
+                memcpy(path[j][fa][lb], g, sizeof(int) * (size_t)nj);
+            }
+        } while (next_perm(loc, nj));
+        npairs[j] = 0;
+        for (int a = 0; a < nj; ++a)
+            for (int b = 0; b < nj; ++b)
+                if (have[j][a][b]) { pair_a[j][npairs[j]] = a; pair_b[j][npairs[j]] = b; ++npairs[j]; }
+    }
+    long long ncand = factorial(nseg);
+    for (int j = 0; j < nseg; ++j) ncand *= npairs[j];
+    if (ncand > (1ll << 26)) return ORC_ETOOLARGE;
+    /* step 3: stitch over segment orders x endpoint pairs, full recompute */
+    int tau[6];
+    for (int k = 0; k < nseg; ++k) tau[k] = k;
+    int best_seq[16], cand[16], got = 0;
+    char best[4] = {0}, cur[4] = {0};
+    long long stitched = 0;
+    do {
+        int choice[6] = {0};
+        for (;;) {
+            int pos = 0;
+            for (int k = 0; k < nseg; ++k) {
+                const int j = tau[k], nj = seg_len[j];
+                const int a = pair_a[j][choice[k]], b = pair_b[j][choice[k]];
+                for (int t = 0; t < nj; ++t) cand[pos++] = path[j][a][b][t];
+            }
+            if (n >= 2) {
+                int rc = orc_route_cost(wtype, D, n, cand, n, cur);
+                if (rc) return rc;
+            } else {
+                memset(cur, 0, 4);
+            }
+            ++stitched;
+            int better = !got || cost_less(wtype, cur, best);
+            if (!better && cost_equal(wtype, cur, best)) {
+                for (int t = 0; t < n; ++t) {
+                    if (cand[t] != best_seq[t]) { better = cand[t] < best_seq[t]; break; }
+                }
+            }
+            if (better) { got = 1; memcpy(best, cur, 4); memcpy(best_seq, cand, sizeof(int) * (size_t)n); }
+            /* next endpoint choice: mixed radix, last segment fastest */
+            int k = nseg - 1;
+            while (k >= 0 && ++choice[k] == npairs[tau[k]]) { choice[k] = 0; --k; }
+            if (k < 0) break;
+        }
+    } while (next_perm(tau, nseg));
+    memcpy(seq_out, best_seq, sizeof(int) * (size_t)n);
+    memcpy(cost_out, best, 4);
+    if (counts_out) { counts_out[0] = seg_evals; counts_out[1] = stitched; }
+    return ORC_OK;
+}
+
 /* Theorem 3.1 (P326-329 §3): undirected count m! 2^(m-1) + (1/2) sum n_j!,  */
 /* and the brute-force undirected count n!/2.                                 */
 void orc_route_count_reduction(int m, const int *n_j, unsigned long long *reduced,
@@ -587,7 +698,7 @@ typedef struct {
     const long long *order_ptr; const int *order_nodes; long long B;
     int m; const int *xy; const int *labels_in;
     int *out_n; int *out_seq; void *out_cost; long long *out_rank; int *out_rc;
-    long long next; pthread_mutex_t mu;
+    long long next; pthread_mutex_t mu; int pairs;
 } route_job;
 
 static void *route_worker(void *arg)
@@ -628,7 +739,8 @@ static void *route_worker(void *arg)
                 orc_kmeans(xy, n, j->m, labels);
             }
             long long counts[2];
-            rc = orc_segmented_route(j->wtype, D, n, labels, seq, cost, counts);
+            if (j->pairs) rc = orc_segmented_pairs_route(j->wtype, D, n, labels, seq, cost, counts);
+            else rc = orc_segmented_route(j->wtype, D, n, labels, seq, cost, counts);
             rank = orc_perm_rank(seq, n);
         }
         j->out_rc[o] = rc;
@@ -641,13 +753,14 @@ static void *route_worker(void *arg)
 }
 
 /* a2..a7 for a batch of orders: stops -> distinct sources -> BF rows ->      */
-/* per-order D -> exact (m <= 1) or segmented (m >= 2, O8 labels from xy)     */
-/* route. out_seq is B x 16 node ids. Returns the first failing code.         */
+/* per-order D -> exact (m <= 1) or segmented (m >= 2, O8 labels from xy;     */
+/* pairs != 0: the NEXT-1 boundary-pair stitch) route. out_seq is B x 16 node */
+/* ids. Returns the first failing code.                                       */
 int orc_route_orders(int V, long long E, const int *src, const int *dst, const void *w,
                      int wtype, const long long *order_ptr, const int *order_nodes,
                      long long B, int m, const int *xy, int nthreads,
                      int *out_n, int *out_seq, void *out_cost, long long *out_rank,
-                     int *out_rc)
+                     int *out_rc, int pairs)
 {
     int *row_of = (int *)malloc(sizeof(int) * (size_t)V);
     for (int v = 0; v < V; ++v) row_of[v] = -1;
@@ -662,7 +775,7 @@ int orc_route_orders(int V, long long E, const int *src, const int *dst, const v
     int rc = orc_bf_many(V, E, src, dst, w, wtype, sources, S, rows, nthreads);
     if (rc == ORC_OK) {
         route_job j = {wtype, V, row_of, rows, order_ptr, order_nodes, B, m, xy, NULL,
-                       out_n, out_seq, out_cost, out_rank, out_rc, 0, PTHREAD_MUTEX_INITIALIZER};
+                       out_n, out_seq, out_cost, out_rank, out_rc, 0, PTHREAD_MUTEX_INITIALIZER, pairs};
         pthread_t th[256];
         if (nthreads < 1) nthreads = 1;
         if (nthreads > 256) nthreads = 256;

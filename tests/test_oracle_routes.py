@@ -273,6 +273,80 @@ def test_segmented_invariants(kind):
         assert np.asarray(oracle.route_cost(D, s)).tobytes() == np.asarray(c).tobytes()
 
 
+# ---------------------------------------------------------------- NEXT-1 boundary pairs
+def _contiguous_best(D, labels):
+    """Brute force over ALL n! orders keeping those in which every segment's
+    stops are consecutive: (min left-to-right cost, lexicographically
+    smallest such order). For int weights this is what the boundary-pair
+    stitch must return (reading R1)."""
+    n = D.shape[0]
+    best = None
+    for p in itertools.permutations(range(n)):
+        seen, prev, ok = set(), None, True
+        for x in p:
+            lab = labels[x]
+            if lab != prev:
+                if lab in seen:
+                    ok = False
+                    break
+                seen.add(lab)
+                prev = lab
+        if not ok:
+            continue
+        c = lr_cost(D, p)
+        if best is None or c < best[0]:   # permutations() is lexicographic: first wins ties
+            best = (c, p)
+    return best
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_pairs_reduces_to_exact(kind):
+    """One segment, or all singletons: the boundary-pair stitch is the exact
+    route (cost and lexicographic argmin)."""
+    rng = np.random.default_rng(71 if kind == "int" else 72)
+    for trial in range(30):
+        n = int(rng.integers(1, 7))   # <= 6 segments (WR_MAX_SEGMENTS)
+        D = random_D(rng, n, kind)
+        ec, er, es = oracle.exact_route(D)
+        for labels in (np.zeros(n, dtype=np.int32), np.arange(n, dtype=np.int32)):
+            c, s, _ = oracle.segmented_pairs_route(D, labels)
+            assert np.asarray(c).tobytes() == np.asarray(ec).tobytes() and s.tolist() == es.tolist()
+
+
+def test_pairs_equals_contiguous_brute_force_and_dominates():
+    """int: the boundary-pair result is the best segment-contiguous order
+    (independent brute force), never worse than the paper's fixed-route
+    stitch (O7), strictly better on some instances; counts follow the
+    definition (sum n_j! segment orders, m! * prod pairs candidates)."""
+    rng = np.random.default_rng(73)
+    strictly = 0
+    for trial in range(120):
+        n = int(rng.integers(2, 8))
+        D = random_D(rng, n, "int")
+        labels = rng.integers(0, 3, n).astype(np.int32)
+        c, s, counts = oracle.segmented_pairs_route(D, labels)
+        bc, bp = _contiguous_best(D, labels)
+        assert int(c) == int(bc) and tuple(s.tolist()) == tuple(bp)
+        oc, _, _ = oracle.segmented_route(D, labels)
+        assert int(c) <= int(oc)
+        strictly += int(c) < int(oc)
+        segs = [int((labels == l).sum()) for l in np.unique(labels)]
+        assert counts[0] == sum(math.factorial(k) for k in segs)
+        pairs = math.prod(k * (k - 1) if k >= 2 else 1 for k in segs)
+        assert counts[1] == math.factorial(len(segs)) * pairs
+    assert strictly > 0
+
+
+def test_pairs_three_aisle_labelings():
+    """Worked example (tests/golden/three_aisle.txt): segments of <= 2 stops
+    give the same stitch as O7 (both orientations are all endpoint pairs):
+    17 / 21 / 22 as in P3."""
+    D = load_three_aisle()["D"]
+    for labels, cost in (([0, 1, 1, 2, 2], 17), ([0, 0, 1, 1, 2], 21), ([0, 1, 2, 0, 1], 22)):
+        c, s, _ = oracle.segmented_pairs_route(D, np.array(labels, np.int32))
+        assert int(c) == cost
+
+
 # ---------------------------------------------------------------- O8
 def test_kmeans_separated_clusters():
     xy = np.array([[0, 0], [100, 100], [1, 0], [0, 1], [200, 0], [101, 99], [201, 1]])
