@@ -189,6 +189,14 @@ typedef struct {
  * results are identical either way - a packed sweep whose distances could
  * exceed 0x7ffe is redone with 32-bit rows). */
 #define WR_ROUTE_ROWS32 1
+/* wr_route_opts.flags: segmented routing (m >= 2) with the boundary-pair
+ * stitch (reading R1) instead of the paper's
+ * fixed-route stitch (O7): per segment the best open path for every ordered
+ * endpoint pair (first, last), then every segment order x one pair per
+ * segment is costed left to right over the full sequence; min cost, ties ->
+ * lexicographically smallest sequence. Segments <= 9 stops and
+ * m'! * prod n_j (n_j - 1) <= 2^26 candidates, else WR_ETOOLARGE. */
+#define WR_ROUTE_PAIRS 2
 
 typedef struct {
     int32_t n;               /* stops (distinct nodes, ascending before routing) */

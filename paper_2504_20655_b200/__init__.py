@@ -23,6 +23,7 @@ WR_I32, WR_F32 = 0, 1
 WR_COO, WR_CSR = 0, 1
 WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE = 0, 1, 2
 WR_ROUTE_ROWS32 = 1
+WR_ROUTE_PAIRS = 2
 MAX_STOPS = 16
 DEFAULT_CHUNK = 2903040
 I32_INF = np.iinfo(np.int32).max
@@ -280,13 +281,14 @@ def decode_cost(results, wtype):
     return bits.view(np.float32) if wtype == WR_F32 else bits.view(np.int32)
 
 
-def route_segmented(g: Graph, stops, labels=None, m: int = 1, chunk: int = 0, stream=None):
+def route_segmented(g: Graph, stops, labels=None, m: int = 1, chunk: int = 0, stream=None, flags: int = 0):
     """a7: Theorem 3.1 route of one stop set (labels align with the sorted
-    distinct stops; None -> O8 plan with K = m)."""
+    distinct stops; None -> O8 plan with K = m). flags=WR_ROUTE_PAIRS: the
+    boundary-pair stitch (NEXT-1)."""
     stops = _arr(stops, np.int32)
     lab = _arr(labels, np.int32) if labels is not None else None
     out = np.zeros(1, dtype=RESULT_DTYPE)
-    o = RouteOpts(_stream_ptr(stream), 0, m, chunk, 0)
+    o = RouteOpts(_stream_ptr(stream), 0, m, chunk, 0, None, 0, flags)
     _check(lib.wr_route_segmented(g.handle, _ptr(stops), int(stops.shape[0]), _ptr(lab), m, C.byref(o),
                                   out.ctypes.data))
     return out[0]

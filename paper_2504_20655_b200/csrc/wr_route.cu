@@ -424,6 +424,9 @@ __global__ void assemble_kernel(const int *stops, const int *n_arr, const int *s
 }
 
 // ------------------------------------------------ route preparation --
+constexpr int PAIRS_MAX_SEG = 9;                  // stops per segment, boundary-pair mode
+constexpr int64_t PAIRS_MAX_CAND = 1ll << 26;      // stitch candidates per order
+
 struct OrderRoute {        // per-order routing state (device)
     int n;
     int status;
@@ -442,7 +445,7 @@ template <class C>
 __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
                                      int64_t nord, const uint32_t *Dall, int m, const int *xy,
                                      const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
-                                     int *item_cnt) {
+                                     int *item_cnt, int pairs) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nord) return;
     const int64_t o = o_lo + t;
@@ -495,6 +498,18 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 const int k = seg_of[i];
                 R.segmap[k] |= (uint64_t)i << (4 * R.seglen[k]);
                 R.seglen[k]++;
+            }
+            if (pairs && nseg >= 2) {
+                // boundary-pair stitch (NEXT-1): per-segment orders and the
+                // stitch run in the finalize warp; limits as the oracle's
+                int64_t ncand = fact(nseg);
+                for (int k = 0; k < nseg; ++k) {
+                    const int nj = R.seglen[k];
+                    if (nj > PAIRS_MAX_SEG) R.status = WR_ETOOLARGE;
+                    ncand *= nj >= 2 ? (int64_t)nj * (nj - 1) : 1;
+                }
+                if (ncand > PAIRS_MAX_CAND) R.status = WR_ETOOLARGE;
+                nseg = 0;   // no enumeration problems
             }
             for (int k = 0; k < nseg; ++k) {
                 if (R.seglen[k] > WR_MAX_EXACT) { R.status = WR_ETOOLARGE; break; }
@@ -554,8 +569,11 @@ __global__ void route_emit_kernel(int64_t nord, OrderRoute *ordr, const int *pro
 template <class C>
 __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, const uint64_t *prob_best,
                                       const RouteProblem *probs, const uint32_t *Dall, const int *stops,
-                                      int64_t o_lo, wr_route_result *out, unsigned long long *counters) {
+                                      int64_t o_lo, wr_route_result *out, unsigned long long *counters, int pairs) {
     __shared__ uint32_t sD[4][DSTRIDE];
+    // boundary-pair mode: best (cost key << 32 | local lexicographic rank)
+    // per (segment, first, last), then the path as a nibble sequence
+    __shared__ unsigned long long sPair[4][WR_MAX_SEGMENTS][PAIRS_MAX_SEG][PAIRS_MAX_SEG];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t t = (int64_t)blockIdx.x * 4 + warp;
     if (t >= nord) return;
@@ -577,10 +595,116 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     uint32_t *Ds = sD[warp];
     for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
     __syncwarp();
+    uint64_t final_seq = 0;
+    uint32_t final_cost = 0;
+    unsigned long long perms = 0;
+    if (pairs && R.mseg >= 2) {
+        // NEXT-1 boundary-pair stitch (oracle: orc_segmented_pairs_route).
+        // 1. per segment, every local order (lexicographic rank r) is costed
+        //    left to right; its (first, last) bin keeps the smallest
+        //    (cost key, r) - ties -> the lexicographically smallest order
+        const int m = R.mseg;
+        unsigned long long(*tab)[PAIRS_MAX_SEG][PAIRS_MAX_SEG] = sPair[warp];
+        for (int k = 0; k < m; ++k)
+            for (int e = lane; e < PAIRS_MAX_SEG * PAIRS_MAX_SEG; e += 32)
+                tab[k][e / PAIRS_MAX_SEG][e % PAIRS_MAX_SEG] = ~0ull;
+        __syncwarp();
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            if (nj < 2) continue;
+            const int64_t nf = fact(nj);
+            perms += (unsigned long long)nf;
+            for (int64_t r = lane; r < nf; r += 32) {
+                const uint64_t loc = unrank_nib(r, nj);
+                int prev = nib(R.segmap[k], nib(loc, 0));
+                const int nx = nib(R.segmap[k], nib(loc, 1));
+                uint32_t cost = Ds[prev * MS + nx];
+                prev = nx;
+                for (int a = 2; a < nj; ++a) {
+                    const int x = nib(R.segmap[k], nib(loc, a));
+                    cost = C::add(cost, Ds[prev * MS + x]);
+                    prev = x;
+                }
+                const unsigned long long key = ((unsigned long long)C::key(cost) << 32) | (unsigned long long)r;
+                atomicMin(&tab[k][nib(loc, 0)][nib(loc, nj - 1)], key);
+            }
+        }
+        __syncwarp();
+        // 2. the kept path of every pair as a nibble sequence of order stops
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            for (int e = lane; e < nj * nj; e += 32) {
+                const int a = e / nj, b = e % nj;
+                uint64_t g = 0;
+                if (nj == 1) {
+                    g = R.segmap[k];
+                } else if (a != b) {
+                    const uint64_t loc = unrank_nib((int64_t)(uint32_t)tab[k][a][b], nj);
+                    for (int t2 = 0; t2 < nj; ++t2) g |= (uint64_t)nib(R.segmap[k], nib(loc, t2)) << (4 * t2);
+                }
+                tab[k][a][b] = g;
+            }
+        }
+        __syncwarp();
+        // 3. stitch: segment order x one endpoint pair per segment, full
+        //    left-to-right recompute, ties -> lexicographically smallest
+        int np[WR_MAX_SEGMENTS];
+        int64_t P = 1;
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            np[k] = nj >= 2 ? nj * (nj - 1) : 1;
+            P *= np[k];
+        }
+        const int64_t ncand = fact(m) * P;
+        uint32_t best_key = 0xffffffffu;
+        uint64_t best_seq = ~0ull;
+        for (int64_t c = lane; c < ncand; c += 32) {
+            const uint64_t tau = unrank_nib(c / P, m);
+            int64_t rest = c % P;
+            uint64_t seq = 0;
+            int pos = 0;
+            for (int k = m - 1; k >= 0; --k) {   // mixed radix, last segment fastest
+                const int j = nib(tau, k);
+                const int nj = R.seglen[j];
+                const int p = (int)(rest % np[j]);
+                rest /= np[j];
+                int a = 0, b = 0;
+                if (nj >= 2) {
+                    a = p / (nj - 1);
+                    b = p % (nj - 1);
+                    b += b >= a;
+                }
+                // place segment k's path at its position: positions are
+                // filled right to left (segments k+1.. already placed)
+                pos += nj;
+                seq |= tab[j][a][b] << (4 * (n - pos));
+            }
+            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
+            for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
+            const uint32_t key = C::key(cost);
+            uint64_t lex = 0;
+            for (int a = 0; a < n; ++a) lex |= (uint64_t)nib(seq, a) << (4 * (15 - a));
+            if (key < best_key || (key == best_key && lex < best_seq)) {
+                best_key = key;
+                best_seq = lex;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
+            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
+            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
+                best_key = k2;
+                best_seq = s2;
+            }
+        }
+        final_cost = C::unkey(best_key);
+        for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
+        if (lane == 0) atomicAdd(&counters[1], (unsigned long long)ncand);
+    } else {
     // each segment's best route as a nibble sequence of order-stop indices
     uint64_t segseq[WR_MAX_SEGMENTS];
     int pi = R.prob0;
-    unsigned long long perms = 0;
     for (int k = 0; k < R.mseg; ++k) {
         const int nj = R.seglen[k];
         if (nj >= 2) {
@@ -595,8 +719,6 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
             segseq[k] = R.segmap[k];   // 0 or 1 stop
         }
     }
-    uint64_t final_seq;
-    uint32_t final_cost;
     if (R.mseg == 1) {
         final_seq = segseq[0];
         if (n >= 2) {
@@ -648,6 +770,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         final_seq = 0;
         for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
         if (lane == 0) atomicAdd(&counters[1], (unsigned long long)ncand);
+    }
     }
     if (lane == 0) {
         // Lehmer rank of the final sequence among the n! orders
@@ -702,6 +825,7 @@ struct Plan {               // wr_plan
     int64_t src_lo = 0, src_hi = 0, order_lo = 0, order_hi = 0;
     int64_t send_count = 0, max_send = 0;
     int m = 1;
+    int pairs = 0;          // WR_ROUTE_PAIRS: boundary-pair stitch (NEXT-1)
     int64_t chunk = WR_DEFAULT_CHUNK;
     DBuf<int> stops, n_arr, status, is_src, src_row, sources;
     DBuf<int64_t> blk;      // world+1 source block boundaries
@@ -738,6 +862,7 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     P->rank = rank;
     P->world = world;
     P->m = o.m;
+    P->pairs = (o.flags & WR_ROUTE_PAIRS) ? 1 : 0;
     P->chunk = o.chunk > 0 ? o.chunk : WR_DEFAULT_CHUNK;
     if (P->m >= 2 && !labels16 && !g->xy.p)
         return fail(WR_EINVAL, "wr_orders_plan: segmented routing without labels needs graph xy (O8)");
@@ -1009,7 +1134,7 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     WR_CUDA(cudaMemsetAsync(icnt.p + nord, 0, 4, st));
     route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
         P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
-        P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p);
+        P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs);
     count_launch();
     WR_LAUNCH_CHECK();
     scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
@@ -1033,7 +1158,7 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
         WR_LAUNCH_CHECK();
     }
     route_finalize_kernel<C><<<gridn(nord, 4), 128, 0, st>>>(nord, ordr.p, prob_best.p, probs.p, Dall, P.stops.p,
-                                                             o_lo, d_res, d_counters);
+                                                             o_lo, d_res, d_counters, P.pairs);
     count_launch();
     WR_LAUNCH_CHECK();
     WR_CUDA(cudaStreamSynchronize(st));   // temporaries are freed on return

@@ -213,11 +213,49 @@ def test_route_segmented_random_labels(wtype):
         assert r["seq"][:n].tolist() == stops[s].tolist()
 
 
-def compare_orders(g, orders, m, chunk=0, G=None, results=None):
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_segmented_pairs_random_labels(wtype):
+    """NEXT-1 boundary-pair stitch through wr_route_segmented against the
+    oracle's step-by-step definition (segments up to 9 stops)."""
+    g = gen.config(3, wtype=wtype)[0]
+    G = wr.Graph.from_gen(g)
+    rng = np.random.default_rng(33 if wtype == "i32" else 34)
+    for trial in range(25):
+        n = int(rng.integers(2, 13))
+        stops = np.sort(rng.choice(5000, n, replace=False)).astype(np.int32)
+        labels = rng.integers(0, min(6, max(2, n // 3)), n).astype(np.int32)
+        D = oracle.bf_many(g, stops)[:, stops]
+        try:
+            c, s, counts = oracle.segmented_pairs_route(D, labels)
+        except oracle.OracleError as e:
+            assert e.code == 6
+            r = wr.route_segmented(G, stops, labels=labels, m=6, flags=wr.WR_ROUTE_PAIRS)
+            assert r["status"] == wr.WR_ETOOLARGE
+            continue
+        r = wr.route_segmented(G, stops, labels=labels, m=6, flags=wr.WR_ROUTE_PAIRS)
+        assert wr.decode_cost(np.array([r]), G.wtype)[0].tobytes() == np.asarray(c).tobytes()
+        assert r["seq"][:n].tolist() == stops[s].tolist()
+
+
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_orders_pairs_config4(wtype):
+    """C4 (10-11 stops, m = 3 O8 segments) with the boundary-pair stitch: every
+    order equals the oracle; int costs never exceed the paper's stitch."""
+    g, orders, _ = gen.config(4, wtype=wtype, B=256)
+    G = wr.Graph.from_gen(g)
+    res, st = compare_orders(g, orders, m=3, G=G, flags=wr.WR_ROUTE_PAIRS)
+    assert st.stitch_candidates > 0
+    if wtype == "i32":
+        base, _ = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=3)
+        a, b = wr.decode_cost(res, G.wtype), wr.decode_cost(base, G.wtype)
+        assert (a <= b).all() and (a < b).any()
+
+
+def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
     G = G or wr.Graph.from_gen(g)
-    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk) if results is None \
-        else (results, None)
-    exp = oracle.route_orders(g, orders, m=m)
+    res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk, flags=flags) \
+        if results is None else (results, None)
+    exp = oracle.route_orders(g, orders, m=m, pairs=bool(flags & wr.WR_ROUTE_PAIRS))
     ok = exp["order_rc"] == 0
     assert np.array_equal(res["status"][ok], np.zeros(ok.sum()))
     cost = wr.decode_cost(res, G.wtype)
