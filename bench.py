@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--wtype", default="i32", choices=["i32", "f32"])
     ap.add_argument("--m", type=int, default=1, help="segments (1 = exact routes)")
+    ap.add_argument("--pairs", action="store_true", help="segmented routes with the boundary-pair stitch (NEXT-1)")
     ap.add_argument("--no-pred", action="store_true", help="skip a4 (diagnostics only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -108,7 +109,7 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(g, orders, seconds, S_total):
+def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
     """The oracle as it stands, on the host cores, on a bounded sample: BF from
     a prefix of the distinct sources and exact routing of a prefix of the
     orders (their D rows recomputed by the oracle); extrapolated to the whole
@@ -135,7 +136,7 @@ def cpu_baseline(g, orders, seconds, S_total):
                      order_nodes=orders.order_nodes[:int(orders.order_ptr[nord])].copy())
         sstops = np.unique(sub.order_nodes)
         t0 = time.perf_counter()
-        res = oracle.route_orders(g, sub, m=1, nthreads=threads)
+        res = oracle.route_orders(g, sub, m=m, nthreads=threads, pairs=pairs)
         dt = time.perf_counter() - t0
         assert res["rc"] == 0
         t_route = max(0.0, (dt - t_bf * sstops.size)) / nord
@@ -162,7 +163,7 @@ def run_reference(a):
     cb = None
     for s in range(a.warmup + a.steps):
         t0 = time.perf_counter()
-        cb = cpu_baseline(g, orders, max(2.0, a.cpu_seconds / max(1, a.steps)), S)
+        cb = cpu_baseline(g, orders, max(2.0, a.cpu_seconds / max(1, a.steps)), S, m=a.m, pairs=a.pairs)
         if s >= a.warmup:
             per_step.append(time.perf_counter() - t0)
     val = cb["value"]
@@ -204,7 +205,8 @@ def main():
     d_nodes = torch.from_numpy(orders.order_nodes).to(dev)
     stream = torch.cuda.current_stream()
 
-    plan0 = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream)
+    rflags = wr.WR_ROUTE_PAIRS if a.pairs else 0
+    plan0 = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, flags=rflags)
     info = plan0.info
     n_my = info.order_hi - info.order_lo
     d_res = torch.empty((max(n_my, 1), wr.RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
@@ -221,13 +223,14 @@ def main():
 
     def step():
         if world == 1:
-            _, st = wr.route_orders(G, d_ptr, d_nodes, m=a.m, results=d_res, stream=stream, pred_out=pred_buf)
+            _, st = wr.route_orders(G, d_ptr, d_nodes, m=a.m, results=d_res, stream=stream, pred_out=pred_buf,
+                                    flags=rflags)
             launches[0] += st.kernel_launches
             bf_ms[0] += st.bf_ms
             relax[0] += st.relaxations
             row_bits[0] = st.row_bits
             return
-        p = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, pred_out=pred_buf)
+        p = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, pred_out=pred_buf, flags=rflags)
         s1 = p.local(send)
         dist.all_gather_into_tensor(gathered, send)
         _, s2 = p.finish(gathered, results=d_res)
@@ -275,10 +278,10 @@ def main():
 
         def e2e_step():
             if world == 1:
-                wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream,
+                wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream, flags=rflags,
                                 pred_out=pred_buf)
                 return
-            p = wr.OrdersPlan(G, h_ptr.numpy(), h_nodes.numpy(), rank, world, m=a.m, stream=stream,
+            p = wr.OrdersPlan(G, h_ptr.numpy(), h_nodes.numpy(), rank, world, m=a.m, stream=stream, flags=rflags,
                               pred_out=pred_buf)
             p.local(send)
             dist.all_gather_into_tensor(gathered, send)
@@ -339,6 +342,7 @@ def main():
         "vs_baseline": None, "dtype": a.wtype, "data": "synthetic",
         "config": {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]", "orders": B,
                    "sources": S, "V": g.V, "E": E, "m": a.m, "pred": not a.no_pred,
+                   "stitch": "boundary pairs (NEXT-1)" if a.pairs else ("paper O7" if a.m >= 2 else "exact"),
                    "bf_rows": ("packed u16x2, exact (15-bit bound checked per tile, else a 32-bit redo); "
                                "outputs int32") if rb == 16 else "32-bit",
                    "l2": "working set (dist rows 4*V*S = %.1f GB) >> 126 MB L2; no flush needed" % (4 * g.V * S / 1e9)},
@@ -361,7 +365,7 @@ def main():
         "e2e": e2e,
     }
     if not a.no_cpu and world == 1:   # rank 0 at N=1 only
-        line["cpu_baseline"] = cpu_baseline(g, orders, a.cpu_seconds, S)
+        line["cpu_baseline"] = cpu_baseline(g, orders, a.cpu_seconds, S, m=a.m, pairs=a.pairs)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

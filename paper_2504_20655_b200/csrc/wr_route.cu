@@ -571,9 +571,6 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
                                       const RouteProblem *probs, const uint32_t *Dall, const int *stops,
                                       int64_t o_lo, wr_route_result *out, unsigned long long *counters, int pairs) {
     __shared__ uint32_t sD[4][DSTRIDE];
-    // boundary-pair mode: best (cost key << 32 | local lexicographic rank)
-    // per (segment, first, last), then the path as a nibble sequence
-    __shared__ unsigned long long sPair[4][WR_MAX_SEGMENTS][PAIRS_MAX_SEG][PAIRS_MAX_SEG];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t t = (int64_t)blockIdx.x * 4 + warp;
     if (t >= nord) return;
@@ -591,6 +588,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         if (lane == 0) out[t] = res;
         return;
     }
+    if (pairs && R.mseg >= 2) return;   // route_pairs_kernel writes these orders
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     uint32_t *Ds = sD[warp];
     for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
@@ -598,110 +596,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     uint64_t final_seq = 0;
     uint32_t final_cost = 0;
     unsigned long long perms = 0;
-    if (pairs && R.mseg >= 2) {
-        // NEXT-1 boundary-pair stitch (oracle: orc_segmented_pairs_route).
-        // 1. per segment, every local order (lexicographic rank r) is costed
-        //    left to right; its (first, last) bin keeps the smallest
-        //    (cost key, r) - ties -> the lexicographically smallest order
-        const int m = R.mseg;
-        unsigned long long(*tab)[PAIRS_MAX_SEG][PAIRS_MAX_SEG] = sPair[warp];
-        for (int k = 0; k < m; ++k)
-            for (int e = lane; e < PAIRS_MAX_SEG * PAIRS_MAX_SEG; e += 32)
-                tab[k][e / PAIRS_MAX_SEG][e % PAIRS_MAX_SEG] = ~0ull;
-        __syncwarp();
-        for (int k = 0; k < m; ++k) {
-            const int nj = R.seglen[k];
-            if (nj < 2) continue;
-            const int64_t nf = fact(nj);
-            perms += (unsigned long long)nf;
-            for (int64_t r = lane; r < nf; r += 32) {
-                const uint64_t loc = unrank_nib(r, nj);
-                int prev = nib(R.segmap[k], nib(loc, 0));
-                const int nx = nib(R.segmap[k], nib(loc, 1));
-                uint32_t cost = Ds[prev * MS + nx];
-                prev = nx;
-                for (int a = 2; a < nj; ++a) {
-                    const int x = nib(R.segmap[k], nib(loc, a));
-                    cost = C::add(cost, Ds[prev * MS + x]);
-                    prev = x;
-                }
-                const unsigned long long key = ((unsigned long long)C::key(cost) << 32) | (unsigned long long)r;
-                atomicMin(&tab[k][nib(loc, 0)][nib(loc, nj - 1)], key);
-            }
-        }
-        __syncwarp();
-        // 2. the kept path of every pair as a nibble sequence of order stops
-        for (int k = 0; k < m; ++k) {
-            const int nj = R.seglen[k];
-            for (int e = lane; e < nj * nj; e += 32) {
-                const int a = e / nj, b = e % nj;
-                uint64_t g = 0;
-                if (nj == 1) {
-                    g = R.segmap[k];
-                } else if (a != b) {
-                    const uint64_t loc = unrank_nib((int64_t)(uint32_t)tab[k][a][b], nj);
-                    for (int t2 = 0; t2 < nj; ++t2) g |= (uint64_t)nib(R.segmap[k], nib(loc, t2)) << (4 * t2);
-                }
-                tab[k][a][b] = g;
-            }
-        }
-        __syncwarp();
-        // 3. stitch: segment order x one endpoint pair per segment, full
-        //    left-to-right recompute, ties -> lexicographically smallest
-        int np[WR_MAX_SEGMENTS];
-        int64_t P = 1;
-        for (int k = 0; k < m; ++k) {
-            const int nj = R.seglen[k];
-            np[k] = nj >= 2 ? nj * (nj - 1) : 1;
-            P *= np[k];
-        }
-        const int64_t ncand = fact(m) * P;
-        uint32_t best_key = 0xffffffffu;
-        uint64_t best_seq = ~0ull;
-        for (int64_t c = lane; c < ncand; c += 32) {
-            const uint64_t tau = unrank_nib(c / P, m);
-            int64_t rest = c % P;
-            uint64_t seq = 0;
-            int pos = 0;
-            for (int k = m - 1; k >= 0; --k) {   // mixed radix, last segment fastest
-                const int j = nib(tau, k);
-                const int nj = R.seglen[j];
-                const int p = (int)(rest % np[j]);
-                rest /= np[j];
-                int a = 0, b = 0;
-                if (nj >= 2) {
-                    a = p / (nj - 1);
-                    b = p % (nj - 1);
-                    b += b >= a;
-                }
-                // place segment k's path at its position: positions are
-                // filled right to left (segments k+1.. already placed)
-                pos += nj;
-                seq |= tab[j][a][b] << (4 * (n - pos));
-            }
-            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
-            for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
-            const uint32_t key = C::key(cost);
-            uint64_t lex = 0;
-            for (int a = 0; a < n; ++a) lex |= (uint64_t)nib(seq, a) << (4 * (15 - a));
-            if (key < best_key || (key == best_key && lex < best_seq)) {
-                best_key = key;
-                best_seq = lex;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
-            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
-            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
-                best_key = k2;
-                best_seq = s2;
-            }
-        }
-        final_cost = C::unkey(best_key);
-        for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
-        if (lane == 0) atomicAdd(&counters[1], (unsigned long long)ncand);
-    } else {
+    {
     // each segment's best route as a nibble sequence of order-stop indices
     uint64_t segseq[WR_MAX_SEGMENTS];
     int pi = R.prob0;
@@ -785,6 +680,165 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         for (int a = 0; a < n; ++a) res.seq[a] = s[nib(final_seq, a)];
         out[t] = res;
         atomicAdd(&counters[0], perms);
+    }
+}
+
+// NEXT-1 boundary-pair stitch (WR_ROUTE_PAIRS; oracle:
+// orc_segmented_pairs_route): one block per order, so a segment of up to 9
+// stops (9! local orders) is enumerated by PAIRS_THREADS threads.
+constexpr int PAIRS_THREADS = 256;
+template <class C>
+__global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord, const OrderRoute *ordr,
+                                                                    const uint32_t *Dall, const int *stops,
+                                                                    int64_t o_lo, wr_route_result *out,
+                                                                    unsigned long long *counters) {
+    __shared__ uint32_t Ds[DSTRIDE];
+    // best (cost key << 32 | local lexicographic rank) per (segment, first,
+    // last), then the kept path as a nibble sequence of order stops
+    __shared__ unsigned long long sPair[WR_MAX_SEGMENTS][PAIRS_MAX_SEG][PAIRS_MAX_SEG];
+    __shared__ uint32_t sBestKey[PAIRS_THREADS / 32];
+    __shared__ uint64_t sBestSeq[PAIRS_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t = blockIdx.x;
+    if (t >= nord) return;
+    const OrderRoute R = ordr[t];
+    if (R.status != WR_OK || R.mseg < 2) return;   // route_finalize_kernel writes these
+    const int n = R.n;
+    const int *s = stops + (o_lo + t) * MS;
+    const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+    for (int e = tid; e < DSTRIDE; e += PAIRS_THREADS) Ds[e] = D[e];
+    unsigned long long perms = 0;
+    {
+        // NEXT-1 boundary-pair stitch (oracle: orc_segmented_pairs_route).
+        // 1. per segment, every local order (lexicographic rank r) is costed
+        //    left to right; its (first, last) bin keeps the smallest
+        //    (cost key, r) - ties -> the lexicographically smallest order
+        const int m = R.mseg;
+        unsigned long long(*tab)[PAIRS_MAX_SEG][PAIRS_MAX_SEG] = sPair;
+        for (int k = 0; k < m; ++k)
+            for (int e = tid; e < PAIRS_MAX_SEG * PAIRS_MAX_SEG; e += PAIRS_THREADS)
+                tab[k][e / PAIRS_MAX_SEG][e % PAIRS_MAX_SEG] = ~0ull;
+        __syncthreads();
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            if (nj < 2) continue;
+            const int64_t nf = fact(nj);
+            perms += (unsigned long long)nf;
+            for (int64_t r = tid; r < nf; r += PAIRS_THREADS) {
+                const uint64_t loc = unrank_nib(r, nj);
+                int prev = nib(R.segmap[k], nib(loc, 0));
+                const int nx = nib(R.segmap[k], nib(loc, 1));
+                uint32_t cost = Ds[prev * MS + nx];
+                prev = nx;
+                for (int a = 2; a < nj; ++a) {
+                    const int x = nib(R.segmap[k], nib(loc, a));
+                    cost = C::add(cost, Ds[prev * MS + x]);
+                    prev = x;
+                }
+                const unsigned long long key = ((unsigned long long)C::key(cost) << 32) | (unsigned long long)r;
+                atomicMin(&tab[k][nib(loc, 0)][nib(loc, nj - 1)], key);
+            }
+        }
+        __syncthreads();
+        // 2. the kept path of every pair as a nibble sequence of order stops
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            for (int e = tid; e < nj * nj; e += PAIRS_THREADS) {
+                const int a = e / nj, b = e % nj;
+                uint64_t g = 0;
+                if (nj == 1) {
+                    g = R.segmap[k];
+                } else if (a != b) {
+                    const uint64_t loc = unrank_nib((int64_t)(uint32_t)tab[k][a][b], nj);
+                    for (int t2 = 0; t2 < nj; ++t2) g |= (uint64_t)nib(R.segmap[k], nib(loc, t2)) << (4 * t2);
+                }
+                tab[k][a][b] = g;
+            }
+        }
+        __syncthreads();
+        // 3. stitch: segment order x one endpoint pair per segment, full
+        //    left-to-right recompute, ties -> lexicographically smallest
+        int np[WR_MAX_SEGMENTS];
+        uint32_t P = 1;   // <= PAIRS_MAX_CAND: 32-bit index arithmetic
+        for (int k = 0; k < m; ++k) {
+            const int nj = R.seglen[k];
+            np[k] = nj >= 2 ? nj * (nj - 1) : 1;
+            P *= (uint32_t)np[k];
+        }
+        const uint32_t ncand = (uint32_t)fact(m) * P;
+        uint32_t best_key = 0xffffffffu;
+        uint64_t best_seq = ~0ull;
+        for (uint32_t c = tid; c < ncand; c += PAIRS_THREADS) {
+            const uint64_t tau = unrank_nib((int64_t)(c / P), m);
+            uint32_t rest = c % P;
+            uint64_t seq = 0;
+            int pos = 0;
+            for (int k = m - 1; k >= 0; --k) {   // mixed radix, last segment fastest
+                const int j = nib(tau, k);
+                const int nj = R.seglen[j];
+                const int p = (int)(rest % (uint32_t)np[j]);
+                rest /= (uint32_t)np[j];
+                int a = 0, b = 0;
+                if (nj >= 2) {
+                    a = p / (nj - 1);
+                    b = p % (nj - 1);
+                    b += b >= a;
+                }
+                // place segment k's path at its position: positions are
+                // filled right to left (segments k+1.. already placed)
+                pos += nj;
+                seq |= tab[j][a][b] << (4 * (n - pos));
+            }
+            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
+            for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
+            const uint32_t key = C::key(cost);
+            uint64_t lex = 0;
+            for (int a = 0; a < n; ++a) lex |= (uint64_t)nib(seq, a) << (4 * (15 - a));
+            if (key < best_key || (key == best_key && lex < best_seq)) {
+                best_key = key;
+                best_seq = lex;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
+            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
+            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
+                best_key = k2;
+                best_seq = s2;
+            }
+        }
+        if (lane == 0) {
+            sBestKey[warp] = best_key;
+            sBestSeq[warp] = best_seq;
+        }
+        __syncthreads();
+        if (tid != 0) return;
+        for (int w2 = 1; w2 < PAIRS_THREADS / 32; ++w2)
+            if (sBestKey[w2] < best_key || (sBestKey[w2] == best_key && sBestSeq[w2] < best_seq)) {
+                best_key = sBestKey[w2];
+                best_seq = sBestSeq[w2];
+            }
+        const uint32_t final_cost = C::unkey(best_key);
+        uint64_t final_seq = 0;
+        for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
+        atomicAdd(&counters[1], (unsigned long long)ncand);
+        int64_t rank = 0;   // Lehmer rank of the final sequence among the n! orders
+        for (int a = 0; a < n; ++a) {
+            int smaller = 0;
+            for (int b2 = a + 1; b2 < n; ++b2) smaller += nib(final_seq, b2) < nib(final_seq, a);
+            rank += smaller * fact(n - 1 - a);
+        }
+        wr_route_result res;
+        res.n = n;
+        res.status = WR_OK;
+        res.m_used = m;
+        res.rank = rank;
+        res.cost_bits = final_cost;
+        for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[nib(final_seq, a)] : -1;
+        out[t] = res;
+        atomicAdd(&counters[0], perms);
+
     }
 }
 
@@ -1161,6 +1215,12 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
                                                              o_lo, d_res, d_counters, P.pairs);
     count_launch();
     WR_LAUNCH_CHECK();
+    if (P.pairs) {
+        route_pairs_kernel<C><<<(unsigned)nord, PAIRS_THREADS, 0, st>>>(nord, ordr.p, Dall, P.stops.p, o_lo, d_res,
+                                                                      d_counters);
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
     WR_CUDA(cudaStreamSynchronize(st));   // temporaries are freed on return
 }
 
