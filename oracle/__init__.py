@@ -52,6 +52,7 @@ def lib():
         L.orc_exact_route_chunked.argtypes = [C.c_int, vp, C.c_int, C.c_longlong, vp, vp, lp, lp]
         L.orc_segmented_route.argtypes = [C.c_int, vp, C.c_int, vp, vp, vp, vp]
         L.orc_segmented_pairs_route.argtypes = [C.c_int, vp, C.c_int, vp, vp, vp, vp]
+        L.orc_held_karp_route.argtypes = [C.c_int, vp, C.c_int, vp, vp, vp]
         L.orc_kmeans.argtypes = [vp, C.c_int, C.c_int, vp]
         L.orc_order_stops.argtypes = [vp, C.c_int, vp]
         L.orc_perm_rank.argtypes = [vp, C.c_int]
@@ -167,6 +168,19 @@ def exact_route(D):
     rc = lib().orc_exact_route(wt, _p(D), n, _p(seq), _p(cost), C.byref(rank))
     if rc:
         raise OracleError(rc, "exact_route")
+    return cost[0], rank.value, seq
+
+
+def held_karp_route(D):
+    """NEXT-2: exact route of up to 16 stops by the Held-Karp subset DP:
+    (cost, rank, seq), the same result as exact_route."""
+    D, wt, n = _D(D)
+    seq = np.zeros(n, dtype=np.int32)
+    cost = np.zeros(1, dtype=_vdt(wt))
+    rank = C.c_longlong(0)
+    rc = lib().orc_held_karp_route(wt, _p(D), n, _p(seq), _p(cost), C.byref(rank))
+    if rc:
+        raise OracleError(rc, "held_karp_route")
     return cost[0], rank.value, seq
 
 

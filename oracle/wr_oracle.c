@@ -35,6 +35,10 @@
  *                     pinned: m=1 == exact, singletons == exact, and for int
  *                     weights == (min cost, lex-smallest) over ALL segment-
  *                     contiguous orders by brute force; int cost <= O7's.
+ *   orc_held_karp_route  NEXT-2 exact route for 13-16 stops (subset DP,
+ *                     P370 §3) pinned: == O5 enumeration (cost, order, rank)
+ *                     on n <= 9 incl. tie-heavy matrices; cost == the tests'
+ *                     independent Python Held-Karp for n up to 14.
  *   orc_kmeans        O8 deterministic integer K-means   pinned: hand-made
  *                     separated clusters, brute-force Lloyd fixpoint check.
  *   orc_order_stops   a2 stop projection (P226-238 §2.4) pinned: numpy unique.
@@ -345,6 +349,101 @@ int orc_exact_route(int wtype, const void *D, int n, int *seq_out, void *cost_ou
                     long long *rank_out)
 {
     return orc_exact_route_range(wtype, D, n, 0, factorial(n), seq_out, cost_out, rank_out);
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2 exact route for up to 16 stops by the Held-Karp subset DP (the     */
+/* paper mentions Held-Karp O(n^2 2^n) as the exact-TSP alternative, P370   */
+/* §3; reading R2 in DESIGN.md). Same result as O5:     */
+/* the minimum left-to-right cost over all n! orders, ties -> the           */
+/* lexicographically smallest order:                                        */
+/*  state (S, j) = orders of the stop set S ending at j; it keeps the        */
+/*  cheapest prefix cost (left to right: fl(prefix + D[i][j]), which is     */
+/*  monotone in the prefix, so the minimum of the left-to-right sums is     */
+/*  exact - reading A16) and, among equal costs, the lexicographically      */
+/*  smallest prefix (equal suffixes keep that order). Prefixes are kept as  */
+/*  nibble keys, first stop in the most significant nibble.                 */
+/*  final = min over j of (cost(all, j), key).                              */
+/* int sums in int64 (INF leg -> INF); a finite result outside int32 ->     */
+/* ORC_EOVERFLOW.                                                           */
+/* ------------------------------------------------------------------------ */
+int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cost_out,
+                        long long *rank_out)
+{
+    if (n < 1 || n > 16) return ORC_EINVAL;
+    if (n == 1) {
+        seq_out[0] = 0;
+        memset(cost_out, 0, 4);
+        *rank_out = 0;
+        return ORC_OK;
+    }
+    const size_t NS = (size_t)1 << n;
+    const int64_t IINF = INT64_MAX / 4;
+    int64_t *ci = NULL;
+    float *cf = NULL;
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * NS * (size_t)n);
+    char *have = (char *)calloc(NS * (size_t)n, 1);
+    if (wtype == ORC_I32) ci = (int64_t *)malloc(sizeof(int64_t) * NS * (size_t)n);
+    else cf = (float *)malloc(sizeof(float) * NS * (size_t)n);
+    if (!key || !have || (!ci && !cf)) { free(key); free(have); free(ci); free(cf); return ORC_ENOMEM; }
+    for (int j = 0; j < n; ++j) {
+        const size_t st = ((size_t)1 << j) * n + j;
+        have[st] = 1;
+        key[st] = (uint64_t)j << 60;
+        if (ci) ci[st] = 0; else cf[st] = 0.0f;
+    }
+    for (size_t S = 1; S < NS; ++S) {
+        const int k = __builtin_popcountll((unsigned long long)S);
+        if (k < 2) continue;
+        for (int j = 0; j < n; ++j) {
+            if (!((S >> j) & 1)) continue;
+            const size_t P = S & ~((size_t)1 << j);
+            const size_t st = S * n + j;
+            for (int i = 0; i < n; ++i) {
+                if (!((P >> i) & 1) || !have[P * n + i]) continue;
+                const uint64_t kk = key[P * n + i] | ((uint64_t)j << (4 * (15 - (k - 1))));
+                int better;
+                if (ci) {
+                    const int leg = ((const int *)D)[(size_t)i * n + j];
+                    const int64_t pre = ci[P * n + i];
+                    const int64_t c = (leg == I32_INF || pre >= IINF) ? IINF : (k == 2 ? (int64_t)leg : pre + leg);
+                    better = !have[st] || c < ci[st] || (c == ci[st] && kk < key[st]);
+                    if (better) ci[st] = c;
+                } else {
+                    const float leg = ((const float *)D)[(size_t)i * n + j];
+                    const float c = k == 2 ? leg : cf[P * n + i] + leg;
+                    better = !have[st] || c < cf[st] || (c == cf[st] && kk < key[st]);
+                    if (better) cf[st] = c;
+                }
+                if (better) { have[st] = 1; key[st] = kk; }
+            }
+        }
+    }
+    const size_t F = NS - 1;
+    int bj = -1;
+    for (int j = 0; j < n; ++j) {
+        const size_t st = F * n + j;
+        if (!have[st]) continue;
+        int better;
+        if (bj < 0) better = 1;
+        else if (ci) better = ci[st] < ci[F * n + bj] || (ci[st] == ci[F * n + bj] && key[st] < key[F * n + bj]);
+        else better = cf[st] < cf[F * n + bj] || (cf[st] == cf[F * n + bj] && key[st] < key[F * n + bj]);
+        if (better) bj = j;
+    }
+    const uint64_t kb = key[F * n + bj];
+    for (int a = 0; a < n; ++a) seq_out[a] = (int)((kb >> (4 * (15 - a))) & 0xf);
+    int rc = ORC_OK;
+    if (ci) {
+        const int64_t c = ci[F * n + bj];
+        if (c >= IINF) *(int *)cost_out = I32_INF;
+        else if (c >= I32_INF || c < INT32_MIN) rc = ORC_EOVERFLOW;
+        else *(int *)cost_out = (int)c;
+    } else {
+        *(float *)cost_out = cf[F * n + bj];
+    }
+    *rank_out = orc_perm_rank(seq_out, n);
+    free(key); free(have); free(ci); free(cf);
+    return rc;
 }
 
 /* O6 combine: chunks of <= C permutations, (cost, rank) lexicographic min. */
@@ -729,7 +828,8 @@ static void *route_worker(void *arg)
         char cost[4];
         long long rank = 0;
         if (j->m <= 1) {
-            rc = orc_exact_route(j->wtype, D, n, seq, cost, &rank);
+            if (n > 12) rc = orc_held_karp_route(j->wtype, D, n, seq, cost, &rank);   /* NEXT-2 */
+            else rc = orc_exact_route(j->wtype, D, n, seq, cost, &rank);
         } else {
             int labels[32], xy[64];
             if (j->labels_in) {

@@ -273,6 +273,42 @@ def test_segmented_invariants(kind):
         assert np.asarray(oracle.route_cost(D, s)).tobytes() == np.asarray(c).tobytes()
 
 
+# ---------------------------------------------------------------- NEXT-2 Held-Karp exact
+@pytest.mark.parametrize("kind", ["int", "int_ties", "fp32"])
+def test_held_karp_equals_enumeration(kind):
+    """The subset DP returns exactly O5's result (cost bits, lexicographic
+    argmin, rank) - including matrices with many equal-cost orders."""
+    rng = np.random.default_rng(81)
+    for trial in range(60):
+        n = int(rng.integers(1, 10))
+        if kind == "int_ties":
+            D = rng.integers(0, 3, (n, n)).astype(np.int32)
+            np.fill_diagonal(D, 0)
+        else:
+            D = random_D(rng, n, kind)
+        ec, er, es = oracle.exact_route(D)
+        hc, hr, hs = oracle.held_karp_route(D)
+        assert np.asarray(hc).tobytes() == np.asarray(ec).tobytes()
+        assert hs.tolist() == es.tolist() and hr == er
+
+
+def test_held_karp_large_vs_independent_dp():
+    """n = 12..13 (beyond cheap enumeration): cost equals the tests' own
+    Held-Karp; the int order equals the independent suffix-DP lexicographic
+    argmin; the worked example gives 17, (0,2,1,3,4), rank 6."""
+    rng = np.random.default_rng(82)
+    for n, kind in ((12, "int"), (13, "int"), (12, "fp32")):
+        D = random_D(rng, n, kind)
+        hc, hr, hs = oracle.held_karp_route(D)
+        assert np.asarray(hc).tobytes() == np.asarray(held_karp(D)).tobytes()
+        if kind == "int":
+            c2, s2 = lex_argmin_int(D)
+            assert int(hc) == c2 and hs.tolist() == list(s2)
+    D = load_three_aisle()["D"]
+    hc, hr, hs = oracle.held_karp_route(D)
+    assert int(hc) == 17 and hs.tolist() == [0, 2, 1, 3, 4] and hr == 6
+
+
 # ---------------------------------------------------------------- NEXT-1 boundary pairs
 def _contiguous_best(D, labels):
     """Brute force over ALL n! orders keeping those in which every segment's
