@@ -54,7 +54,9 @@ typedef int32_t wr_status;
 #define WR_CSR 1           /* arcs given as out-adjacency row_ptr[V+1], col[E] */
 
 #define WR_MAX_STOPS 16    /* stops per order (distinct location nodes)      */
-#define WR_MAX_EXACT 12    /* stops of one exhaustively routed (sub)problem  */
+#define WR_MAX_EXACT 12    /* stops of one exhaustively routed (sub)problem; */
+                           /* exact orders of 13-16 stops use the Held-Karp  */
+                           /* subset DP instead (same result, DESIGN R2)     */
 #define WR_MAX_SEGMENTS 6  /* segments stitched per order (m'! 2^m' candidates) */
 #define WR_DEFAULT_CHUNK 2903040LL /* permutations per chunk, P658 §4.6      */
 

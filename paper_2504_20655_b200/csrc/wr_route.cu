@@ -435,6 +435,8 @@ struct OrderRoute {        // per-order routing state (device)
     int nprob;
     uint64_t segmap[WR_MAX_SEGMENTS];  // nibble map of each segment's stops
     int seglen[WR_MAX_SEGMENTS];
+    int hk;                // exact route of 13-16 stops by route_hk_kernel (NEXT-2)
+    int noenum;            // no enumeration problems (Held-Karp or boundary-pair stitch)
 };
 
 template <class C>
@@ -445,7 +447,7 @@ template <class C>
 __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
                                      int64_t nord, const uint32_t *Dall, int m, const int *xy,
                                      const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
-                                     int *item_cnt, int pairs) {
+                                     int *item_cnt, int pairs, int *hk_count) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nord) return;
     const int64_t o = o_lo + t;
@@ -455,6 +457,8 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
     R.mseg = 1;
     R.prob0 = 0;
     R.nprob = 0;
+    R.hk = 0;
+    R.noenum = 0;
     int nitems = 0;
     const int n = R.n;
     if (R.status == WR_OK) {
@@ -499,6 +503,13 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 R.segmap[k] |= (uint64_t)i << (4 * R.seglen[k]);
                 R.seglen[k]++;
             }
+            if (nseg == 1 && n > WR_MAX_EXACT) {
+                // exact route of 13-16 stops: Held-Karp subset DP (NEXT-2)
+                R.hk = 1;
+                R.noenum = 1;
+                nseg = 0;
+                atomicAdd(hk_count, 1);
+            }
             if (pairs && nseg >= 2) {
                 // boundary-pair stitch (NEXT-1): per-segment orders and the
                 // stitch run in the finalize warp; limits as the oracle's
@@ -509,6 +520,7 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                     ncand *= nj >= 2 ? (int64_t)nj * (nj - 1) : 1;
                 }
                 if (ncand > PAIRS_MAX_CAND) R.status = WR_ETOOLARGE;
+                R.noenum = 1;
                 nseg = 0;   // no enumeration problems
             }
             for (int k = 0; k < nseg; ++k) {
@@ -537,7 +549,7 @@ __global__ void route_emit_kernel(int64_t nord, OrderRoute *ordr, const int *pro
     if (t >= nord) return;
     OrderRoute &R = ordr[t];
     R.prob0 = prob_off[t];
-    if (R.status != WR_OK) return;
+    if (R.status != WR_OK || R.noenum) return;   // counted no problems (prepare)
     int pi = prob_off[t], ii = item_off[t];
     for (int k = 0; k < R.mseg; ++k) {
         const int nj = R.seglen[k];
@@ -589,6 +601,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         return;
     }
     if (pairs && R.mseg >= 2) return;   // route_pairs_kernel writes these orders
+    if (R.hk) return;                   // route_hk_kernel writes these orders
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     uint32_t *Ds = sD[warp];
     for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
@@ -839,6 +852,134 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
         out[t] = res;
         atomicAdd(&counters[0], perms);
 
+    }
+}
+
+// NEXT-2 exact route for 13-16 stops (oracle: orc_held_karp_route, reading
+// R2): Held-Karp subset DP. State (S, j) = the stop set S visited, ending at
+// j: cheapest left-to-right prefix cost (fl(prefix + D[i][j]) is monotone in
+// the prefix, so the minimum is exact) and, among equal costs, the
+// lexicographically smallest prefix as a nibble key (first stop most
+// significant). Persistent blocks, one order at a time per block, each with
+// its own global state table (2^16 x 16 costs + keys = 12 MB); the subset
+// layers |S| = 2..n are separated by block barriers.
+constexpr int HK_THREADS = 256;
+constexpr int HK_MAX = WR_MAX_STOPS;
+template <class C>
+__global__ void __launch_bounds__(HK_THREADS) route_hk_kernel(int64_t nord, const OrderRoute *ordr,
+                                                              const uint32_t *Dall, const int *stops, int64_t o_lo,
+                                                              wr_route_result *out, unsigned long long *counters,
+                                                              int *next_order, uint32_t *cost_ws,
+                                                              unsigned long long *key_ws) {
+    __shared__ uint32_t Ds[DSTRIDE];
+    __shared__ int s_t;
+    __shared__ uint32_t sBestKey[HK_THREADS / 32];
+    __shared__ unsigned long long sBestSeq[HK_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t *cost = cost_ws + (size_t)blockIdx.x * ((size_t)1 << HK_MAX) * HK_MAX;
+    unsigned long long *key = key_ws + (size_t)blockIdx.x * ((size_t)1 << HK_MAX) * HK_MAX;
+    for (;;) {
+        if (tid == 0) s_t = atomicAdd(next_order, 1);
+        __syncthreads();
+        const int64_t t = s_t;
+        if (t >= nord) break;
+        const OrderRoute R = ordr[t];
+        if (R.status != WR_OK || !R.hk) {
+            __syncthreads();
+            continue;
+        }
+        const int n = R.n;
+        const uint32_t NS = 1u << n;
+        const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+        for (int e = tid; e < DSTRIDE; e += HK_THREADS) Ds[e] = D[e];
+        for (int j = tid; j < n; j += HK_THREADS) {
+            const size_t st = (size_t)(1u << j) * n + j;
+            cost[st] = 0u;
+            key[st] = (unsigned long long)j << 60;
+        }
+        __syncthreads();
+        for (int k = 2; k <= n; ++k) {
+            for (uint32_t S = tid; S < NS; S += HK_THREADS) {
+                if (__popc(S) != k) continue;
+                for (int j = 0; j < n; ++j) {
+                    if (!((S >> j) & 1u)) continue;
+                    const uint32_t P = S & ~(1u << j);
+                    uint32_t bc = 0, bk = 0;
+                    unsigned long long bkey = 0;
+                    bool have = false;
+                    for (int i = 0; i < n; ++i) {
+                        if (!((P >> i) & 1u)) continue;
+                        const uint32_t leg = Ds[i * MS + j];
+                        const uint32_t c = k == 2 ? leg : C::add(cost[(size_t)P * n + i], leg);
+                        const uint32_t ck = C::key(c);
+                        const unsigned long long kk =
+                            key[(size_t)P * n + i] | ((unsigned long long)j << (4 * (15 - (k - 1))));
+                        if (!have || ck < bk || (ck == bk && kk < bkey)) {
+                            have = true;
+                            bc = c;
+                            bk = ck;
+                            bkey = kk;
+                        }
+                    }
+                    cost[(size_t)S * n + j] = bc;
+                    key[(size_t)S * n + j] = bkey;
+                }
+            }
+            __syncthreads();
+        }
+        // final: min over the last stop j of (cost key, order key)
+        uint32_t best_key = 0xffffffffu;
+        unsigned long long best_seq = ~0ull;
+        const uint32_t F = NS - 1;
+        for (int j = tid; j < n; j += HK_THREADS) {
+            const uint32_t ck = C::key(cost[(size_t)F * n + j]);
+            const unsigned long long kk = key[(size_t)F * n + j];
+            if (ck < best_key || (ck == best_key && kk < best_seq)) {
+                best_key = ck;
+                best_seq = kk;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
+            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
+            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
+                best_key = k2;
+                best_seq = s2;
+            }
+        }
+        if (lane == 0) {
+            sBestKey[warp] = best_key;
+            sBestSeq[warp] = best_seq;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w2 = 1; w2 < HK_THREADS / 32; ++w2)
+                if (sBestKey[w2] < best_key || (sBestKey[w2] == best_key && sBestSeq[w2] < best_seq)) {
+                    best_key = sBestKey[w2];
+                    best_seq = sBestSeq[w2];
+                }
+            const int *s = stops + (o_lo + t) * MS;
+            wr_route_result res;
+            res.n = n;
+            res.status = WR_OK;
+            res.m_used = 1;
+            res.cost_bits = C::unkey(best_key);
+            int64_t rank = 0;   // Lehmer rank among the n! orders
+            int seq[MS];
+            for (int a = 0; a < n; ++a) seq[a] = (int)((best_seq >> (4 * (15 - a))) & 0xf);
+            for (int a = 0; a < n; ++a) {
+                int smaller = 0;
+                for (int b = a + 1; b < n; ++b) smaller += seq[b] < seq[a];
+                rank += smaller * fact(n - 1 - a);
+            }
+            res.rank = rank;
+            for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[seq[a]] : -1;
+            out[t] = res;
+            // work: states x predecessors = sum over S, j in S of |S| - 1
+            atomicAdd(&counters[0], (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
+        }
+        __syncthreads();
     }
 }
 
@@ -1183,19 +1324,22 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     if (nord <= 0) return;
     const int *xy = P.g->xy.p;
     DBuf<OrderRoute> ordr(nord);
-    DBuf<int> pcnt(nord + 1), icnt(nord + 1);
+    DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(2);
     WR_CUDA(cudaMemsetAsync(pcnt.p + nord, 0, 4, st));
     WR_CUDA(cudaMemsetAsync(icnt.p + nord, 0, 4, st));
+    WR_CUDA(cudaMemsetAsync(hk_ctr.p, 0, 8, st));
     route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
         P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
-        P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs);
+        P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs,
+        hk_ctr.p);
     count_launch();
     WR_LAUNCH_CHECK();
     scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
     scan_exclusive_i32(icnt.p, icnt.p, (int)(nord + 1), st);
-    int nprob = 0, nitems = 0;
+    int nprob = 0, nitems = 0, nhk = 0;
     WR_CUDA(cudaMemcpyAsync(&nprob, pcnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaMemcpyAsync(&nitems, icnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaMemcpyAsync(&nhk, hk_ctr.p, 4, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
     DBuf<RouteProblem> probs(std::max(nprob, 1));
     DBuf<RouteWorkItem> items(std::max(nitems, 1));
@@ -1220,6 +1364,19 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
                                                                       d_counters);
         count_launch();
         WR_LAUNCH_CHECK();
+    }
+    if (nhk > 0) {   // 13-16-stop exact routes: persistent Held-Karp blocks, 12 MB of states each
+        int nsm = 0;
+        WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.device));
+        const int nblk = std::min(nhk, 2 * nsm);
+        const size_t states = (size_t)1 << HK_MAX;
+        DBuf<uint32_t> hk_cost((size_t)nblk * states * HK_MAX);
+        DBuf<unsigned long long> hk_key((size_t)nblk * states * HK_MAX);
+        route_hk_kernel<C><<<nblk, HK_THREADS, 0, st>>>(nord, ordr.p, Dall, P.stops.p, o_lo, d_res, d_counters,
+                                                        hk_ctr.p + 1, hk_cost.p, hk_key.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+        WR_CUDA(cudaStreamSynchronize(st));   // workspace lifetime
     }
     WR_CUDA(cudaStreamSynchronize(st));   // temporaries are freed on return
 }

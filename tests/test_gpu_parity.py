@@ -251,6 +251,25 @@ def test_route_orders_pairs_config4(wtype):
         assert (a <= b).all() and (a < b).any()
 
 
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_orders_held_karp_13_to_16(wtype):
+    """NEXT-2: exact routes of 13-16 stops (Held-Karp subset DP on the GPU)
+    equal the oracle's (cost bits, order, rank); mixed with <= 12-stop orders
+    routed by enumeration in the same call."""
+    g = gen.config(3, wtype=wtype)[0]
+    rng = np.random.default_rng(91 if wtype == "i32" else 92)
+    sizes = [13, 14, 15, 16, 13, 16, 8, 12, 14, 5, 15, 16]
+    nodes = np.concatenate([np.sort(rng.choice(5000, k, replace=False)) for k in sizes]).astype(np.int32)
+    ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, len(sizes)
+    res, st = compare_orders(g, orders, m=1)
+    assert res["n"].tolist() == sizes
+
+
 def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
     G = G or wr.Graph.from_gen(g)
     res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk, flags=flags) \
