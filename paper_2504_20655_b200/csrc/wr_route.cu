@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
 // significant). Persistent blocks, one order at a time per block, each with
 // its own global state table (2^16 x 16 costs + keys = 12 MB); the subset
 // layers |S| = 2..n are separated by block barriers.
-constexpr int HK_THREADS = 256;
+constexpr int HK_THREADS = 512;
 constexpr int HK_MAX = WR_MAX_STOPS;
 template <class C>
 __global__ void __launch_bounds__(HK_THREADS) route_hk_kernel(int64_t nord, const OrderRoute *ordr,
@@ -1368,7 +1368,7 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     if (nhk > 0) {   // 13-16-stop exact routes: persistent Held-Karp blocks, 12 MB of states each
         int nsm = 0;
         WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.device));
-        const int nblk = std::min(nhk, 2 * nsm);
+        const int nblk = std::min(nhk, 4 * nsm);
         const size_t states = (size_t)1 << HK_MAX;
         DBuf<uint32_t> hk_cost((size_t)nblk * states * HK_MAX);
         DBuf<unsigned long long> hk_key((size_t)nblk * states * HK_MAX);
