@@ -140,6 +140,27 @@ struct Dfs<C, 2> {   // two stops left, a < b: leaves (a, b) then (b, a)
     }
 };
 template <class C>
+struct Dfs<C, 3> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+                                               Best &best, uint32_t &rank) {
+        const int a = __ffs(unused) - 1;
+        const uint32_t u2 = unused & (unused - 1);
+        const int b = __ffs(u2) - 1;
+        const int c = __ffs(u2 & (u2 - 1)) - 1;
+        const uint32_t *Dp = Ds + prev * n, *Da = Ds + a * n, *Db = Ds + b * n, *Dc = Ds + c * n;
+        const uint32_t pa = C::add(cost, Dp[a]), pb = C::add(cost, Dp[b]), pc = C::add(cost, Dp[c]);
+        const uint32_t ab = C::add(pa, Da[b]), ac = C::add(pa, Da[c]);
+        const uint32_t ba = C::add(pb, Db[a]), bc = C::add(pb, Db[c]);
+        const uint32_t ca = C::add(pc, Dc[a]), cb = C::add(pc, Dc[b]);
+        leaf<C>(C::add(ab, Db[c]), best, rank);   // a b c
+        leaf<C>(C::add(ac, Dc[b]), best, rank);   // a c b
+        leaf<C>(C::add(ba, Da[c]), best, rank);   // b a c
+        leaf<C>(C::add(bc, Dc[a]), best, rank);   // b c a
+        leaf<C>(C::add(ca, Da[b]), best, rank);   // c a b
+        leaf<C>(C::add(cb, Db[a]), best, rank);   // c b a
+    }
+};
+template <class C>
 struct Dfs<C, 1> {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
