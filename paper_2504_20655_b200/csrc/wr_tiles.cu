@@ -214,6 +214,11 @@ int balanced_tiles(int64_t n, int tsw, int64_t max_tiles, int &fill) {
 }
 
 int64_t tiles_to_allocate(int64_t sb, int tsw, int64_t extra_bytes, int64_t tile_bytes) {
+    // extra tiles only serve the opt-in balancing; without it the buffer size
+    // must not depend on the budget path (a repeated call then reuses the
+    // cached block instead of growing the pool: 1.7 s for 34 GB)
+    static const bool balance = getenv("WR_TILE_BALANCE") != nullptr;
+    if (!balance) return sb / tsw;
     int nsm = 0, dev = 0;
     WR_CUDA(cudaGetDevice(&dev));
     WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
