@@ -118,19 +118,19 @@ def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
     threads = os.cpu_count() or 1
     stops_all = np.unique(orders.order_nodes)
     # sources: time one batch of `threads` sources, grow until ~seconds/2
-    nsrc = threads
+    nsrc = min(threads, S_total)
     t_bf = None
     while True:
         t0 = time.perf_counter()
         oracle.bf_many(g, stops_all[:nsrc], nthreads=threads)
         dt = time.perf_counter() - t0
         t_bf = dt / nsrc
-        if dt > seconds / 4 or nsrc >= 4 * threads:
+        if dt > seconds / 4 or nsrc >= min(4 * threads, S_total):
             break
-        nsrc *= 2
+        nsrc = min(nsrc * 2, S_total)
     # orders: route a prefix (the oracle BF for their stops is charged above)
     from gen.warehouse import Orders
-    nord = 64
+    nord = min(64, orders.B)
     while True:
         sub = Orders(order_ptr=orders.order_ptr[:nord + 1].copy(),
                      order_nodes=orders.order_nodes[:int(orders.order_ptr[nord])].copy())
@@ -140,9 +140,9 @@ def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
         dt = time.perf_counter() - t0
         assert res["rc"] == 0
         t_route = max(0.0, (dt - t_bf * sstops.size)) / nord
-        if dt > seconds / 2 or nord >= 4096:
+        if dt > seconds / 2 or nord >= min(4096, orders.B):
             break
-        nord *= 4
+        nord = min(nord * 4, orders.B)
     B = orders.B
     t_full = S_total * t_bf + B * t_route
     return {"value": B / t_full, "unit": "orders/s", "cores": threads, "kind": "oracle",
