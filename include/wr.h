@@ -152,7 +152,10 @@ typedef struct {
  *            fixpoint of d[v] = min(d[v], fl(d[u] + w)) (O2)
  *   pred     S x V int32 canonical predecessor (O3) or NULL
  *   stats    optional
- * Errors: WR_EINVAL (bad vertex), WR_ENEGCYCLE, WR_ENOMEM, WR_ECUDA. */
+ * Errors: WR_EINVAL (bad vertex), WR_ENEGCYCLE, WR_ENOMEM, WR_ECUDA,
+ * WR_ETOOLARGE if V exceeds the shared-memory frontier (about 190,000
+ * vertices on a B200: 36 bytes of per-vertex bitmaps, stamps and word lists
+ * per CTA; the same limit applies to wr_route_orders). */
 wr_status wr_bf_batch(const wr_graph *g, const int32_t *sources, int32_t S,
                       const int32_t *targets, int32_t T, void *dist, int32_t *pred,
                       const wr_bf_opts *opts, wr_bf_stats *stats);
