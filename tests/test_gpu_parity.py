@@ -326,6 +326,23 @@ def test_route_orders_edge_cases():
     assert res["status"].tolist() == [0, wr.WR_EUNREACHABLE]
 
 
+def test_frontier_size_limit_and_fallback_shape():
+    """V beyond the shared-memory frontier -> WR_ETOOLARGE (documented in
+    wr.h); V between the default and the fallback launch shape still routes
+    exactly (path graph: dist = prefix sums)."""
+    def path(V):
+        src = np.arange(V - 1, dtype=np.int32)
+        return wr.Graph(V, np.concatenate([src, src + 1]), np.concatenate([src + 1, src]),
+                        np.ones(2 * (V - 1), np.int32))
+    with pytest.raises(wr.WrError) as e:
+        wr.bf_batch(path(250_000), [0], pred=False)
+    assert e.value.code == wr.WR_ETOOLARGE
+    G = path(150_000)
+    d, p, _ = wr.bf_batch(G, [0, 149_999], pred=True)
+    assert d[0].tolist() == list(range(150_000)) and d[1][0] == 149_999
+    assert p[0][1:].tolist() == list(range(149_999)) and p[0][0] == -1
+
+
 def G_disconnected():
     return G(4, [0, 1, 2, 3], [1, 0, 3, 2], np.array([1, 1, 1, 1], np.int32))
 
