@@ -290,6 +290,10 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
 // Task-queue capacity per vertex: per-warp queues of 32 x QC packed (u, w)
 // pairs after the bitmaps in dynamic shared memory.
 constexpr int QCAP = 16;
+#ifndef WR_FUSED_PA
+#define WR_FUSED_PA 2
+#endif
+constexpr int FPA = WR_FUSED_PA;   // in-arcs per vertex per step in the fused pred jobs
 
 template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
@@ -681,7 +685,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 }
             }
             t = __shfl_sync(FULL, t, 0);
-            pred_job<Op, SPL, 1>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
+            pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
                                  (int)(j % chunks) * PV, spw, lane);
         }
     }
