@@ -201,22 +201,6 @@ __device__ __forceinline__ bool vless(const Vec<SPL> &a, const Vec<SPL> &b) {
     return r;
 }
 
-// ------------------------------------------------------------ tile setup --
-__global__ void make_tiles_kernel(const int *sources, int64_t lo, int64_t hi, int *tile_src, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    tile_src[i] = (lo + i < hi) ? sources[lo + i] : -1;
-}
-
-void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_tile_src, cudaStream_t st) {
-    const int64_t ntiles = (hi - lo + tsw - 1) / tsw;
-    const int64_t n = ntiles * tsw;
-    if (n == 0) return;
-    make_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_sources, lo, hi, d_tile_src, n);
-    count_launch();
-    WR_LAUNCH_CHECK();
-}
-
 // ---------------------------------------------------- relaxing one word --
 // Delta pull. In round r+1 a candidate only needs the in-arcs whose tail
 // improved in round r: an in-neighbour that did not change since the

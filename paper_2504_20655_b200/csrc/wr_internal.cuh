@@ -214,17 +214,17 @@ void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int
 void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles,
                      int64_t out_row0, int32_t *pred_out, cudaStream_t st);
 
-// Builds tile_src for sources [lo, hi) of a device source list (tsw slots/tile).
-void make_tiles(const int *d_sources, int64_t lo, int64_t hi, int tsw, int *d_tile_src, cudaStream_t st);
-// Same, with spatially compact tiles (recursive coordinate bisection of the
-// graph's coordinates when present) and a whole number of waves of tiles
-// (<= max_tiles) with the sources spread evenly: slot_row[slot] = source
-// offset in [0, hi-lo) (-1 = empty slot), pos_of[offset] = slot position.
-// Returns the number of tiles (wr_tiles.cu).
+// Builds the tiles for sources [lo, hi) of a device source list: tsw slots
+// per tile, spatially compact (recursive coordinate bisection of the
+// graph's coordinates when present), ceil(n / tsw) full tiles (or, with
+// WR_TILE_BALANCE, a whole number of waves of tiles <= max_tiles):
+// tile_src[slot] = source vertex, slot_row[slot] = source offset in
+// [0, hi-lo) (-1 = empty slot), pos_of[offset] = slot position. Returns the
+// number of tiles (wr_tiles.cu).
 int make_tiles_ordered(const wr_graph *g, const int *d_sources, int64_t lo, int64_t hi, int tsw, int64_t max_tiles,
                        int *tile_src, int *slot_row, int *pos_of, cudaStream_t st);
-// Tiles to allocate for segments of sb sources: sb/tsw, plus up to one wave
-// of extra (partly filled) tiles if extra_bytes allow (tile_bytes each).
+// Tiles to allocate for segments of sb sources: sb/tsw (with WR_TILE_BALANCE
+// plus up to one wave of extra, partly filled tiles if extra_bytes allow).
 int64_t tiles_to_allocate(int64_t sb, int tsw, int64_t extra_bytes, int64_t tile_bytes);
 
 // ------------------------------------------------------------- routing --

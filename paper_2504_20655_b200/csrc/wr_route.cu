@@ -30,7 +30,6 @@ namespace wr {
 
 constexpr int MS = WR_MAX_STOPS;      // 16
 constexpr int DSTRIDE = MS * MS;      // D entries per order (row-major 16 x 16)
-constexpr int TS = 32;
 
 // ------------------------------------------------------------ cost ops --
 // Route costs: int32 exact (with negatives possible when D < 0), fp32 RN.
