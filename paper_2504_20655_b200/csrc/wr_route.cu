@@ -629,7 +629,6 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     uint64_t final_seq = 0;
     uint32_t final_cost = 0;
     unsigned long long perms = 0;
-    {
     // each segment's best route as a nibble sequence of order-stop indices
     uint64_t segseq[WR_MAX_SEGMENTS];
     int pi = R.prob0;
@@ -698,7 +697,6 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         final_seq = 0;
         for (int a = 0; a < n; ++a) final_seq |= (uint64_t)((best_seq >> (4 * (15 - a))) & 0xf) << (4 * a);
         if (lane == 0) atomicAdd(&counters[1], (unsigned long long)ncand);
-    }
     }
     if (lane == 0) {
         // Lehmer rank of the final sequence among the n! orders
