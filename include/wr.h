@@ -62,8 +62,12 @@ typedef int32_t wr_status;
 
 const char *wr_last_error(void);
 int32_t wr_version(void);
-/* Device work memory comes from a per-device stream-ordered pool that keeps
- * freed blocks for the next call; this returns the idle part to the driver. */
+/* Device work memory comes from a per-device stream-ordered pool behind a
+ * same-stream block cache: freed blocks are kept for the next call of the
+ * same shape (no allocation driver call on repeated calls; an allocation
+ * that fails releases the cache and retries). This returns every idle and
+ * cached block to the driver (e.g. before handing the memory to another
+ * allocator). */
 wr_status wr_release_cached(int32_t device);
 
 /* ---------------------------------------------------------------- graphs -- */

@@ -15,7 +15,7 @@ import numpy as np
 
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwr.so")
+LIB_PATH = os.environ.get("WR_LIB") or os.path.join(_HERE, "libwr.so")   # WR_LIB: an experimental build
 
 WR_OK, WR_EINVAL, WR_ENOMEM, WR_ENEGCYCLE, WR_EOVERFLOW, WR_EUNREACHABLE, WR_ETOOLARGE, WR_ECUDA, \
     WR_ENCCL, WR_EINTERNAL = range(10)

@@ -273,7 +273,13 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
 // Returns the word's change mask.
 // Task-queue capacity per vertex: per-warp queues of 32 x QC packed (u, w)
 // pairs after the bitmaps in dynamic shared memory.
-constexpr int QCAP = 16;
+#ifndef WR_QCAP
+#define WR_QCAP 16
+#endif
+constexpr int QCAP = WR_QCAP;
+#ifndef WR_AQ
+#define WR_AQ 8   // in-arcs loaded per batch in step A
+#endif
 #ifndef WR_FUSED_PA
 #define WR_FUSED_PA 2
 #endif
@@ -299,7 +305,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     // ---- A: queue this lane's changed in-arcs; the packed (u, w) arcs are
     // loaded AQ at a time (independent loads in flight, no branch between
     // them) before their tails' change bits are tested
-    constexpr int AQ = 8;
+    constexpr int AQ = WR_AQ;
     int c = 0;
     for (int k0 = a0; k0 < a1; k0 += AQ) {
         int2 arc[AQ];
