@@ -755,19 +755,42 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
             if (nj < 2) continue;
             const int64_t nf = fact(nj);
             perms += (unsigned long long)nf;
-            for (int64_t r = tid; r < nf; r += PAIRS_THREADS) {
-                const uint64_t loc = unrank_nib(r, nj);
-                int prev = nib(R.segmap[k], nib(loc, 0));
-                const int nx = nib(R.segmap[k], nib(loc, 1));
-                uint32_t cost = Ds[prev * MS + nx];
-                prev = nx;
-                for (int a = 2; a < nj; ++a) {
-                    const int x = nib(R.segmap[k], nib(loc, a));
-                    cost = C::add(cost, Ds[prev * MS + x]);
+            // each thread walks a contiguous rank range: one unrank, then
+            // lexicographic successors (next permutation) - no per-order
+            // 64-bit divisions
+            const int64_t per = (nf + PAIRS_THREADS - 1) / PAIRS_THREADS;
+            const int64_t r0 = (int64_t)tid * per, r1 = r0 + per < nf ? r0 + per : nf;
+            if (r0 < r1) {
+                int loc[PAIRS_MAX_SEG], stp[PAIRS_MAX_SEG];
+                const uint64_t l0 = unrank_nib(r0, nj);
+                for (int a = 0; a < nj; ++a) loc[a] = nib(l0, a);
+                for (int a = 0; a < nj; ++a) stp[a] = nib(R.segmap[k], a);
+                for (int64_t r = r0;;) {
+                    int prev = stp[loc[0]];
+                    int x = stp[loc[1]];
+                    uint32_t cost = Ds[prev * MS + x];
                     prev = x;
+                    for (int a = 2; a < nj; ++a) {
+                        x = stp[loc[a]];
+                        cost = C::add(cost, Ds[prev * MS + x]);
+                        prev = x;
+                    }
+                    const unsigned long long key = ((unsigned long long)C::key(cost) << 32) | (unsigned long long)r;
+                    atomicMin(&tab[k][loc[0]][loc[nj - 1]], key);
+                    if (++r >= r1) break;
+                    int i = nj - 2;   // next permutation of loc (lexicographic)
+                    while (loc[i] > loc[i + 1]) --i;
+                    int j = nj - 1;
+                    while (loc[j] < loc[i]) --j;
+                    const int tmp = loc[i];
+                    loc[i] = loc[j];
+                    loc[j] = tmp;
+                    for (int a = i + 1, b = nj - 1; a < b; ++a, --b) {
+                        const int t2 = loc[a];
+                        loc[a] = loc[b];
+                        loc[b] = t2;
+                    }
                 }
-                const unsigned long long key = ((unsigned long long)C::key(cost) << 32) | (unsigned long long)r;
-                atomicMin(&tab[k][nib(loc, 0)][nib(loc, nj - 1)], key);
             }
         }
         __syncthreads();
