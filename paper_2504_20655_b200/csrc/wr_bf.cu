@@ -24,6 +24,7 @@
 //   * pred is not written inside the racy sweep: a4 recomputes the
 //     canonical predecessor from the converged dist (O3), deterministic.
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -907,17 +908,22 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
 }
 
 // Sources per lane for S sources; WR_BF_SPL forces a width.
-int choose_spl(int64_t S, int nsm) {
-    (void)S;
-    (void)nsm;
+int choose_spl(int64_t S, int nsm, int pack) {
     const int forced = env_int("WR_BF_SPL", 0);
     if (forced == 1 || forced == 2 || forced == 4) return forced;
-    // Always the widest tile (measured): a tile's time is
-    // set by its chain of ~100 latency-bound rounds, almost independent of
-    // its width, so 128 sources per tile finish in the same time as 32 and
-    // the wave count ceil(tiles / SMs) is smallest at SPL 4 (per-rank shard
-    // of config 5 at W = 4: SPL 4 47 ms vs the narrow-tile 124 ms).
-    return 4;
+    // The widest tile that still yields at least half an SM's worth of tiles
+    // per SM pair (>= nsm / 2 tiles), else the narrowest. Measured on C5
+    // shards with packed rows (tools/shard_probe.py): 84.7k / 42.3k / 21.2k
+    // sources -> 256-source tiles (331 / 166 / 83 tiles; 128-source tiles
+    // were slower: 36.5 vs 31.6 ms at 42k, 22.8 vs 18.8 ms at 21k); 10.6k ->
+    // 128 (14.7 ms vs 16.9 at 256, 19.7 at 64); C4's 4k -> 64 (3.5 ms vs
+    // 7.2 at 256): a tile's sweep time shrinks with its width, but less than
+    // linearly, so narrower tiles pay only when SMs would otherwise idle.
+    for (int spl = 4; spl > 1; spl /= 2) {
+        const int64_t per = 32LL * spl * pack;
+        if ((std::max<int64_t>(S, 1) + per - 1) / per >= std::max(nsm / 2, 1)) return spl;
+    }
+    return 1;
 }
 
 // --------------------------------------------------- a4 + output layout --
@@ -1487,7 +1493,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     const int variant = o.variant == WR_BF_DENSE ? WR_BF_DENSE : WR_BF_FRONTIER;
     int nsm = 0;
     WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
-    const int spl = choose_spl(S, nsm);
+    const int spl = choose_spl(S, nsm, 1);
     const int tsw = 32 * spl;
 
     cudaEvent_t e0, e1;

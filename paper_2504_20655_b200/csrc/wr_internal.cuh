@@ -166,7 +166,7 @@ int64_t budget_bytes(int64_t requested, int64_t fixed, int64_t want_pooled);
 int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_source_bytes,
                             int64_t S, int tsw);
 // Sources per lane (1, 2, 4) for S sources on nsm SMs (env WR_BF_SPL forces).
-int choose_spl(int64_t S, int nsm);
+int choose_spl(int64_t S, int nsm, int pack);
 
 // The canonical-pred pass fused into the sweep: CTAs whose tile claims have
 // run out take pred jobs of finished tiles (in completion order) while the

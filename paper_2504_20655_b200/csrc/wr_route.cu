@@ -1221,7 +1221,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         const int64_t fixed = gi.device_bytes + (128 << 20);
         int nsm = 0;
         WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
-        const int spl = choose_spl(nsrc, nsm);
+        const int spl = choose_spl(nsrc, nsm, pk);
         const int tsw = 32 * spl * pk;            // sources per tile
         const int64_t src_bytes = 4LL * V / pk;   // row bytes per source
         const double h_pre = hms();
