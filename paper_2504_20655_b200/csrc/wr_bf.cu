@@ -1105,8 +1105,9 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
             int my_u = 0;
             uint32_t my_w = 0;
             if (sub < cnt) {
-                my_u = g.in_src[base + sub];
-                my_w = g.in_w[base + sub];
+                const int2 arc = g.in_arc[base + sub];   // (u, w) in one 8-B load
+                my_u = arc.x;
+                my_w = (uint32_t)arc.y;
             }
             // per-vertex early exit: a vertex whose slots all have their
             // pred stops gathering (its arc count drops to k)
