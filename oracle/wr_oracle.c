@@ -35,10 +35,13 @@
  *                     pinned: m=1 == exact, singletons == exact, and for int
  *                     weights == (min cost, lex-smallest) over ALL segment-
  *                     contiguous orders by brute force; int cost <= O7's.
- *   orc_held_karp_route  NEXT-2 exact route for 13-16 stops (subset DP,
- *                     P370 §3) pinned: == O5 enumeration (cost, order, rank)
- *                     on n <= 9 incl. tie-heavy matrices; cost == the tests'
- *                     independent Python Held-Karp for n up to 14.
+ *   orc_held_karp_route  NEXT-2 exact route for 13-16 stops (subset DP +
+ *                     backward feasibility + lexicographic greedy, P370 §3)
+ *                     pinned: == itertools brute force (cost, order, rank) on
+ *                     n <= 8 fp32 absorption matrices and the committed
+ *                     reproducers (tests/golden/hk_absorption.txt); == O5 on
+ *                     n <= 9 incl. tie-heavy matrices; cost == the tests'
+ *                     independent Python Held-Karp for n up to 13.
  *   orc_kmeans        O8 deterministic integer K-means   pinned: hand-made
  *                     separated clusters, brute-force Lloyd fixpoint check.
  *   orc_order_stops   a2 stop projection (P226-238 §2.4) pinned: numpy unique.
@@ -356,17 +359,44 @@ int orc_exact_route(int wtype, const void *D, int n, int *seq_out, void *cost_ou
 /* paper mentions Held-Karp O(n^2 2^n) as the exact-TSP alternative, P370   */
 /* §3; reading R2 in DESIGN.md). Same result as O5:     */
 /* the minimum left-to-right cost over all n! orders, ties -> the           */
-/* lexicographically smallest order:                                        */
-/*  state (S, j) = orders of the stop set S ending at j; it keeps the        */
-/*  cheapest prefix cost (left to right: fl(prefix + D[i][j]), which is     */
-/*  monotone in the prefix, so the minimum of the left-to-right sums is     */
-/*  exact - reading A16) and, among equal costs, the lexicographically      */
-/*  smallest prefix (equal suffixes keep that order). Prefixes are kept as  */
-/*  nibble keys, first stop in the most significant nibble.                 */
-/*  final = min over j of (cost(all, j), key).                              */
+/* lexicographically smallest order. Three steps:                           */
+/*  1. forward DP over states (S, j) = stop set S visited, ending at j:      */
+/*     F({j}, j) = 0, F(S, j) = min over i in S-{j} of fl(F(S-{j}, i) +     */
+/*     D[i][j]); C* = min_j F(all, j). fl(c + d) is monotone in c, so the    */
+/*     minimum of the left-to-right sums is exact (reading A16).            */
+/*  2. backward feasibility: M(S, j) = the largest prefix cost c with which  */
+/*     some completion of (S, j) still ends at a cost <= C*:                 */
+/*     M(all, j) = C*; M(S, j) = max over k not in S of                     */
+/*     inv(D[j][k], M(S+{k}, k)), inv(d, m) = max{c : fl(c + d) <= m}       */
+/*     (int: m - d exactly; fp32: bisection over the ordered bit patterns   */
+/*     of c >= 0, valid because fl(c + d) is monotone in c); "none" if no c. */
+/*  3. lexicographic greedy: the first stop is the smallest a with           */
+/*     M({a}, a) >= 0 (prefix cost 0), each next stop the smallest k not    */
+/*     yet visited with fl(c + D[j][k]) <= M(S+{k}, k). No order costs less  */
+/*     than C*, so "<= C*" is "== C*": the greedy walks the lexicographically */
+/*     smallest optimal order, which is O5's first minimum.                   */
+/* Keeping one cheapest prefix per state (the earlier version) is NOT enough */
+/* for fp32: fl(c + d) is monotone but not strictly, so a costlier,         */
+/* lexicographically smaller prefix can tie after rounding.    */
+/* If every order costs INF (an INF leg in each), O5 returns the identity.  */
 /* int sums in int64 (INF leg -> INF); a finite result outside int32 ->     */
 /* ORC_EOVERFLOW.                                                           */
 /* ------------------------------------------------------------------------ */
+static float f32_of_bits(uint32_t b) { float f; memcpy(&f, &b, 4); return f; }
+
+/* max{c >= 0 float : fl(c + d) <= m}, or -1 if none (d, m >= 0 or +inf). */
+static float f32_inv(float d, float m)
+{
+    if (!(0.0f + d <= m)) return -1.0f;              /* not even c = 0 */
+    uint32_t lo = 0, hi = 0x7f800000u;               /* +0 .. +inf      */
+    if (f32_of_bits(hi) + d <= m) return f32_of_bits(hi);
+    while (hi - lo > 1) {                            /* P(lo) true, P(hi) false */
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (f32_of_bits(mid) + d <= m) lo = mid; else hi = mid;
+    }
+    return f32_of_bits(lo);
+}
+
 int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cost_out,
                         long long *rank_out)
 {
@@ -377,72 +407,109 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
         *rank_out = 0;
         return ORC_OK;
     }
-    const size_t NS = (size_t)1 << n;
-    const int64_t IINF = INT64_MAX / 4;
-    int64_t *ci = NULL;
-    float *cf = NULL;
-    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * NS * (size_t)n);
-    char *have = (char *)calloc(NS * (size_t)n, 1);
+    const size_t NS = (size_t)1 << n, F = NS - 1;
+    const int64_t IINF = INT64_MAX / 4, NONE = INT64_MIN;
+    const int *Di = (const int *)D;
+    const float *Df = (const float *)D;
+    int64_t *ci = NULL;        /* int:  F then M, [S * n + j] */
+    float *cf = NULL;          /* fp32: F then M              */
     if (wtype == ORC_I32) ci = (int64_t *)malloc(sizeof(int64_t) * NS * (size_t)n);
     else cf = (float *)malloc(sizeof(float) * NS * (size_t)n);
-    if (!key || !have || (!ci && !cf)) { free(key); free(have); free(ci); free(cf); return ORC_ENOMEM; }
-    for (int j = 0; j < n; ++j) {
-        const size_t st = ((size_t)1 << j) * n + j;
-        have[st] = 1;
-        key[st] = (uint64_t)j << 60;
-        if (ci) ci[st] = 0; else cf[st] = 0.0f;
-    }
+    if (!ci && !cf) return ORC_ENOMEM;
+    /* 1. forward DP */
     for (size_t S = 1; S < NS; ++S) {
-        const int k = __builtin_popcountll((unsigned long long)S);
-        if (k < 2) continue;
         for (int j = 0; j < n; ++j) {
             if (!((S >> j) & 1)) continue;
-            const size_t P = S & ~((size_t)1 << j);
-            const size_t st = S * n + j;
+            const size_t P = S & ~((size_t)1 << j), st = S * n + j;
+            if (P == 0) { if (ci) ci[st] = 0; else cf[st] = 0.0f; continue; }
+            int first = 1;
             for (int i = 0; i < n; ++i) {
-                if (!((P >> i) & 1) || !have[P * n + i]) continue;
-                const uint64_t kk = key[P * n + i] | ((uint64_t)j << (4 * (15 - (k - 1))));
-                int better;
+                if (!((P >> i) & 1)) continue;
                 if (ci) {
-                    const int leg = ((const int *)D)[(size_t)i * n + j];
+                    const int leg = Di[(size_t)i * n + j];
                     const int64_t pre = ci[P * n + i];
-                    const int64_t c = (leg == I32_INF || pre >= IINF) ? IINF : (k == 2 ? (int64_t)leg : pre + leg);
-                    better = !have[st] || c < ci[st] || (c == ci[st] && kk < key[st]);
-                    if (better) ci[st] = c;
+                    const int64_t c = (leg == I32_INF || pre >= IINF) ? IINF : pre + leg;
+                    if (first || c < ci[st]) ci[st] = c;
                 } else {
-                    const float leg = ((const float *)D)[(size_t)i * n + j];
-                    const float c = k == 2 ? leg : cf[P * n + i] + leg;
-                    better = !have[st] || c < cf[st] || (c == cf[st] && kk < key[st]);
-                    if (better) cf[st] = c;
+                    const float c = cf[P * n + i] + Df[(size_t)i * n + j];
+                    if (first || c < cf[st]) cf[st] = c;
                 }
-                if (better) { have[st] = 1; key[st] = kk; }
+                first = 0;
             }
         }
     }
-    const size_t F = NS - 1;
-    int bj = -1;
+    int64_t cstar_i = 0;
+    float cstar_f = 0.0f;
     for (int j = 0; j < n; ++j) {
-        const size_t st = F * n + j;
-        if (!have[st]) continue;
-        int better;
-        if (bj < 0) better = 1;
-        else if (ci) better = ci[st] < ci[F * n + bj] || (ci[st] == ci[F * n + bj] && key[st] < key[F * n + bj]);
-        else better = cf[st] < cf[F * n + bj] || (cf[st] == cf[F * n + bj] && key[st] < key[F * n + bj]);
-        if (better) bj = j;
+        if (ci) { if (j == 0 || ci[F * n + j] < cstar_i) cstar_i = ci[F * n + j]; }
+        else { if (j == 0 || cf[F * n + j] < cstar_f) cstar_f = cf[F * n + j]; }
     }
-    const uint64_t kb = key[F * n + bj];
-    for (int a = 0; a < n; ++a) seq_out[a] = (int)((kb >> (4 * (15 - a))) & 0xf);
+    int all_inf = ci ? cstar_i >= IINF : isinf(cstar_f);
+    if (all_inf) {                                   /* every order costs INF: O5 keeps rank 0 */
+        for (int a = 0; a < n; ++a) seq_out[a] = a;
+        if (ci) *(int *)cost_out = I32_INF; else *(float *)cost_out = INFINITY;
+        *rank_out = 0;
+        free(ci); free(cf);
+        return ORC_OK;
+    }
+    /* 2. backward feasibility bound M (overwrites F, full set first) */
+    for (size_t S = NS - 1; S >= 1; --S) {
+        for (int j = 0; j < n; ++j) {
+            if (!((S >> j) & 1)) continue;
+            const size_t st = S * n + j;
+            if (S == F) { if (ci) ci[st] = cstar_i; else cf[st] = cstar_f; continue; }
+            int64_t bi = NONE;
+            float bf = -1.0f;
+            for (int k = 0; k < n; ++k) {
+                if ((S >> k) & 1) continue;
+                const size_t nx = (S | ((size_t)1 << k)) * n + k;
+                if (ci) {
+                    const int leg = Di[(size_t)j * n + k];
+                    if (leg == I32_INF || ci[nx] == NONE) continue;
+                    const int64_t c = ci[nx] - leg;      /* max c with c + leg <= M */
+                    if (c > bi) bi = c;
+                } else {
+                    if (cf[nx] < 0.0f) continue;
+                    const float c = f32_inv(Df[(size_t)j * n + k], cf[nx]);
+                    if (c > bf) bf = c;
+                }
+            }
+            if (ci) ci[st] = bi; else cf[st] = bf;
+        }
+        if (S == 1) break;
+    }
+    /* 3. lexicographic greedy along the feasible states */
+    size_t S = 0;
+    int j = -1;
+    int64_t pi = 0;
+    float pf = 0.0f;
+    for (int t = 0; t < n; ++t) {
+        int pick = -1;
+        for (int k = 0; k < n && pick < 0; ++k) {
+            if ((S >> k) & 1) continue;
+            const size_t nx = (S | ((size_t)1 << k)) * n + k;
+            if (ci) {
+                const int64_t c = t == 0 ? 0 : (Di[(size_t)j * n + k] == I32_INF ? IINF : pi + Di[(size_t)j * n + k]);
+                if (ci[nx] != NONE && c < IINF && c <= ci[nx]) { pick = k; pi = c; }
+            } else {
+                const float c = t == 0 ? 0.0f : pf + Df[(size_t)j * n + k];
+                if (cf[nx] >= 0.0f && c <= cf[nx]) { pick = k; pf = c; }
+            }
+        }
+        if (pick < 0) { free(ci); free(cf); return ORC_EINVAL; }   /* unreachable by construction */
+        seq_out[t] = pick;
+        S |= (size_t)1 << pick;
+        j = pick;
+    }
     int rc = ORC_OK;
     if (ci) {
-        const int64_t c = ci[F * n + bj];
-        if (c >= IINF) *(int *)cost_out = I32_INF;
-        else if (c >= I32_INF || c < INT32_MIN) rc = ORC_EOVERFLOW;
-        else *(int *)cost_out = (int)c;
+        if (pi >= I32_INF || pi < INT32_MIN) rc = ORC_EOVERFLOW;
+        else *(int *)cost_out = (int)pi;
     } else {
-        *(float *)cost_out = cf[F * n + bj];
+        *(float *)cost_out = pf;
     }
     *rank_out = orc_perm_rank(seq_out, n);
-    free(key); free(have); free(ci); free(cf);
+    free(ci); free(cf);
     return rc;
 }
 

@@ -292,6 +292,89 @@ def test_held_karp_equals_enumeration(kind):
         assert hs.tolist() == es.tolist() and hr == er
 
 
+def load_hk_absorption():
+    mats, cur = {}, None
+    for line in open(os.path.join(GOLD, "hk_absorption.txt")):
+        line = line.split("#")[0].split()
+        if not line:
+            continue
+        if line[0] == "matrix":
+            cur = line[1]
+            mats[cur] = []
+        else:
+            mats[cur].append([np.float32(x) for x in line])
+    return {k: np.array(v, np.float32) for k, v in mats.items()}
+
+
+def absorption_D(rng, n):
+    """fp32 matrices built to make rounding ties: n-1 "near" stops joined by
+    small legs (0.5 .. 3) and one "far" stop whose legs are ~1e8 (ulp 8),
+    so every order pays one big leg that absorbs the small prefix sums
+    before it (reading A16: fl(c + d) is monotone but not strictly)."""
+    small = np.array([0.5, 1, 1.5, 2, 3], np.float32)
+    D = rng.choice(small, (n, n)).astype(np.float32)
+    far = int(rng.integers(0, n))
+    D[far, :] = np.float32(1e8) + rng.integers(0, 4, n).astype(np.float32) * 8
+    D[:, far] = np.float32(1e8) + rng.integers(0, 4, n).astype(np.float32) * 8
+    np.fill_diagonal(D, 0)
+    return D
+
+
+def cheapest_prefix_dp_argmin(D):
+    """The round-1 DP (kept for the test only): per state the cheapest
+    prefix, ties -> lexicographically smaller prefix. Not O5 for fp32."""
+    n = D.shape[0]
+    best = {(1 << j, j): (np.float32(0), (j,)) for j in range(n)}
+    for size in range(2, n + 1):
+        for S in range(1 << n):
+            if bin(S).count("1") != size:
+                continue
+            for j in range(n):
+                if not S >> j & 1:
+                    continue
+                P = S & ~(1 << j)
+                cands = [(np.float32(best[(P, i)][0] + D[i, j]), best[(P, i)][1] + (j,)) for i in range(n) if P >> i & 1]
+                best[(S, j)] = min(cands, key=lambda x: (x[0], x[1]))
+    full = (1 << n) - 1
+    return min((best[(full, j)] for j in range(n)), key=lambda x: (x[0], x[1]))[1]
+
+
+def test_held_karp_fp32_absorption_reproducers():
+    """The round-1 counterexamples (tests/golden/hk_absorption.txt and a real
+    C3 fp32 order): the subset DP must return O5's lexicographically smallest
+    optimum, recomputed here by itertools brute force."""
+    for name, D in load_hk_absorption().items():
+        bc, br, bs = brute(D)
+        hc, hr, hs = oracle.held_karp_route(D)
+        assert np.float32(hc).tobytes() == np.float32(bc).tobytes(), name
+        assert hs.tolist() == list(bs) and hr == br == 0, name
+    g, _, _ = gen.config(3, wtype="f32")
+    stops = np.array([40, 1544, 1568, 2145, 2441, 2455, 3461, 3876, 4878], np.int32)
+    D = oracle.bf_many(g, stops)[:, stops]
+    bc, br, bs = brute(D)
+    hc, hr, hs = oracle.held_karp_route(D)
+    assert np.float32(hc).tobytes() == np.float32(bc).tobytes()
+    assert hs.tolist() == list(bs) and hr == br
+
+
+def test_held_karp_fp32_absorption_random_vs_brute():
+    """Absorption-heavy fp32 matrices, n = 4..7: (cost, order, rank) equal the
+    itertools brute force; at least some instances have several optimal
+    orders whose prefixes differ in cost, so the round-1 DP that kept one
+    cheapest prefix per state returns another order on them."""
+    rng = np.random.default_rng(83)
+    hard = 0   # instances the round-1 DP (cheapest prefix per state) got wrong
+    for trial in range(150):
+        n = int(rng.integers(4, 8))
+        D = absorption_D(rng, n)
+        bc, br, bs = brute(D)
+        hc, hr, hs = oracle.held_karp_route(D)
+        assert np.float32(hc).tobytes() == np.float32(bc).tobytes(), trial
+        assert hs.tolist() == list(bs) and hr == br, trial
+        hard += list(cheapest_prefix_dp_argmin(D)) != list(bs)
+    assert hard >= 5
+
+
 def test_held_karp_large_vs_independent_dp():
     """n = 12..13 (beyond cheap enumeration): cost equals the tests' own
     Held-Karp; the int order equals the independent suffix-DP lexicographic
