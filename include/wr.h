@@ -130,8 +130,11 @@ typedef struct {
     void *stream;            /* cudaStream_t; NULL = default stream          */
     int32_t async;           /* 1: device outputs, no host sync              */
     int32_t variant;         /* WR_BF_*                                      */
-    int32_t max_rounds;      /* 0 = V-1 (P724 §4.7); fewer -> WR_EINTERNAL if
-                                not converged                                */
+    int32_t max_rounds;      /* relaxation rounds, 0 = V-1 (P724 §4.7); one
+                                more round checks convergence: if it still
+                                improves a distance -> WR_ENEGCYCLE (default
+                                max_rounds, a negative cycle is reachable) or
+                                WR_EINTERNAL (caller's max_rounds too small) */
     int64_t hbm_budget;      /* working-set bytes per segment; 0 = 180e9,
                                 clamped to 90 % of free device memory (a8)  */
 } wr_bf_opts;

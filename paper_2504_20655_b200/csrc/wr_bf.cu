@@ -611,7 +611,11 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             uint32_t *t = cur;
             cur = nxt;
             nxt = t;
-            if (more && rounds >= max_rounds) {
+            // max_rounds relaxation rounds (P724 §4.7: V-1), then one more
+            // round as the check pass (the oracle's extra pass): a change in
+            // round max_rounds + 1 means a negative cycle (or, for a caller's
+            // smaller max_rounds, no convergence)
+            if (more && rounds > max_rounds) {
                 if (threadIdx.x == 0) atomicMax(&stats->negcycle_tile, tile);
                 more = false;
             }
@@ -1489,8 +1493,8 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     StreamScope stream_scope(st);
     const int V = g->V;
     const int ncols = targets ? T : V;
-    int max_rounds = o.max_rounds > 0 ? o.max_rounds : std::max(1, V - 1);
-    if (!g->has_negative && o.max_rounds <= 0) max_rounds = V;  // no negative cycle possible
+    // V-1 relaxation rounds (P724 §4.7) + the kernel's check round
+    const int max_rounds = o.max_rounds > 0 ? o.max_rounds : std::max(1, V - 1);
     const int variant = o.variant == WR_BF_DENSE ? WR_BF_DENSE : WR_BF_FRONTIER;
     int nsm = 0;
     WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));

@@ -24,6 +24,8 @@
 #include <memory>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "wr_internal.cuh"
 
 namespace wr {
@@ -467,7 +469,7 @@ template <class C>
 __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
                                      int64_t nord, const uint32_t *Dall, int m, const int *xy,
                                      const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
-                                     int *item_cnt, int pairs, int *hk_count) {
+                                     int *item_cnt, int pairs, int *hk_count, int *hk_list) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nord) return;
     const int64_t o = o_lo + t;
@@ -528,7 +530,8 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 R.hk = 1;
                 R.noenum = 1;
                 nseg = 0;
-                atomicAdd(hk_count, 1);
+                hk_list[atomicAdd(hk_count, 1)] = (int)t;   // [0] count, [2] max n
+                atomicMax(hk_count + 2, n);
             }
             if (pairs && nseg >= 2) {
                 // boundary-pair stitch (NEXT-1): per-segment orders and the
@@ -897,131 +900,261 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
 }
 
 // NEXT-2 exact route for 13-16 stops (oracle: orc_held_karp_route, reading
-// R2): Held-Karp subset DP. State (S, j) = the stop set S visited, ending at
-// j: cheapest left-to-right prefix cost (fl(prefix + D[i][j]) is monotone in
-// the prefix, so the minimum is exact) and, among equal costs, the
-// lexicographically smallest prefix as a nibble key (first stop most
-// significant). Persistent blocks, one order at a time per block, each with
-// its own global state table (2^16 x 16 costs + keys = 12 MB); the subset
-// layers |S| = 2..n are separated by block barriers.
+// R2): O5's result - the minimum left-to-right cost, ties -> the
+// lexicographically smallest order - in three passes over cost-only state
+// tables W[S][j] (S = stop set, j = last stop, row stride 16):
+//  1. forward subset DP F(S, j) = min_i fl(F(S-j, i) + D[i][j]) -> C*;
+//  2. backward bound M(S, j) = the largest prefix cost with which some
+//     completion still ends <= C*: M(all, j) = C*, M(S, j) = max over
+//     unvisited k of inv(D[j][k], M(S+k, k)), inv(d, m) = max{c : fl(c + d)
+//     <= m} (written over F, layer by layer);
+//  3. lexicographic greedy: next stop = the smallest k with fl(c + D[j][k])
+//     <= M(S+k, k).
+// One order per 8-CTA cluster: a layer's states are split over the cluster's
+// 4,096 threads and layers are separated by cluster barriers; the subsets of
+// each popcount come from a precomputed list. At most HK_CLUSTERS tables of
+// 2^n x 16 x 4 B (4 MB at n = 16) are live, so they stay in L2; workspace
+// loads/stores bypass L1 (ld/st .cg).
 constexpr int HK_THREADS = 512;
+constexpr int HK_CL = 8;            // CTAs per cluster (one order each)
+constexpr int HK_CLUSTERS = 18;     // clusters in flight: 144 SMs, 72 MB of tables
+constexpr int HK_MIN = WR_MAX_EXACT + 1;
 constexpr int HK_MAX = WR_MAX_STOPS;
+constexpr int HK_RS = 16;           // workspace row stride (states of one S)
+
+// fp32: max{c >= 0 : fl(c + d) <= m} exactly (RN-even), -1 if none. fl(x) <=
+// m iff x < T or (x == T and m's significand is even), T = m + ulp(m)/2 (the
+// midpoint to the next float; exact in double); c is the largest float below
+// T - d (or equal to it when the tie goes to m): directed double subtraction,
+// then directed conversion.
+__device__ inline float f32_inv(float d, float m) {
+    if (!(d <= m)) return -1.0f;                       // even c = 0 gives fl(d) > m
+    if (isinf(m)) return __int_as_float(0x7f800000);
+    const uint32_t mb = __float_as_uint(m);
+    const int e = (int)(mb >> 23);
+    const double ulp = e > 0 ? ldexp(1.0, e - 150) : ldexp(1.0, -149);
+    const double T = (double)m + 0.5 * ulp;
+    const double lo = __dsub_rd(T, (double)d), hi = __dsub_ru(T, (double)d);
+    float c = __double2float_rd(lo);
+    if ((mb & 1u) && lo == hi && (double)c == lo) c = __uint_as_float(__float_as_uint(c) - 1u);   // strict
+    return c;
+}
+
 template <class C>
-__global__ void __launch_bounds__(HK_THREADS) route_hk_kernel(int64_t nord, const OrderRoute *ordr,
-                                                              const uint32_t *Dall, const int *stops, int64_t o_lo,
-                                                              wr_route_result *out, unsigned long long *counters,
-                                                              int *next_order, uint32_t *cost_ws,
-                                                              unsigned long long *key_ws) {
+struct HkOps;
+template <>
+struct HkOps<CostI32> {    // int32 (sums exact within the route bound, A7)
+    static constexpr uint32_t NONE = 0x80000000u;
+    __device__ static uint32_t fwd(uint32_t pre, uint32_t leg) {
+        return (pre == CostI32::INF || leg == CostI32::INF) ? CostI32::INF : (uint32_t)((int)pre + (int)leg);
+    }
+    // max c with c + leg <= m, saturated to int32 (prefix sums stay strictly
+    // inside (INT32_MIN, INT32_MAX), so saturation never changes a test)
+    __device__ static uint32_t inv(uint32_t leg, uint32_t m) {
+        if (leg == CostI32::INF || m == NONE) return NONE;
+        int64_t c = (int64_t)(int)m - (int)leg;
+        if (c >= (int64_t)INT32_MAX) c = INT32_MAX - 1;
+        if (c <= (int64_t)INT32_MIN) return NONE;
+        return (uint32_t)(int)c;
+    }
+    __device__ static bool gt(uint32_t a, uint32_t b) { return (int)a > (int)b; }   // NONE is the least
+    __device__ static bool step(uint32_t c, uint32_t leg, uint32_t m, uint32_t &out) {
+        if (m == NONE || leg == CostI32::INF) return false;
+        const int64_t x = (int64_t)(int)c + (int)leg;
+        out = (uint32_t)(int)x;
+        return x <= (int64_t)(int)m;
+    }
+};
+template <>
+struct HkOps<CostF32> {    // fp32 >= 0; NONE = -1.0f
+    static constexpr uint32_t NONE = 0xbf800000u;
+    __device__ static uint32_t fwd(uint32_t pre, uint32_t leg) { return CostF32::add(pre, leg); }
+    __device__ static uint32_t inv(uint32_t leg, uint32_t m) {
+        if (m == NONE) return NONE;
+        return __float_as_uint(f32_inv(__uint_as_float(leg), __uint_as_float(m)));
+    }
+    __device__ static bool gt(uint32_t a, uint32_t b) { return __uint_as_float(a) > __uint_as_float(b); }
+    __device__ static bool step(uint32_t c, uint32_t leg, uint32_t m, uint32_t &out) {
+        if (m == NONE) return false;
+        out = CostF32::add(c, leg);
+        return __uint_as_float(out) <= __uint_as_float(m);
+    }
+};
+
+struct HkLists {           // subsets of [0, n) sorted by popcount, n = 13..16
+    const uint16_t *sets;  // concatenated lists
+    int off[HK_MAX - HK_MIN + 1][HK_MAX + 2];   // [n - HK_MIN][k] start of popcount k
+};
+
+template <class C>
+__global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
+    route_hk_kernel(const int *__restrict__ hk_list, int nhk, const OrderRoute *ordr, const uint32_t *Dall,
+                    const int *stops, int64_t o_lo, wr_route_result *out, unsigned long long *counters,
+                    int *next, uint32_t *ws, size_t ws_stride, HkLists L) {
+    namespace cg = cooperative_groups;
+    using H = HkOps<C>;
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned crank = cl.block_rank();
+    const int tid = threadIdx.x;
+    const int gtid = (int)crank * HK_THREADS + tid, gstride = HK_CL * HK_THREADS;
     __shared__ uint32_t Ds[DSTRIDE];
-    __shared__ int s_t;
-    __shared__ uint32_t sBestKey[HK_THREADS / 32];
-    __shared__ unsigned long long sBestSeq[HK_THREADS / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t *cost = cost_ws + (size_t)blockIdx.x * ((size_t)1 << HK_MAX) * HK_MAX;
-    unsigned long long *key = key_ws + (size_t)blockIdx.x * ((size_t)1 << HK_MAX) * HK_MAX;
+    __shared__ int s_i;
+    uint32_t *W = ws + (size_t)(blockIdx.x / HK_CL) * ws_stride;
     for (;;) {
-        if (tid == 0) s_t = atomicAdd(next_order, 1);
-        __syncthreads();
-        const int64_t t = s_t;
-        if (t >= nord) break;
+        if (crank == 0 && tid == 0) s_i = atomicAdd(next, 1);
+        cl.sync();
+        const int i = *cl.map_shared_rank(&s_i, 0);
+        cl.sync();   // every CTA has read rank 0's claim
+        if (i >= nhk) break;
+        const int t = hk_list[i];
         const OrderRoute R = ordr[t];
-        if (R.status != WR_OK || !R.hk) {
-            __syncthreads();
-            continue;
-        }
         const int n = R.n;
-        const uint32_t NS = 1u << n;
         const uint32_t *D = Dall + (size_t)t * DSTRIDE;
         for (int e = tid; e < DSTRIDE; e += HK_THREADS) Ds[e] = D[e];
-        for (int j = tid; j < n; j += HK_THREADS) {
-            const size_t st = (size_t)(1u << j) * n + j;
-            cost[st] = 0u;
-            key[st] = (unsigned long long)j << 60;
-        }
+        const uint16_t *sets = L.sets;
+        const int *off = L.off[n - HK_MIN];
+        if (gtid < n) __stcg(W + (size_t)(1u << gtid) * HK_RS + gtid, 0u);   // F({j}, j) = 0
         __syncthreads();
+        cl.sync();
+        // 1. forward layers |S| = 2..n
         for (int k = 2; k <= n; ++k) {
-            for (uint32_t S = tid; S < NS; S += HK_THREADS) {
-                if (__popc(S) != k) continue;
-                for (int j = 0; j < n; ++j) {
-                    if (!((S >> j) & 1u)) continue;
-                    const uint32_t P = S & ~(1u << j);
-                    uint32_t bc = 0, bk = 0;
-                    unsigned long long bkey = 0;
-                    bool have = false;
-                    for (int i = 0; i < n; ++i) {
-                        if (!((P >> i) & 1u)) continue;
-                        const uint32_t leg = Ds[i * MS + j];
-                        const uint32_t c = k == 2 ? leg : C::add(cost[(size_t)P * n + i], leg);
-                        const uint32_t ck = C::key(c);
-                        const unsigned long long kk =
-                            key[(size_t)P * n + i] | ((unsigned long long)j << (4 * (15 - (k - 1))));
-                        if (!have || ck < bk || (ck == bk && kk < bkey)) {
-                            have = true;
-                            bc = c;
-                            bk = ck;
-                            bkey = kk;
-                        }
-                    }
-                    cost[(size_t)S * n + j] = bc;
-                    key[(size_t)S * n + j] = bkey;
-                }
-            }
-            __syncthreads();
-        }
-        // final: min over the last stop j of (cost key, order key)
-        uint32_t best_key = 0xffffffffu;
-        unsigned long long best_seq = ~0ull;
-        const uint32_t F = NS - 1;
-        for (int j = tid; j < n; j += HK_THREADS) {
-            const uint32_t ck = C::key(cost[(size_t)F * n + j]);
-            const unsigned long long kk = key[(size_t)F * n + j];
-            if (ck < best_key || (ck == best_key && kk < best_seq)) {
-                best_key = ck;
-                best_seq = kk;
-            }
-        }
+            const int base = off[k], items = (off[k + 1] - base) * k;
+            for (int x = gtid; x < items; x += gstride) {
+                const int sidx = x / k, b = x - sidx * k;
+                const uint32_t S = sets[base + sidx];
+                const int j = __fns(S, 0, b + 1);
+                const uint32_t P = S & ~(1u << j);
+                const uint4 *row = reinterpret_cast<const uint4 *>(W + (size_t)P * HK_RS);
+                uint32_t r[16];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const uint32_t k2 = __shfl_xor_sync(0xffffffffu, best_key, o);
-            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, best_seq, o);
-            if (k2 < best_key || (k2 == best_key && s2 < best_seq)) {
-                best_key = k2;
-                best_seq = s2;
-            }
-        }
-        if (lane == 0) {
-            sBestKey[warp] = best_key;
-            sBestSeq[warp] = best_seq;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int w2 = 1; w2 < HK_THREADS / 32; ++w2)
-                if (sBestKey[w2] < best_key || (sBestKey[w2] == best_key && sBestSeq[w2] < best_seq)) {
-                    best_key = sBestKey[w2];
-                    best_seq = sBestSeq[w2];
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 v = __ldcg(row + q);
+                    r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
                 }
+                uint32_t best = 0xffffffffu;
+#pragma unroll
+                for (int a = 0; a < 16; ++a)
+                    if ((P >> a) & 1u) best = min(best, C::key(H::fwd(r[a], Ds[a * MS + j])));
+                __stcg(W + (size_t)S * HK_RS + j, C::unkey(best));
+            }
+            cl.sync();
+        }
+        // C* = min over the last stop of F(all, j)
+        const uint32_t F = (1u << n) - 1u;
+        uint32_t ck = 0xffffffffu;
+        for (int j = 0; j < n; ++j) ck = min(ck, C::key(__ldcg(W + (size_t)F * HK_RS + j)));
+        const uint32_t cstar = C::unkey(ck);
+        cl.sync();   // every CTA has C* before M(all, .) overwrites F(all, .)
+        wr_route_result res;
+        if (cstar == C::INF) {   // every order costs INF: O5 keeps the identity (rank 0)
+            if (crank == 0 && tid == 0) {
+                const int *s = stops + (o_lo + t) * MS;
+                res.n = n;
+                res.status = WR_OK;
+                res.m_used = 1;
+                res.cost_bits = C::INF;
+                res.rank = 0;
+                for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[a] : -1;
+                out[t] = res;
+            }
+            cl.sync();
+            continue;
+        }
+        // 2. backward bound, layers |S| = n .. 1
+        if (gtid < n) __stcg(W + (size_t)F * HK_RS + gtid, cstar);
+        cl.sync();
+        for (int k = n - 1; k >= 1; --k) {
+            const int base = off[k], items = (off[k + 1] - base) * k;
+            for (int x = gtid; x < items; x += gstride) {
+                const int sidx = x / k, b = x - sidx * k;
+                const uint32_t S = sets[base + sidx];
+                const int j = __fns(S, 0, b + 1);
+                uint32_t best = H::NONE;
+                for (uint32_t rest = F & ~S; rest; rest &= rest - 1) {
+                    const int q = __ffs(rest) - 1;
+                    const uint32_t m = __ldcg(W + (size_t)(S | (1u << q)) * HK_RS + q);
+                    const uint32_t c = H::inv(Ds[j * MS + q], m);
+                    if (H::gt(c, best)) best = c;
+                }
+                __stcg(W + (size_t)S * HK_RS + j, best);
+            }
+            cl.sync();
+        }
+        // 3. lexicographic greedy (one thread)
+        if (crank == 0 && tid == 0) {
+            uint32_t S = 0, c = 0;
+            int j = -1, seq[MS];
+            bool ok = true;
+            for (int a = 0; a < n && ok; ++a) {
+                int pick = -1;
+                uint32_t cn = 0;
+                for (int q = 0; q < n && pick < 0; ++q) {
+                    if ((S >> q) & 1u) continue;
+                    const uint32_t m = __ldcg(W + (size_t)(S | (1u << q)) * HK_RS + q);
+                    uint32_t nx = 0;
+                    if (a == 0) {
+                        if (m != H::NONE && !H::gt(0u, m)) { pick = q; nx = 0u; }
+                    } else if (H::step(c, Ds[j * MS + q], m, nx)) {
+                        pick = q;
+                    }
+                    cn = nx;
+                }
+                ok = pick >= 0;
+                if (!ok) break;
+                seq[a] = pick;
+                S |= 1u << pick;
+                j = pick;
+                c = cn;
+            }
             const int *s = stops + (o_lo + t) * MS;
-            wr_route_result res;
             res.n = n;
-            res.status = WR_OK;
+            res.status = ok ? WR_OK : WR_EINTERNAL;
             res.m_used = 1;
-            res.cost_bits = C::unkey(best_key);
+            res.cost_bits = c;
             int64_t rank = 0;   // Lehmer rank among the n! orders
-            int seq[MS];
-            for (int a = 0; a < n; ++a) seq[a] = (int)((best_seq >> (4 * (15 - a))) & 0xf);
-            for (int a = 0; a < n; ++a) {
+            for (int a = 0; a < n && ok; ++a) {
                 int smaller = 0;
                 for (int b = a + 1; b < n; ++b) smaller += seq[b] < seq[a];
                 rank += smaller * fact(n - 1 - a);
             }
             res.rank = rank;
-            for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[seq[a]] : -1;
+            for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[seq[a]] : -1;
             out[t] = res;
-            // work: states x predecessors = sum over S, j in S of |S| - 1
-            atomicAdd(&counters[0], (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
+            // work: forward transitions n (n-1) 2^(n-2), as many in the bound pass
+            atomicAdd(&counters[0], 2ull * (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
         }
-        __syncthreads();
+        cl.sync();   // the table is reused by the cluster's next order
     }
+}
+
+// The popcount-sorted subset lists for n = 13..16 (host-built once per
+// device; 240 KB).
+static HkLists hk_lists(int device) {
+    static std::vector<std::pair<int, HkLists>> cache;
+    static std::vector<DBuf<uint16_t>> keep;
+    for (auto &e : cache)
+        if (e.first == device) return e.second;
+    HkLists L{};
+    std::vector<uint16_t> all;
+    for (int n = HK_MIN; n <= HK_MAX; ++n) {
+        int *off = L.off[n - HK_MIN];
+        for (int k = 0; k <= n; ++k) {
+            off[k] = (int)all.size();
+            for (uint32_t S = 0; S < (1u << n); ++S)
+                if (__builtin_popcount(S) == k) all.push_back((uint16_t)S);
+        }
+        off[n + 1] = (int)all.size();
+    }
+    DBuf<uint16_t> d;
+    {
+        StreamScope s0(0);   // process-lifetime buffer on the legacy stream
+        d = to_device<uint16_t>(all.data(), all.size(), 0);
+        WR_CUDA(cudaStreamSynchronize(0));
+    }
+    L.sets = d.p;
+    keep.push_back(std::move(d));
+    cache.push_back({device, L});
+    return L;
 }
 
 // ------------------------------------------------------ route_cost (O4) --
@@ -1245,7 +1378,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         static const bool no_fuse = getenv("WR_NO_FUSED_PRED") != nullptr;
         const bool fused = o.pred_out && !g->has_negative && !no_fuse;
         DBuf<int> done_list(fused ? max_tiles : 0), fuse_ctr(fused ? 4 : 0);
-        int max_rounds = g->has_negative ? std::max(1, V - 1) : V;
+        const int max_rounds = std::max(1, V - 1);   // + the kernel's check round (ENEGCYCLE if it changes)
         const int64_t *off_r = P->off_all.p + (int64_t)P->rank * (P->B + 1);
         cudaEvent_t b0, b1, b2;
         WR_CUDA(cudaEventCreate(&b0));
@@ -1365,23 +1498,24 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     if (nord <= 0) return;
     const int *xy = P.g->xy.p;
     DBuf<OrderRoute> ordr(nord);
-    DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(2);
+    DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(4), hk_list(nord);
     WR_CUDA(cudaMemsetAsync(pcnt.p + nord, 0, 4, st));
     WR_CUDA(cudaMemsetAsync(icnt.p + nord, 0, 4, st));
-    WR_CUDA(cudaMemsetAsync(hk_ctr.p, 0, 8, st));
+    WR_CUDA(cudaMemsetAsync(hk_ctr.p, 0, 16, st));
     route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
         P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
         P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs,
-        hk_ctr.p);
+        hk_ctr.p, hk_list.p);
     count_launch();
     WR_LAUNCH_CHECK();
     scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
     scan_exclusive_i32(icnt.p, icnt.p, (int)(nord + 1), st);
-    int nprob = 0, nitems = 0, nhk = 0;
+    int nprob = 0, nitems = 0, hkc[4] = {0, 0, 0, 0};
     WR_CUDA(cudaMemcpyAsync(&nprob, pcnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaMemcpyAsync(&nitems, icnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
-    WR_CUDA(cudaMemcpyAsync(&nhk, hk_ctr.p, 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaMemcpyAsync(hkc, hk_ctr.p, 16, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
+    const int nhk = hkc[0];
     DBuf<RouteProblem> probs(std::max(nprob, 1));
     DBuf<RouteWorkItem> items(std::max(nitems, 1));
     DBuf<uint64_t> item_best(std::max(nitems, 1)), prob_best(std::max(nprob, 1));
@@ -1406,15 +1540,14 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
         count_launch();
         WR_LAUNCH_CHECK();
     }
-    if (nhk > 0) {   // 13-16-stop exact routes: persistent Held-Karp blocks, 12 MB of states each
-        int nsm = 0;
-        WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.device));
-        const int nblk = std::min(nhk, 4 * nsm);
-        const size_t states = (size_t)1 << HK_MAX;
-        DBuf<uint32_t> hk_cost((size_t)nblk * states * HK_MAX);
-        DBuf<unsigned long long> hk_key((size_t)nblk * states * HK_MAX);
-        route_hk_kernel<C><<<nblk, HK_THREADS, 0, st>>>(nord, ordr.p, Dall, P.stops.p, o_lo, d_res, d_counters,
-                                                        hk_ctr.p + 1, hk_cost.p, hk_key.p);
+    if (nhk > 0) {   // 13-16-stop exact routes: one order per 8-CTA cluster, L2-resident tables
+        const int nmax = hkc[2];
+        const int ncl = std::min(nhk, HK_CLUSTERS);
+        const size_t stride = ((size_t)1 << nmax) * HK_RS;
+        DBuf<uint32_t> ws((size_t)ncl * stride);
+        route_hk_kernel<C><<<ncl * HK_CL, HK_THREADS, 0, st>>>(hk_list.p, nhk, ordr.p, Dall, P.stops.p, o_lo, d_res,
+                                                               d_counters, hk_ctr.p + 1, ws.p, stride,
+                                                               hk_lists(P.device));
         count_launch();
         WR_LAUNCH_CHECK();
         WR_CUDA(cudaStreamSynchronize(st));   // workspace lifetime

@@ -24,7 +24,7 @@ def _cuda():
 class G:
     def __init__(self, V, src, dst, w, xy=None):
         self.V, self.src, self.dst, self.w = V, np.asarray(src, np.int32), np.asarray(dst, np.int32), np.asarray(w)
-        self.xy = xy
+        self.xy, self.z = xy, None
 
 
 def check_bf(g, sources, pred=True, variant=wr.WR_BF_AUTO, budget=0, targets=None):
@@ -128,6 +128,51 @@ def test_bf_negative_int_weights_and_negcycle():
             continue
         check_bf(g, srcs)
         done += 1
+
+
+def _neg_path(V=64, seed=11):
+    """Bidirectional path 0 - 1 - ... - V-1: forward arcs 1..3 with one -1,
+    backward arcs 5 (no negative cycle). From vertex 0 the shortest path to
+    V-1 has V-1 hops, so Bellman-Ford still improves in round V-1 and must
+    only stop after its check round V (§4.7, V-1 rounds)."""
+    rng = np.random.default_rng(seed)
+    fw = rng.integers(1, 4, V - 1).astype(np.int32)
+    fw[V // 2] = -1
+    src = list(range(V - 1)) + list(range(1, V))
+    dst = list(range(1, V)) + list(range(V - 1))
+    w = np.concatenate([fw, np.full(V - 1, 5, np.int32)])
+    return G(V, src, dst, w, xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+
+
+def test_bf_negative_weights_depth_v_minus_1():
+    """Round-1 false WR_ENEGCYCLE: V = 2 with the single arc 0->1 (w = -1),
+    and a 64-vertex path whose shortest path has V-1 hops; valid cycles
+    still report WR_ENEGCYCLE. Through wr_bf_batch and wr_route_orders."""
+    check_bf(G(2, [0], [1], np.array([-1], np.int32)), np.array([0, 1], np.int32))
+    g = _neg_path()
+    check_bf(g, np.array([0, 63, 31, 32], np.int32))
+    Gp = wr.Graph(g.V, g.src, g.dst, g.w, xy=g.xy)
+    _, _, st = wr.bf_batch(Gp, np.array([0], np.int32))
+    assert st.rounds_max >= g.V - 1
+
+    class O:
+        pass
+    orders = O()
+    nodes = np.array([0, 63, 10, 40, 5, 63, 1, 62], np.int32)
+    orders.order_ptr, orders.order_nodes, orders.B = np.array([0, 2, 5, 8], np.int64), nodes, 3
+    compare_orders(g, orders, m=1, G=Gp)
+    # the same path with a negative 2-cycle: 10 -> 11 (-1) -> 10 (-1)
+    w2 = g.w.copy()
+    w2[10] = -1
+    w2[63 + 10] = -1
+    Gc = wr.Graph(g.V, g.src, g.dst, w2, xy=g.xy)
+    with pytest.raises(oracle.OracleError):
+        oracle.bf_many(G(g.V, g.src, g.dst, w2, xy=g.xy), np.array([0], np.int32))
+    for call in (lambda: wr.bf_batch(Gc, np.array([0, 5], np.int32)),
+                 lambda: wr.route_orders(Gc, orders.order_ptr, orders.order_nodes)):
+        with pytest.raises(wr.WrError) as e:
+            call()
+        assert e.value.code == wr.WR_ENEGCYCLE
 
 
 def test_bf_targets_repeats_and_device_outputs():
@@ -268,6 +313,49 @@ def test_route_orders_held_karp_13_to_16(wtype):
     orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, len(sizes)
     res, st = compare_orders(g, orders, m=1)
     assert res["n"].tolist() == sizes
+
+
+def _absorption_graph(seed, near=24):
+    """fp32 graph whose stop distances make rounding ties (reading A16): a
+    complete digraph of `near` nodes with small weights (0.5 .. 3) and two
+    far nodes joined to every near node by ~1e8 arcs (ulp 8), so every route
+    through a far node absorbs the small prefix sums before its big leg."""
+    rng = np.random.default_rng(seed)
+    src, dst, w = [], [], []
+    small = np.array([0.5, 1, 1.5, 2, 3], np.float32)
+    for a in range(near):
+        for b in range(near):
+            if a != b:
+                src.append(a); dst.append(b); w.append(rng.choice(small))
+    for f in (near, near + 1):
+        for a in range(near):
+            src += [a, f]; dst += [f, a]
+            w += [np.float32(1e8) + np.float32(8 * rng.integers(0, 4)), np.float32(1e8) + np.float32(8 * rng.integers(0, 4))]
+    V = near + 2
+    return G(V, src, dst, np.array(w, np.float32), xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+
+
+def test_route_orders_held_karp_fp32_absorption():
+    """NEXT-2 with fp32 absorption ties: 13-16-stop orders through the far
+    nodes have many optimal orders whose prefixes differ in cost; the GPU
+    (forward DP, backward bound, greedy) must return the oracle's O5 answer."""
+    g = _absorption_graph(93)
+    rng = np.random.default_rng(94)
+    sizes = [13, 14, 15, 16] * 6
+    seqs = []
+    for k in sizes:
+        far = rng.choice([24, 25], int(rng.integers(1, 3)), replace=False)
+        near = rng.choice(24, k - far.size, replace=False)
+        seqs.append(np.sort(np.concatenate([near, far])))
+    nodes = np.concatenate(seqs).astype(np.int32)
+    ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, len(sizes)
+    res, st = compare_orders(g, orders, m=1)
+    assert (res["status"] == 0).all()
 
 
 def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
@@ -490,6 +578,8 @@ def test_sharded_phases_equal_single(world):
     parts = [p.finish(gathered)[0] for p in plans]
     got = np.concatenate(parts)
     assert got.tobytes() == ref.tobytes()
+    # and against the oracle directly (a9 parity, not only CUDA == CUDA)
+    compare_orders(g, orders, m=1, G=G, results=got)
 
 
 # ------------------------------------------------------------------ full size
