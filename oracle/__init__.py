@@ -59,10 +59,13 @@ def lib():
         L.orc_perm_rank.restype = C.c_longlong
         L.orc_route_count_reduction.argtypes = [C.c_int, vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]
         L.orc_bf_many.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int]
+        L.orc_pred_many.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
         L.orc_route_orders.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, vp, C.c_longlong,
                                        C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int]
         L.orc_certificate.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
         L.orc_certificate.restype = C.c_longlong
+        L.orc_pred_certificate.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, lp]
+        L.orc_pred_certificate.restype = C.c_longlong
     return _lib
 
 
@@ -139,6 +142,20 @@ def pred(g, s: int, dist):
     rc = lib().orc_pred(V, src.size, _p(src), _p(dst), _p(w), wt, int(s), _p(dist), _p(out))
     if rc:
         raise OracleError(rc, "pred")
+    return out
+
+
+def pred_many(g, sources, dist, nthreads: int = None):
+    """O3 for many rows (dist S x V from bf_many), on nthreads workers."""
+    V, src, dst, w = _graph(g)
+    wt = _wt(w)
+    sources = np.ascontiguousarray(sources, dtype=np.int32)
+    dist = np.ascontiguousarray(dist, dtype=_vdt(wt))
+    out = np.empty((sources.size, V), dtype=np.int32)
+    rc = lib().orc_pred_many(V, src.size, _p(src), _p(dst), _p(w), wt, _p(sources), sources.size, _p(dist),
+                             _p(out), nthreads or os.cpu_count())
+    if rc:
+        raise OracleError(rc, "pred_many")
     return out
 
 
@@ -289,3 +306,18 @@ def certificate(g, sources, dist, pred_rows=None, nthreads: int = None) -> int:
     pr = None if pred_rows is None else np.ascontiguousarray(pred_rows, dtype=np.int32)
     return lib().orc_certificate(V, src.size, _p(src), _p(dst), _p(w), wt, _p(sources), sources.size,
                                  _p(dist), _p(pr), nthreads or os.cpu_count())
+
+
+def pred_certificate(g, sources, pred_rows, nthreads: int = None):
+    """P9 from pred rows alone: (bad row count, first bad row or -1). A row
+    passes iff pred is a tree rooted at its source whose path sums satisfy
+    every arc (so they are the BF fixpoint) and pred is canonical (O3)."""
+    V, src, dst, w = _graph(g)
+    wt = _wt(w)
+    sources = np.ascontiguousarray(sources, dtype=np.int32)
+    pr = np.ascontiguousarray(pred_rows, dtype=np.int32)
+    assert pr.shape == (sources.size, V)
+    first = C.c_longlong(-1)
+    bad = lib().orc_pred_certificate(V, src.size, _p(src), _p(dst), _p(w), wt, _p(sources), sources.size,
+                                     _p(pr), nthreads or os.cpu_count(), C.byref(first))
+    return bad, first.value

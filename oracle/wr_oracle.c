@@ -47,6 +47,11 @@
  *   orc_order_stops   a2 stop projection (P226-238 §2.4) pinned: numpy unique.
  *   orc_route_orders  a2..a7 composed (per order), threads over sources/orders.
  *   orc_certificate   P9 fixpoint certificate for full-size GPU outputs.
+ *   orc_pred_certificate  P9 from pred rows alone (rebuilt path sums) + the
+ *                     O3 canonical rule; pinned: oracle rows pass, mutated
+ *                     rows (non-canonical tie, non-arc, cycle, dropped
+ *                     vertex, wrong root) fail.
+ *   orc_pred_many     O3 on many rows (threads only).
  */
 #include <math.h>
 #include <pthread.h>
@@ -859,6 +864,45 @@ int orc_bf_many(int V, long long E, const int *src, const int *dst, const void *
     return rc;
 }
 
+/* O3 for S rows at once: orc_pred per row on nthreads workers (threading  */
+/* only; every row is the plain sequential orc_pred above).                  */
+typedef struct {
+    int V; long long E; const int *src, *dst; const void *w; int wtype;
+    const int *sources; int S; const void *dist; int *pred; int *rc;
+    int next; pthread_mutex_t mu;
+} pred_job;
+
+static void *pred_worker(void *arg)
+{
+    pred_job *j = (pred_job *)arg;
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        int k = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (k >= j->S) break;
+        j->rc[k] = orc_pred(j->V, j->E, j->src, j->dst, j->w, j->wtype, j->sources[k],
+                            (const char *)j->dist + (size_t)4 * j->V * k, j->pred + (size_t)j->V * k);
+    }
+    return NULL;
+}
+
+int orc_pred_many(int V, long long E, const int *src, const int *dst, const void *w,
+                  int wtype, const int *sources, int S, const void *dist, int *pred, int nthreads)
+{
+    pred_job j = {V, E, src, dst, w, wtype, sources, S, dist, pred, NULL, 0, PTHREAD_MUTEX_INITIALIZER};
+    j.rc = (int *)calloc((size_t)(S > 0 ? S : 1), sizeof(int));
+    if (!j.rc) return ORC_ENOMEM;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, pred_worker, &j);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    int rc = ORC_OK;
+    for (int k = 0; k < S; ++k) if (j.rc[k]) { rc = j.rc[k]; break; }
+    free(j.rc);
+    return rc;
+}
+
 typedef struct {
     int wtype, V; const int *row_of; const void *rows;
     const long long *order_ptr; const int *order_nodes; long long B;
@@ -1051,6 +1095,149 @@ long long orc_certificate(int V, long long E, const int *src, const int *dst, co
     pthread_t th[256];
     for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, cert_worker, &j);
     for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(in_ptr); free(in_arc); free(fill);
+    return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* P9 from pred rows alone (full-size GPU outputs whose dist rows are not    */
+/* returned): per row, (a) pred must be a tree rooted at s (pred[s] = -1,    */
+/* every walk reaches s in <= V-1 steps); (b) rebuild d along it, d[s] = 0,  */
+/* d[v] = min over the arcs pred[v]->v of fl(d[pred[v]] + w) (a left-to-     */
+/* right path sum, so d >= the BF fixpoint); (c) every arc satisfies         */
+/* d[v] <= fl(d[u] + w) for finite d[u] (so d <= every path sum: d IS the    */
+/* fixpoint, unreachable vertices included); (d) pred is canonical (O3) for  */
+/* that d: the smallest steep tight tail; rows with a flat vertex or a       */
+/* negative weight are compared whole with orc_pred on the rebuilt d.        */
+/* Returns the number of rows failing; *first_bad = the first such row.      */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int V; long long E; const int *src, *dst; const void *w; int wtype; int has_neg;
+    const long long *in_ptr, *in_arc;
+    const int *sources; int S; const int *pred; long long *bad; long long first_bad;
+    int next; pthread_mutex_t mu;
+} pcert_job;
+
+static int pcert_row(pcert_job *j, int k, int *depth, int *stack, void *dv, int *canon)
+{
+    const int V = j->V, s = j->sources[k];
+    const int *p = j->pred + (size_t)V * k;
+    int *di = (int *)dv;
+    float *df = (float *)dv;
+    if (s < 0 || s >= V || p[s] != -1) return 1;
+    for (int v = 0; v < V; ++v) {
+        depth[v] = -1;
+        if (j->wtype == ORC_I32) di[v] = I32_INF; else df[v] = INFINITY;
+    }
+    depth[s] = 0;
+    if (j->wtype == ORC_I32) di[s] = 0; else df[s] = 0.0f;
+    /* (a) + (b): walk up to a vertex with known d, then assign down */
+    for (int v = 0; v < V; ++v) {
+        if (depth[v] >= 0 || p[v] == -1) continue;
+        int top = 0, x = v;
+        while (depth[x] == -1) {
+            if (p[x] < -1 || p[x] >= V) return 2;
+            if (p[x] == -1) return 3;             /* a walk ending at a root != s */
+            depth[x] = -2; stack[top++] = x; x = p[x];
+        }
+        if (depth[x] == -2) return 3;              /* cycle */
+        while (top > 0) {
+            int y = stack[--top], u = p[y], found = 0;
+            depth[y] = depth[u] + 1;
+            if (depth[y] > V - 1) return 3;
+            for (long long q = j->in_ptr[y]; q < j->in_ptr[y + 1]; ++q) {
+                long long e = j->in_arc[q];
+                if (j->src[e] != u) continue;
+                if (j->wtype == ORC_I32) {
+                    int64_t c = (int64_t)di[u] + ((const int *)j->w)[e];
+                    if (!found || c < di[y]) di[y] = (int)c;
+                } else {
+                    float c = df[u] + ((const float *)j->w)[e];
+                    if (!found || c < df[y]) df[y] = c;
+                }
+                found = 1;
+            }
+            if (!found) return 4;                  /* pred[y] -> y is not an arc */
+        }
+    }
+    /* (c) every arc */
+    for (long long e = 0; e < j->E; ++e) {
+        int u = j->src[e], v = j->dst[e];
+        if (!finite_at(j->wtype, dv, u)) continue;
+        if (j->wtype == ORC_I32) {
+            if ((int64_t)di[u] + ((const int *)j->w)[e] < (int64_t)di[v]) return 5;
+        } else {
+            float c = df[u] + ((const float *)j->w)[e];
+            if (c < df[v]) return 5;
+        }
+    }
+    /* (d) canonical */
+    int flat = j->has_neg;
+    for (int v = 0; v < V && !flat; ++v) {
+        if (v == s || p[v] < 0) continue;
+        int best = -1;
+        for (long long q = j->in_ptr[v]; q < j->in_ptr[v + 1]; ++q) {
+            long long e = j->in_arc[q];
+            int u = j->src[e];
+            if (tight_arc(j->wtype, dv, j->w, e, u, v) && less_at(j->wtype, dv, u, v) && (best < 0 || u < best))
+                best = u;
+        }
+        if (best < 0) flat = 1;
+        else if (best != p[v]) return 6;
+    }
+    if (flat) {
+        if (orc_pred(V, j->E, j->src, j->dst, j->w, j->wtype, s, dv, canon) != ORC_OK) return 7;
+        if (memcmp(canon, p, sizeof(int) * (size_t)V) != 0) return 6;
+    }
+    return 0;
+}
+
+static void *pcert_worker(void *arg)
+{
+    pcert_job *j = (pcert_job *)arg;
+    int *depth = (int *)malloc(sizeof(int) * (size_t)j->V);
+    int *stack = (int *)malloc(sizeof(int) * (size_t)j->V);
+    int *canon = (int *)malloc(sizeof(int) * (size_t)j->V);
+    void *dv = malloc((size_t)4 * j->V);
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        int k = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (k >= j->S) break;
+        if (pcert_row(j, k, depth, stack, dv, canon)) {
+            pthread_mutex_lock(&j->mu);
+            *j->bad += 1;
+            if (j->first_bad < 0 || k < j->first_bad) j->first_bad = k;
+            pthread_mutex_unlock(&j->mu);
+        }
+    }
+    free(depth); free(stack); free(canon); free(dv);
+    return NULL;
+}
+
+long long orc_pred_certificate(int V, long long E, const int *src, const int *dst, const void *w,
+                               int wtype, const int *sources, int S, const int *pred, int nthreads,
+                               long long *first_bad)
+{
+    long long *in_ptr = (long long *)calloc((size_t)V + 1, sizeof(long long));
+    long long *in_arc = (long long *)malloc(sizeof(long long) * (size_t)(E > 0 ? E : 1));
+    long long *fill = (long long *)malloc(sizeof(long long) * (size_t)V);
+    int has_neg = 0;
+    if (wtype == ORC_I32)
+        for (long long e = 0; e < E; ++e) if (((const int *)w)[e] < 0) has_neg = 1;
+    for (long long e = 0; e < E; ++e) in_ptr[dst[e] + 1]++;
+    for (int v = 0; v < V; ++v) in_ptr[v + 1] += in_ptr[v];
+    memcpy(fill, in_ptr, sizeof(long long) * (size_t)V);
+    for (long long e = 0; e < E; ++e) in_arc[fill[dst[e]]++] = e;
+    long long bad = 0;
+    pcert_job j = {V, E, src, dst, w, wtype, has_neg, in_ptr, in_arc, sources, S, pred, &bad, -1,
+                   0, PTHREAD_MUTEX_INITIALIZER};
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, pcert_worker, &j);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    if (first_bad) *first_bad = j.first_bad;
     free(in_ptr); free(in_arc); free(fill);
     return bad;
 }

@@ -361,3 +361,80 @@ def test_paper_mteps_arithmetic():
     assert visits == 262295285
     assert abs(visits / 2627e6 * 1e3 - 99.85) < 0.01
     assert math.ceil(26999 / 256) == 106
+
+
+# ------------------------------------------- P9 from pred rows (full-size tier)
+def _pc(g, srcs, P):
+    return oracle.pred_certificate(g, srcs, P, nthreads=2)
+
+
+def test_pred_certificate_accepts_oracle_rows():
+    """Oracle pred rows (O3 on Dijkstra-pinned BF rows) pass: int and fp32
+    aisle graphs, the worked example (pred ties), zero-weight flat vertices
+    and negative int weights (both compared whole against orc_pred)."""
+    cases = [gen.aisle(4, 10, 4, jitter_seed=3), gen.aisle(4, 10, 4, wtype="f32", jitter_seed=3),
+             gen.aisle(3, 4, 2, ws=1, wa=3, wd=2),
+             G(4, [0, 1, 2, 2], [1, 2, 1, 3], np.array([1, 0, 0, 0], dtype=np.int32)),
+             G(5, [0, 1, 2, 0, 3], [1, 2, 3, 3, 4], np.array([4, -1, -2, 2, 1], dtype=np.int32))]
+    for g in cases:
+        srcs = np.arange(g.V, dtype=np.int32)
+        rows = oracle.bf_many(g, srcs)
+        P = oracle.pred_many(g, srcs, rows)
+        for k in (0, g.V - 1):
+            assert np.array_equal(P[k], oracle.pred(g, int(srcs[k]), rows[k]))
+        assert _pc(g, srcs, P) == (0, -1)
+
+
+def test_pred_certificate_rejects_corruption():
+    """Each plausible GPU mistake fails the certificate: a non-canonical tie
+    (the larger of two tight tails, worked example P3), a non-arc pred, a
+    non-tight arc (a shortest-hop tree that is not a shortest-path tree), a
+    2-cycle, a dropped reachable vertex, a pred on the source, and a row
+    whose pred tree belongs to another source."""
+    rec = load_three_aisle()
+    g = gen.aisle(3, 4, 2, ws=1, wa=3, wd=2)
+    srcs = np.arange(g.V, dtype=np.int32)
+    rows = oracle.bf_many(g, srcs)
+    P = oracle.pred_many(g, srcs, rows)
+    # P3 tie: slot(0,2) -> slot(1,1) = 8 via the front and via the back cross
+    # node: both tails are steep and tight, the canonical pred is the smaller
+    s, v, p = next(t for t in rec["pred"] if t[0] == 2 and t[1] == 5)
+    tails = [int(u) for u, x, w in zip(g.src, g.dst, g.w) if x == v and rows[s][u] + w == rows[s][v]]
+    assert p == min(tails) and len(tails) >= 1
+    mut = []
+    bad = P.copy()
+    other = [u for u in range(g.V) if u not in tails and u != v]
+    alt = [t for t in rec["pred"] if t[0] == s]
+    # non-canonical: any vertex with two steep tight tails
+    for x in range(g.V):
+        tt = sorted(int(u) for u, y, w in zip(g.src, g.dst, g.w)
+                    if y == x and x != s and rows[s][u] + w == rows[s][x] and rows[s][u] < rows[s][x])
+        if len(tt) >= 2:
+            bad[s, x] = tt[1]
+            mut.append(bad)
+            break
+    assert mut, alt
+    nonarc = [u for u in other if not ((g.src == u) & (g.dst == v)).any()]
+    bad = P.copy(); bad[s, v] = nonarc[0]; mut.append(bad)
+    loose = [(int(u), int(x)) for u, x, w in zip(g.src, g.dst, g.w)
+             if x != s and rows[s][u] + w > rows[s][x]]
+    bad = P.copy(); bad[s, loose[0][1]] = loose[0][0]; mut.append(bad)   # real arc, not tight
+    a, b = int(g.src[0]), int(g.dst[0])
+    bad = P.copy(); bad[s, a] = b; bad[s, b] = a; mut.append(bad)    # 2-cycle (or wrong root)
+    bad = P.copy(); bad[s, v] = -1; mut.append(bad)                  # reachable v dropped
+    bad = P.copy(); bad[s, s] = int(P[s, v]); mut.append(bad)        # pred on the source
+    bad = P.copy(); bad[s] = P[(s + 1) % g.V]; mut.append(bad)       # another source's tree
+    for k, m in enumerate(mut):
+        assert _pc(g, srcs, m) == (1, s), k
+    # fp32: one ulp-wrong rebuilt sum cannot hide: a tree via a costlier tail
+    gf = gen.aisle(4, 10, 4, wtype="f32", jitter_seed=9)
+    sf = np.array([0, 17], dtype=np.int32)
+    rf = oracle.bf_many(gf, sf)
+    Pf = oracle.pred_many(gf, sf, rf)
+    x = 20
+    cand = [int(u) for u, y in zip(gf.src, gf.dst) if y == x and u != Pf[1, x]]
+    ok = 0
+    for u in cand:
+        bad = Pf.copy(); bad[1, x] = u
+        ok += _pc(gf, sf, bad) == (1, 1)
+    assert ok == len(cand)
