@@ -206,39 +206,35 @@ def main():
     stream = torch.cuda.current_stream()
 
     rflags = wr.WR_ROUTE_PAIRS if a.pairs else 0
+    # N > 1: libwr's own context (NCCL communicator bootstrapped over the
+    # process group): wr_route_orders shards sources and orders and runs the
+    # all-gather of the owned D entries inside the call; each rank keeps its
+    # own block of the results (WR_ROUTE_RANK_RESULTS)
+    ctx = wr.Ctx.from_process_group(local) if world > 1 else None
+    if world > 1:
+        rflags |= wr.WR_ROUTE_RANK_RESULTS
     plan0 = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, flags=rflags)
     info = plan0.info
     n_my = info.order_hi - info.order_lo
-    d_res = torch.empty((max(n_my, 1), wr.RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    d_res = torch.empty((max(B, 1), wr.RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
     pred_buf = None
     if not a.no_pred:
         pred_buf = torch.empty((max(int(info.src_hi - info.src_lo), 1), g.V), dtype=torch.int32, device=dev)
-    send = torch.empty(info.max_send, dtype=torch.int32, device=dev)
-    gathered = torch.empty(world * info.max_send, dtype=torch.int32, device=dev) if world > 1 else send
     plan0.close()
     launches = [0]
     bf_ms = [0.0]
     relax = [0]
     row_bits = [32]
+    tiles = [0, 0]
 
     def step():
-        if world == 1:
-            _, st = wr.route_orders(G, d_ptr, d_nodes, m=a.m, results=d_res, stream=stream, pred_out=pred_buf,
-                                    flags=rflags)
-            launches[0] += st.kernel_launches
-            bf_ms[0] += st.bf_ms
-            relax[0] += st.relaxations
-            row_bits[0] = st.row_bits
-            return
-        p = wr.OrdersPlan(G, d_ptr, d_nodes, rank, world, m=a.m, stream=stream, pred_out=pred_buf, flags=rflags)
-        s1 = p.local(send)
-        dist.all_gather_into_tensor(gathered, send)
-        _, s2 = p.finish(gathered, results=d_res)
-        launches[0] += s1.kernel_launches + s2.kernel_launches
-        bf_ms[0] += s1.bf_ms
-        relax[0] += s1.relaxations
-        row_bits[0] = s1.row_bits
-        p.close()
+        _, st = wr.route_orders(G, d_ptr, d_nodes, m=a.m, results=d_res, stream=stream, pred_out=pred_buf,
+                                flags=rflags, ctx=ctx)
+        launches[0] += st.kernel_launches
+        bf_ms[0] += st.bf_ms
+        relax[0] += st.relaxations
+        row_bits[0] = st.row_bits
+        tiles[0], tiles[1] = st.tiles, st.tile_sources
 
     def barrier():
         torch.cuda.synchronize()
@@ -274,19 +270,11 @@ def main():
     if not a.no_e2e:
         h_ptr = torch.from_numpy(orders.order_ptr).pin_memory()
         h_nodes = torch.from_numpy(orders.order_nodes).pin_memory()
-        h_res = np.zeros(max(n_my, 1), dtype=wr.RESULT_DTYPE)
+        h_res = np.zeros(max(B, 1), dtype=wr.RESULT_DTYPE)
 
         def e2e_step():
-            if world == 1:
-                wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream, flags=rflags,
-                                pred_out=pred_buf)
-                return
-            p = wr.OrdersPlan(G, h_ptr.numpy(), h_nodes.numpy(), rank, world, m=a.m, stream=stream, flags=rflags,
-                              pred_out=pred_buf)
-            p.local(send)
-            dist.all_gather_into_tensor(gathered, send)
-            p.finish(gathered, results=h_res)
-            p.close()
+            wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream, flags=rflags,
+                            pred_out=pred_buf, ctx=ctx)
 
         for _ in range(2):
             e2e_step()
@@ -307,6 +295,8 @@ def main():
                "h2d_bytes_per_step": int(orders.order_ptr.nbytes + orders.order_nodes.nbytes),
                "d2h_bytes_per_step": int(n_my * wr.RESULT_DTYPE.itemsize) * world, "ms_per_step": ems}
 
+    if ctx is not None:
+        ctx.close()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -320,11 +310,14 @@ def main():
     # + read the graph (in-arcs (u, w) 8E, out-arcs 4E, offsets 8V) once per
     # tile (128 sources, 256 packed).
     rb = row_bits[0] or 32
-    alg_bytes = S * (g.V * rb // 8) + (S / (128.0 * 32 / rb)) * (12 * E + 8 * g.V)
+    # this rank's sources and the tiles its sweep actually ran (the tile
+    # width follows choose_spl, narrower on shards)
+    S_rank = int(info.src_hi - info.src_lo)
+    alg_bytes = S_rank * (g.V * rb // 8) + tiles[0] * (12 * E + 8 * g.V)
     if not a.no_pred:
         # the canonical-pred pass (a4) runs fused inside the same kernel: it
         # reads every distance once more and writes every int32 pred once
-        alg_bytes += S * g.V * (rb // 8 + 4)
+        alg_bytes += S_rank * g.V * (rb // 8 + 4)
     bf_s = bf_step_ms / 1e3
     achieved = alg_bytes / bf_s / 1e9 if bf_s > 0 else None
     traffic = None

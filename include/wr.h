@@ -18,8 +18,13 @@
  *  - Pointers may be host or device memory (detected with
  *    cudaPointerGetAttributes); device pointers must live on the graph's
  *    device. Host pointers may be pageable or pinned.
- *  - Calls are blocking unless opts.async = 1 and every output is device
- *    memory, in which case results are ordered on opts.stream.
+ *  - Calls are blocking by default. wr_bf_batch with opts.async = 1 and
+ *    device outputs returns once its kernels are enqueued on opts.stream
+ *    (results are stream-ordered; see wr_bf_opts.async for what it skips);
+ *    the route calls are always blocking (their host-side plan needs the
+ *    device's stop counts).
+ *  - Every entry point opens an NVTX range named after it (nested ranges for
+ *    the sweep, pred and route phases), visible to nsys / ncu --nvtx.
  *  - Sentinels: int32 INF = INT32_MAX, fp32 INF = +inf, pred NONE = -1,
  *    dist[s][s] = 0 (+0.0f).
  *  - Arithmetic: int32 sums are exact; fp32 sums are single IEEE-754
@@ -44,7 +49,7 @@ typedef int32_t wr_status;
 #define WR_EUNREACHABLE 5  /* stops of an order are not mutually reachable   */
 #define WR_ETOOLARGE 6     /* problem exceeds a documented size limit        */
 #define WR_ECUDA 7         /* CUDA runtime error                             */
-#define WR_ENCCL 8         /* reserved (the exchange runs in torch.distributed) */
+#define WR_ENCCL 8         /* NCCL failure (wr_ctx communicator / collectives) */
 #define WR_EINTERNAL 9
 
 #define WR_I32 0           /* int32 weights / distances                      */
@@ -69,6 +74,22 @@ int32_t wr_version(void);
  * cached block to the driver (e.g. before handing the memory to another
  * allocator). */
 wr_status wr_release_cached(int32_t device);
+
+/* ------------------------------------------------ multi-GPU context (a9) -- */
+/* One context per process and GPU, owning an NCCL
+ * communicator over `world` ranks. Rank 0 calls wr_nccl_unique_id and the
+ * caller broadcasts the 128 bytes to every rank (e.g. torch.distributed
+ * broadcast_object_list); every rank then calls wr_ctx_create with its rank.
+ * world = 1 may pass NULL (a private one-rank communicator). Calls that take
+ * a context (wr_route_opts.ctx, wr_bf_opts.ctx + shard) are collective: all
+ * ranks make the same call with the same inputs. NCCL is loaded at run time
+ * (libnccl.so.2); failures map to WR_ENCCL. */
+#define WR_NCCL_UID_BYTES 128
+typedef struct wr_ctx wr_ctx;
+wr_status wr_nccl_unique_id(void *uid_out);
+wr_status wr_ctx_create(int32_t rank, int32_t world, const void *nccl_uid, int32_t device, wr_ctx **out);
+wr_status wr_ctx_free(wr_ctx *ctx);
+wr_status wr_ctx_info(const wr_ctx *ctx, int32_t *rank, int32_t *world, int32_t *device);
 
 /* ---------------------------------------------------------------- graphs -- */
 /* a1 Graph ingest (P721 §4.7: "edge-list format using integer arrays u, v,
@@ -128,7 +149,13 @@ wr_status wr_graph_info(const wr_graph *g, wr_graph_info_t *info);
 
 typedef struct {
     void *stream;            /* cudaStream_t; NULL = default stream          */
-    int32_t async;           /* 1: device outputs, no host sync              */
+    int32_t async;           /* 1 with device dist/pred (or NULL), a graph
+                                without negative weights and default
+                                max_rounds: the call returns once the sweep
+                                and output kernels are enqueued (no host sync
+                                after the tiles are built); stats then hold
+                                only segments/tiles/kernel_launches, ms = -1.
+                                Otherwise ignored (blocking).               */
     int32_t variant;         /* WR_BF_*                                      */
     int32_t max_rounds;      /* relaxation rounds, 0 = V-1 (P724 §4.7); one
                                 more round checks convergence: if it still
@@ -137,6 +164,13 @@ typedef struct {
                                 WR_EINTERNAL (caller's max_rounds too small) */
     int64_t hbm_budget;      /* working-set bytes per segment; 0 = 180e9,
                                 clamped to 90 % of free device memory (a8)  */
+    wr_ctx *ctx;             /* optional multi-GPU context                  */
+    int32_t shard;           /* 1 (needs ctx): rank r relaxes its contiguous
+                                block of the S sources (wr_shard_range) and
+                                the dist / pred row blocks are exchanged over
+                                NCCL: every rank returns all S rows,
+                                identical to an unsharded call              */
+    int32_t reserved;        /* must be 0                                   */
 } wr_bf_opts;
 
 typedef struct {
@@ -194,6 +228,9 @@ typedef struct {
     int64_t pred_rows;       /* rows available in pred_out (>= src_hi-src_lo) */
     int32_t flags;           /* WR_ROUTE_* bits, 0 = defaults               */
     int32_t reserved;        /* must be 0                                   */
+    wr_ctx *ctx;             /* wr_route_orders only: NULL = this GPU alone;
+                                a context shards the sources and orders over
+                                its world (collective call, see below)      */
 } wr_route_opts;
 
 /* wr_route_opts.flags: keep the Bellman-Ford working rows in 32 bits even
@@ -209,6 +246,9 @@ typedef struct {
  * lexicographically smallest sequence. Segments <= 9 stops and
  * m'! * prod n_j (n_j - 1) <= 2^26 candidates, else WR_ETOOLARGE. */
 #define WR_ROUTE_PAIRS 2
+/* wr_route_opts.flags, with a context: write only this rank's block
+ * [order_lo, order_hi) of the results (skips the result exchange). */
+#define WR_ROUTE_RANK_RESULTS 4
 
 typedef struct {
     int32_t n;               /* stops (distinct nodes, ascending before routing) */
@@ -234,7 +274,12 @@ typedef struct {
     int64_t visits;           /* BF candidate visits                         */
     int32_t row_bits;         /* BF working-row element width: 16 (packed,
                                  exact) or 32                                */
-    int32_t reserved;
+    int32_t keyed;            /* 1: the 16-bit rows carried (d << 4 | pred
+                                 in-arc index) keys, so the fused pred pass
+                                 only decoded them              */
+    int64_t tiles;            /* BF source tiles swept (this rank)           */
+    int32_t tile_sources;     /* sources per tile (row width)                */
+    int32_t reserved2;
 } wr_route_stats;
 
 /* a7 Segmented route of one stop set (Theorem 3.1, P324-337 §3).
@@ -247,15 +292,27 @@ wr_status wr_route_segmented(const wr_graph *g, const int32_t *stops, int32_t n,
                              const int32_t *labels, int32_t m, const wr_route_opts *opts,
                              wr_route_result *out);
 
-/* a2..a7 for a batch of orders (the production path, "routed orders/sec").
+/* a2..a9 for a batch of orders (the production path, "routed orders/sec").
  *   order_ptr  B+1 int64 offsets into order_nodes
  *   order_nodes location node of each order line (P226-238 §2.4: lines at
  *              the same node are one stop)
+ *   labels     optional segment label (>= 0) of each order line, aligned with
+ *              order_nodes; lines at the same node must carry the same label
+ *              (else WR_EINVAL). Given labels route every order by the stitch
+ *              over the caller's segments (O7, or the pair stitch with
+ *              WR_ROUTE_PAIRS; <= WR_MAX_SEGMENTS labels per order); NULL:
+ *              opts.m decides (exact, or O8 K-means segments)
  *   results    B wr_route_result (host or device)
- * opts.m selects exact or segmented routing for every order. */
+ * With opts.ctx (world W): rank r relaxes its block of the sorted distinct
+ * stops, the owned D entries are all-gathered over NCCL on opts.stream, rank
+ * r routes orders [order_lo, order_hi) (wr_shard_range) and the result
+ * blocks are exchanged (grouped broadcasts) unless WR_ROUTE_RANK_RESULTS:
+ * every rank's results equal the single-GPU call bit for bit. pred_out then
+ * receives the rank's own source block (row 0 = its src_lo). stats are the
+ * calling rank's. */
 wr_status wr_route_orders(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes,
-                          int64_t B, const wr_route_opts *opts, wr_route_result *results,
-                          wr_route_stats *stats);
+                          int64_t B, const int32_t *labels, const wr_route_opts *opts,
+                          wr_route_result *results, wr_route_stats *stats);
 
 /* O8 default segment plan for n points (labels in [0, min(m, n))). */
 wr_status wr_segment_plan(const int32_t *xy, int32_t n, int32_t m, int32_t *labels_out,
@@ -287,9 +344,10 @@ typedef struct {
     int32_t wtype;
 } wr_plan_info_t;
 
+/* labels: as in wr_route_orders (per order line, or NULL). */
 wr_status wr_orders_plan(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes,
-                         int64_t B, int32_t rank, int32_t world, const wr_route_opts *opts,
-                         wr_plan **out);
+                         int64_t B, const int32_t *labels, int32_t rank, int32_t world,
+                         const wr_route_opts *opts, wr_plan **out);
 wr_status wr_plan_info(const wr_plan *p, wr_plan_info_t *info);
 /* send: device buffer of >= max_send 32-bit elements. */
 wr_status wr_orders_local(wr_plan *p, void *send, const wr_route_opts *opts, wr_route_stats *stats);

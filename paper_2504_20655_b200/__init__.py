@@ -24,6 +24,8 @@ WR_COO, WR_CSR = 0, 1
 WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE = 0, 1, 2
 WR_ROUTE_ROWS32 = 1
 WR_ROUTE_PAIRS = 2
+WR_ROUTE_RANK_RESULTS = 4
+NCCL_UID_BYTES = 128
 MAX_STOPS = 16
 DEFAULT_CHUNK = 2903040
 I32_INF = np.iinfo(np.int32).max
@@ -32,7 +34,7 @@ EXPORTS = [
     "wr_last_error", "wr_version", "wr_graph_load", "wr_graph_free", "wr_graph_info", "wr_bf_batch",
     "wr_route_cost", "wr_route_segmented", "wr_route_orders", "wr_segment_plan", "wr_route_count_reduction",
     "wr_orders_plan", "wr_plan_info", "wr_orders_local", "wr_orders_finish", "wr_plan_free", "wr_shard_range",
-    "wr_release_cached",
+    "wr_release_cached", "wr_nccl_unique_id", "wr_ctx_create", "wr_ctx_free", "wr_ctx_info",
 ]
 
 
@@ -56,7 +58,8 @@ class GraphInfo(C.Structure):
 
 class BfOpts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("async_", C.c_int32), ("variant", C.c_int32),
-                ("max_rounds", C.c_int32), ("hbm_budget", C.c_int64)]
+                ("max_rounds", C.c_int32), ("hbm_budget", C.c_int64), ("ctx", C.c_void_p), ("shard", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class BfStats(C.Structure):
@@ -68,7 +71,7 @@ class BfStats(C.Structure):
 class RouteOpts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("async_", C.c_int32), ("m", C.c_int32), ("chunk", C.c_int64),
                 ("hbm_budget", C.c_int64), ("pred_out", C.c_void_p), ("pred_rows", C.c_int64),
-                ("flags", C.c_int32), ("reserved", C.c_int32)]
+                ("flags", C.c_int32), ("reserved", C.c_int32), ("ctx", C.c_void_p)]
 
 
 class RouteStats(C.Structure):
@@ -76,7 +79,8 @@ class RouteStats(C.Structure):
                 ("stitch_candidates", C.c_int64), ("segments", C.c_int32), ("rounds_max", C.c_int32),
                 ("relaxations", C.c_int64), ("ms", C.c_float), ("kernel_launches", C.c_int64),
                 ("bf_ms", C.c_float), ("pred_ms", C.c_float), ("visits", C.c_int64),
-                ("row_bits", C.c_int32), ("reserved", C.c_int32)]
+                ("row_bits", C.c_int32), ("keyed", C.c_int32), ("tiles", C.c_int64), ("tile_sources", C.c_int32),
+                ("reserved2", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -105,10 +109,14 @@ def _load():
     lib.wr_bf_batch.argtypes = [vp, vp, i32, vp, i32, vp, vp, P(BfOpts), P(BfStats)]
     lib.wr_route_cost.argtypes = [i32, vp, i32, vp, i32, i64, vp, vp]
     lib.wr_route_segmented.argtypes = [vp, vp, i32, vp, i32, P(RouteOpts), vp]
-    lib.wr_route_orders.argtypes = [vp, vp, vp, i64, P(RouteOpts), vp, P(RouteStats)]
+    lib.wr_route_orders.argtypes = [vp, vp, vp, i64, vp, P(RouteOpts), vp, P(RouteStats)]
     lib.wr_segment_plan.argtypes = [vp, i32, i32, vp, i32]
     lib.wr_route_count_reduction.argtypes = [i32, vp, P(C.c_uint64), P(C.c_uint64)]
-    lib.wr_orders_plan.argtypes = [vp, vp, vp, i64, i32, i32, P(RouteOpts), P(vp)]
+    lib.wr_orders_plan.argtypes = [vp, vp, vp, i64, vp, i32, i32, P(RouteOpts), P(vp)]
+    lib.wr_nccl_unique_id.argtypes = [vp]
+    lib.wr_ctx_create.argtypes = [i32, i32, vp, i32, P(vp)]
+    lib.wr_ctx_free.argtypes = [vp]
+    lib.wr_ctx_info.argtypes = [vp, P(i32), P(i32), P(i32)]
     lib.wr_plan_info.argtypes = [vp, P(PlanInfo)]
     lib.wr_orders_local.argtypes = [vp, vp, P(RouteOpts), P(RouteStats)]
     lib.wr_orders_finish.argtypes = [vp, vp, vp, P(RouteOpts), P(RouteStats)]
@@ -118,7 +126,8 @@ def _load():
     lib.wr_release_cached.argtypes = [i32]
     for name in ["wr_release_cached", "wr_graph_load", "wr_graph_free", "wr_graph_info", "wr_bf_batch", "wr_route_cost",
                  "wr_route_segmented", "wr_route_orders", "wr_segment_plan", "wr_route_count_reduction",
-                 "wr_orders_plan", "wr_plan_info", "wr_orders_local", "wr_orders_finish", "wr_plan_free"]:
+                 "wr_orders_plan", "wr_plan_info", "wr_orders_local", "wr_orders_finish", "wr_plan_free",
+                 "wr_nccl_unique_id", "wr_ctx_create", "wr_ctx_free", "wr_ctx_info"]:
         getattr(lib, name).restype = i32
     return lib
 
@@ -243,11 +252,15 @@ class Graph:
 
 
 def bf_batch(g: Graph, sources, targets=None, pred: bool = False, dist_out=None, pred_out=None,
-             variant=WR_BF_AUTO, max_rounds=0, hbm_budget=0, stream=None):
+             variant=WR_BF_AUTO, max_rounds=0, hbm_budget=0, stream=None, async_: bool = False,
+             ctx: "Ctx" = None, shard: bool = False):
     """a3/a4: dist (S x T) and optional canonical pred (S x V).
 
     numpy in -> numpy out (host buffers); pass device tensors in dist_out /
-    pred_out to keep results on the GPU. Returns (dist, pred, stats)."""
+    pred_out to keep results on the GPU. async_: with device outputs, return
+    once the kernels are enqueued on `stream` (wr_bf_opts.async). ctx +
+    shard: the sources are split over the context's ranks and every rank
+    receives all rows. Returns (dist, pred, stats)."""
     src = _arr(sources, np.int32)
     S = int(src.shape[0])
     tg = _arr(targets, np.int32) if targets is not None else None
@@ -256,7 +269,8 @@ def bf_batch(g: Graph, sources, targets=None, pred: bool = False, dist_out=None,
         dist_out = np.empty((S, T), dtype=g.vdtype)
     if pred and pred_out is None:
         pred_out = np.empty((S, g.V), dtype=np.int32)
-    o = BfOpts(_stream_ptr(stream), 0, variant, max_rounds, hbm_budget)
+    o = BfOpts(_stream_ptr(stream), 1 if async_ else 0, variant, max_rounds, hbm_budget,
+               ctx.handle if ctx is not None else None, 1 if shard else 0, 0)
     st = BfStats()
     _check(lib.wr_bf_batch(g.handle, _ptr(src), S, _ptr(tg), T if tg is not None else 0, _ptr(dist_out),
                            _ptr(pred_out) if pred else None, C.byref(o), C.byref(st)))
@@ -295,22 +309,71 @@ def route_segmented(g: Graph, stops, labels=None, m: int = 1, chunk: int = 0, st
 
 
 def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, results=None,
-                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0):
-    """a2..a7: route every order. Returns (results, stats); results is a
+                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0, labels=None,
+                 ctx: "Ctx" = None):
+    """a2..a9: route every order. Returns (results, stats); results is a
     RESULT_DTYPE numpy array unless a device buffer is passed. pred_out: an
     optional device int32 tensor (>= S rows x V) receiving the canonical
-    predecessor rows (a4) of the distinct stops in ascending order
-    (OrdersPlan: the rank's own block of sources, row 0 = its src_lo)."""
+    predecessor rows (a4) of the distinct stops in ascending order (with a
+    ctx: the rank's own block of sources, row 0 = its src_lo). labels: an
+    optional segment label per order line (stitched routes over the
+    caller's segments). ctx: shard over the context's ranks (collective)."""
     ptr = _arr(order_ptr, np.int64)
     nodes = _arr(order_nodes, np.int32)
+    lab = _arr(labels, np.int32) if labels is not None else None
     B = int(ptr.shape[0]) - 1
     if results is None:
         results = np.zeros(B, dtype=RESULT_DTYPE)
     o = RouteOpts(_stream_ptr(stream), 0, m, chunk, hbm_budget, _ptr(pred_out),
-                  int(pred_out.shape[0]) if pred_out is not None else 0, flags)
+                  int(pred_out.shape[0]) if pred_out is not None else 0, flags, 0,
+                  ctx.handle if ctx is not None else None)
     st = RouteStats()
-    _check(lib.wr_route_orders(g.handle, _ptr(ptr), _ptr(nodes), B, C.byref(o), _ptr(results), C.byref(st)))
+    _check(lib.wr_route_orders(g.handle, _ptr(ptr), _ptr(nodes), B, _ptr(lab), C.byref(o), _ptr(results),
+                               C.byref(st)))
     return results, st
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for wr_ctx_create (rank 0 makes it, the caller
+    broadcasts it, e.g. torch.distributed.broadcast_object_list)."""
+    buf = C.create_string_buffer(NCCL_UID_BYTES)
+    _check(lib.wr_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Ctx:
+    """a9: libwr's multi-GPU context (wr_ctx): one per process and GPU,
+    owning an NCCL communicator over `world` ranks."""
+
+    def __init__(self, rank: int = 0, world: int = 1, uid: bytes = None, device: int = 0):
+        h = C.c_void_p()
+        ub = C.create_string_buffer(uid, NCCL_UID_BYTES) if uid is not None else None
+        _check(lib.wr_ctx_create(rank, world, ub, device, C.byref(h)))
+        self.handle = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def from_process_group(cls, device: int = None):
+        """Bootstraps the communicator over torch.distributed (any backend):
+        rank 0's unique id is broadcast to every rank."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dev = torch.cuda.current_device() if device is None else device
+        return cls(rank, world, obj[0], dev)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.wr_ctx_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def segment_plan(xy, m: int, device: int = 0):
@@ -332,14 +395,15 @@ class OrdersPlan:
     (caller, torch.distributed) -> finish (route this rank's order block)."""
 
     def __init__(self, g: Graph, order_ptr, order_nodes, rank: int, world: int, m: int = 1, chunk: int = 0,
-                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0):
+                 hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0, labels=None):
         self.g = g
         ptr = _arr(order_ptr, np.int64)
         nodes = _arr(order_nodes, np.int32)
+        lab = _arr(labels, np.int32) if labels is not None else None
         self.opts = RouteOpts(_stream_ptr(stream), 0, m, chunk, hbm_budget, _ptr(pred_out),
                               int(pred_out.shape[0]) if pred_out is not None else 0, flags)
         h = C.c_void_p()
-        _check(lib.wr_orders_plan(g.handle, _ptr(ptr), _ptr(nodes), int(ptr.shape[0]) - 1, rank, world,
+        _check(lib.wr_orders_plan(g.handle, _ptr(ptr), _ptr(nodes), int(ptr.shape[0]) - 1, _ptr(lab), rank, world,
                                   C.byref(self.opts), C.byref(h)))
         self.handle = h
         self.info = PlanInfo()

@@ -36,8 +36,25 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles each translation unit in parallel (no relocatable device
+    code: every kernel lives in one .cu), then links libwr.so."""
     if force or needs_build():
-        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + SOURCES
+        from concurrent.futures import ThreadPoolExecutor
+        objdir = os.path.join(HERE, "build")
+        os.makedirs(objdir, exist_ok=True)
+        compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+        objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in SOURCES]
+
+        def one(pair):
+            src, obj = pair
+            cmd = [nvcc()] + compile_flags + ["-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.check_call(cmd)
+
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            list(ex.map(one, zip(SOURCES, objs)))
+        cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -45,7 +45,8 @@ constexpr uint32_t FULL = 0xffffffffu;
 // relaxes nothing, exactly like the oracle's "skip d[u] == INF".
 struct OpU32 {
     static constexpr int PACK = 1;   // sources per 32-bit word
-    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    static constexpr bool KEYED = false;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w, int) { return w; }
     __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
     __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
     __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
@@ -70,7 +71,8 @@ struct OpU32 {
 // tails give +inf, which never wins.
 struct OpF32 {
     static constexpr int PACK = 1;   // sources per 32-bit word
-    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    static constexpr bool KEYED = false;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w, int) { return w; }
     __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
     __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
     __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
@@ -95,7 +97,8 @@ struct OpF32 {
 // int32 with negative weights: exact 64-bit candidate, INF tails skipped.
 struct OpI32N {
     static constexpr int PACK = 1;   // sources per 32-bit word
-    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) { return w; }
+    static constexpr bool KEYED = false;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w, int) { return w; }
     __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return less(a, b) ? a : b; }
     __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return less(a, b); }
     __device__ __forceinline__ static bool overflow(uint32_t, uint32_t) { return false; }
@@ -126,10 +129,12 @@ struct OpI32N {
 // redoes the segment with 32-bit rows, so results are exact either way.
 struct OpU16 {
     static constexpr int PACK = 2;
+    static constexpr bool KEYED = false;
     static constexpr uint32_t INF = 0x7fff7fffu;
     static constexpr uint32_t INF1 = 0x7fffu;
     static constexpr uint32_t ZERO = 0u;
-    __device__ __forceinline__ static uint32_t prep_w(uint32_t w) {
+    static constexpr uint16_t SEED16 = 0;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w, int) {
         w = min(w, 0x7fffu);
         return w | (w << 16);
     }
@@ -146,6 +151,51 @@ struct OpU16 {
     __device__ __forceinline__ static bool finite(uint32_t x1) { return x1 != INF1; }
     __device__ __forceinline__ static bool steep_tight(uint32_t du1, uint32_t w, uint32_t dv1) {
         return w != 0u && du1 + w == dv1;   // w > 0 on every packed graph
+    }
+};
+
+// Keyed packed rows (the routing path with fused pred): each u16 half holds
+// key = d << 4 | k, where k is the in-arc index (in v's CSC range, sorted by
+// tail) of the arc that set d - the canonical pred (O3: the smallest steep
+// tight tail; with every weight >= 1 each tight arc is steep) rides along
+// with the distance, so the pred pass only decodes k instead of re-testing
+// every in-arc of every vertex against the final distances. One add-min
+// per relaxation relaxes both: c = (x | 0xf) + ((w << 4) + k - 15) strips
+// the tail's own k and appends this arc's, and min over keys is min over
+// d, ties -> smallest k (smallest tail). Every tight arc is offered to v
+// after its tail's last change (delta pull), so the final key holds the
+// smallest tight k whatever the schedule (min is order-free). k = 15 is
+// NONE: the seed key 0x000f (d = 0, source) and INF 0x7fff (unreachable)
+// decode to pred -1. Needs in-degree <= 15, w in [1, 0x7ff], d < 0x7ff
+// (a stored distance reaching 0x7ff - max_w raises the overflow flag and
+// the phase is redone with plain packed, then 32-bit rows).
+struct OpK16 {
+    static constexpr int PACK = 2;
+    static constexpr bool KEYED = true;
+    static constexpr uint32_t INF = 0x7fff7fffu;
+    static constexpr uint32_t INF1 = 0x7fffu;
+    static constexpr uint32_t ZERO = 0x000f000fu;
+    static constexpr uint16_t SEED16 = 0x000f;
+    __device__ __forceinline__ static uint32_t prep_w(uint32_t w, int k) {
+        const uint32_t x = (min(w, 0x7ffu) << 4) + (uint32_t)k - 15u;   // w >= 1: x >= 1
+        return x | (x << 16);
+    }
+    __device__ __forceinline__ static uint32_t relax(uint32_t d, uint32_t du, uint32_t w2) {
+        return __viaddmin_u16x2(du | 0x000f000fu, w2, d);
+    }
+    __device__ __forceinline__ static uint32_t min_word(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+    __device__ __forceinline__ static bool any_less(uint32_t a, uint32_t b) { return __vcmpltu2(a, b) != 0u; }
+    // a distance (not only a pred) improved: what the delta pull propagates
+    __device__ __forceinline__ static bool dist_less(uint32_t a, uint32_t b) {
+        return __vcmpltu2(a | 0x000f000fu, b | 0x000f000fu) != 0u;
+    }
+    __device__ __forceinline__ static bool overflow(uint32_t d, uint32_t thr2) {
+        return (__vcmpgeu2(d, thr2) & ~__vcmpeq2(d, INF)) != 0u;
+    }
+    __device__ __forceinline__ static uint32_t half(uint32_t x, int h) { return (x >> (16 * h)) & 0xffffu; }
+    __device__ __forceinline__ static bool finite(uint32_t x1) { return x1 != INF1; }
+    __device__ __forceinline__ static bool steep_tight(uint32_t du1, uint32_t w, uint32_t dv1) {
+        return w != 0u && (du1 >> 4) + w == (dv1 >> 4);
     }
 };
 
@@ -236,7 +286,7 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
         bool take = false;
         if (lane < cnt) {
             my_u = g.in_src[base + lane];
-            my_w = Op::prep_w(g.in_w[base + lane]);
+            my_w = Op::prep_w(g.in_w[base + lane], base - a0 + lane);
             take = !DELTA || pchg.test(my_u);
         }
         uint32_t m = __ballot_sync(FULL, take);
@@ -316,7 +366,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         for (int j = 0; j < AQ; ++j) {
             const bool take = arc[j].x >= 0 && (!DELTA || pchg.test(arc[j].x));
             // queued: the tail row's word offset (u * TSW < 2^31) and the prepared weight
-            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x * TSW, (int)Op::prep_w((uint32_t)arc[j].y));
+            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x * TSW, (int)Op::prep_w((uint32_t)arc[j].y, k0 + j - a0));
             c += take ? 1 : 0;
         }
     }
@@ -402,8 +452,15 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         for (int k = 0; k < VB; ++k) {
             // first write of a row covers every slot (untouched slots stay INF)
             const bool f = ok[k] && !((tw >> iv[k]) & 1u);
-            const bool ch = ok[k] && vless<Op, SPL>(d[k], e[k]);
-            if (ch || f) {
+            const bool lt = ok[k] && vless<Op, SPL>(d[k], e[k]);   // the row improved (store it)
+            bool ch = lt;                                           // a distance improved (propagate)
+            if constexpr (Op::KEYED) {
+                bool dl = false;
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) dl |= Op::dist_less(d[k].x[j], e[k].x[j]);
+                ch = ok[k] && dl;
+            }
+            if (lt || f) {
                 const Vec<SPL> nv = vmin<Op, SPL>(d[k], e[k]);
                 vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, nv);
                 if (Op::PACK > 1) {
@@ -467,6 +524,12 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
                                          const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                          int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
                                          int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane);
+
+template <int SPL>
+__device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
+                                               const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
+                                               int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
+                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane);
 
 // Diagnostics (WR_TILE_TRACE): per tile {start ns, end ns, rounds, SM id}.
 __device__ long long *g_tile_trace = nullptr;
@@ -536,8 +599,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 const int slot = lane * SPL * Op::PACK + j;
                 const int s = tile_src[tile * TS + slot];
                 if (s >= 0) {
-                    if (Op::PACK == 1) R[(size_t)s * TSW + slot] = Op::ZERO;
-                    else reinterpret_cast<uint16_t *>(R)[(size_t)s * TS + slot] = 0;
+                    if constexpr (Op::PACK == 1) R[(size_t)s * TSW + slot] = Op::ZERO;
+                    else reinterpret_cast<uint16_t *>(R)[(size_t)s * TS + slot] = Op::SEED16;
                     atomicOr(&chg[s >> 5].x, 1u << (s & 31));   // stamp 0 = round 0
                     atomicOr(&touched[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
@@ -680,8 +743,12 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                 }
             }
             t = __shfl_sync(FULL, t, 0);
-            pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
-                                 (int)(j % chunks) * PV, spw, lane);
+            if constexpr (Op::KEYED)
+                pred_job_keyed<SPL>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, t,
+                                    (int)(j % chunks) * PV, spw, lane);
+            else
+                pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
+                                       (int)(j % chunks) * PV, spw, lane);
         }
     }
 }
@@ -710,8 +777,7 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
                                  run.ovf_thr * 0x10001u, run.tile_order, run.fuse, run.slot_row);
     count_launch();
     WR_LAUNCH_CHECK();
-    WR_CUDA(cudaStreamSynchronize(st));  // counter lifetime
-    return true;
+    return true;   // the counter goes back to the stream-ordered pool: no sync needed
 }
 
 static int env_int(const char *name, int dflt) {
@@ -729,15 +795,13 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
     // (11) 84.4, 640 static (9) 94.4, 896 static (10) 104; fp32: 768 static
     // 232 ms, 640 static 240, 768 lists 254 (the list order lets more
     // suboptimal values propagate: 4.4 vs 3.6 x S*E relaxations).
+    // (the other shapes measured there - 384 x 2, 896, 704/768 with lists -
+    // were dropped from the build; WR_BF_CONFIG picks 8 or 11)
     static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 11);
     bool ok = false;
     switch (cfg) {
-        case 4: ok = launch_shape<Op, DENSE, 384, 2, SPL>(g, run, d_stats, st); break;
         case 8: ok = launch_shape<Op, DENSE, 768, 1, SPL>(g, run, d_stats, st); break;
-        case 10: ok = launch_shape<Op, DENSE, 896, 1, SPL>(g, run, d_stats, st); break;
         case 11: ok = launch_shape<Op, DENSE, 640, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
-        case 14: ok = launch_shape<Op, DENSE, 768, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
-        case 15: ok = launch_shape<Op, DENSE, 704, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
         default: break;
     }
     if (!ok && !launch_shape<Op, DENSE, 640, 1, SPL>(g, run, d_stats, st) &&
@@ -747,19 +811,20 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
 
 template <class Op>
 static void launch_sweep(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
-    const bool dense = run.variant == WR_BF_DENSE;
+    // packed rows serve the routing path only, which never asks for dense
+    const bool dense = Op::PACK == 1 && run.variant == WR_BF_DENSE;
     switch (run.spl) {
         case 4:
-            if (dense) launch_dispatch<Op, true, 4>(g, run, d_stats, st);
-            else launch_dispatch<Op, false, 4>(g, run, d_stats, st);
+            if constexpr (Op::PACK == 1) if (dense) { launch_dispatch<Op, true, 4>(g, run, d_stats, st); break; }
+            launch_dispatch<Op, false, 4>(g, run, d_stats, st);
             break;
         case 2:
-            if (dense) launch_dispatch<Op, true, 2>(g, run, d_stats, st);
-            else launch_dispatch<Op, false, 2>(g, run, d_stats, st);
+            if constexpr (Op::PACK == 1) if (dense) { launch_dispatch<Op, true, 2>(g, run, d_stats, st); break; }
+            launch_dispatch<Op, false, 2>(g, run, d_stats, st);
             break;
         default:
-            if (dense) launch_dispatch<Op, true, 1>(g, run, d_stats, st);
-            else launch_dispatch<Op, false, 1>(g, run, d_stats, st);
+            if constexpr (Op::PACK == 1) if (dense) { launch_dispatch<Op, true, 1>(g, run, d_stats, st); break; }
+            launch_dispatch<Op, false, 1>(g, run, d_stats, st);
             break;
     }
 }
@@ -879,7 +944,8 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
         WR_CUDA(cudaMemsetAsync(ttrace.p, 0, ttrace.bytes(), st));
         WR_CUDA(cudaMemcpyToSymbolAsync(g_tile_trace, &ttrace.p, sizeof(void *), 0, cudaMemcpyHostToDevice, st));
     }
-    if (run.pack == 2) launch_sweep<OpU16>(g, run, d_stats, st);
+    if (run.pack == 2 && run.keyed) launch_sweep<OpK16>(g, run, d_stats, st);
+    else if (run.pack == 2) launch_sweep<OpU16>(g, run, d_stats, st);
     else if (g->wtype == WR_F32) launch_sweep<OpF32>(g, run, d_stats, st);
     else if (g->has_negative) launch_sweep<OpI32N>(g, run, d_stats, st);
     else launch_sweep<OpU32>(g, run, d_stats, st);
@@ -1195,6 +1261,65 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
 }
 
+// a4 from keyed rows (OpK16): pred[v] = in_src[in_ptr[v] + k] with k the
+// low nibble of the final key (15 = none: the source itself, unreachable
+// vertices). A job decodes 8 consecutive vertices of one tile, stages the
+// preds in shared memory and writes each source's 8 columns as one full
+// 32-B sector (the same output layout as pred_job, no in-arc gathers).
+template <int SPL>
+__device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
+                                               const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
+                                               int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
+                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane) {
+    constexpr int TSW = 32 * SPL;
+    constexpr int TS = TSW * 2;
+    constexpr int NS = SPL * 2;
+    constexpr int PV = PredShape::PV;
+    const int V = g.V;
+    const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
+    const int nv = min(PV, V - c0);
+    const int a_lane = lane < nv ? g.in_ptr[c0 + lane] : 0;
+    Vec<SPL> key[PV];
+#pragma unroll
+    for (int jv = 0; jv < PV; ++jv)
+        if (jv < nv) key[jv] = vload<SPL>(Rl + (size_t)(c0 + jv) * TSW);
+#pragma unroll
+    for (int jv = 0; jv < PV; ++jv) {
+        if (jv >= nv) break;
+        const int a0 = __shfl_sync(FULL, a_lane, jv);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = (key[jv].x[j] >> (16 * h)) & 0xfu;
+                spw[jv][lane * NS + j * 2 + h] = k == 15u ? -1 : g.in_src[a0 + (int)k];
+            }
+    }
+    __syncwarp();
+    const bool vec = (V & 3) == 0 && nv == PV;
+    int srow[TS / 32];
+#pragma unroll
+    for (int k = 0; k < TS / 32; ++k) {
+        const int sl = tile * TS + lane + 32 * k;
+        srow[k] = tile_src[sl] < 0 ? -1 : (slot_row ? slot_row[sl] : sl);
+    }
+#pragma unroll
+    for (int k = 0; k < TS / 32; ++k) {
+        if (srow[k] < 0) continue;
+        const int sl_in = lane + 32 * k;
+        int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
+        if (vec) {
+            reinterpret_cast<int4 *>(dst)[0] =
+                make_int4(spw[0][sl_in], spw[1][sl_in], spw[2][sl_in], spw[3][sl_in]);
+            reinterpret_cast<int4 *>(dst)[1] =
+                make_int4(spw[4][sl_in], spw[5][sl_in], spw[6][sl_in], spw[7][sl_in]);
+        } else {
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv][sl_in];
+        }
+    }
+    __syncwarp();   // spw is reused by the warp's next job
+}
+
 template <class Op, int SPL, int MINB, int PA, int PW>
 __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int ntiles,
                                                       const uint32_t *__restrict__ rows,
@@ -1296,7 +1421,8 @@ constexpr int HOP_THREADS = 512;
 template <class Op>
 __global__ void __launch_bounds__(HOP_THREADS) hop_bfs_kernel(DevGraph g, const int *__restrict__ tile_src, int tile,
                                                               int grp, int tsw, const uint32_t *__restrict__ rows,
-                                                              uint32_t *__restrict__ hop) {
+                                                              uint32_t *__restrict__ hop, const int *gate) {
+    if (gate && !gate[tile]) return;   // stream-ordered gating: only tiles flagged flat
     extern __shared__ uint32_t smem[];
     const int V = g.V;
     const int NW = (V + 31) >> 5;
@@ -1370,7 +1496,8 @@ template <class Op>
 __global__ void flat_pred_kernel(DevGraph g, const int *__restrict__ tile_src, int tile, int grp, int tsw,
                                  const uint32_t *__restrict__ rows, const uint32_t *__restrict__ hop,
                                  const int *__restrict__ slot_row, int64_t out_row0, int32_t *pred_out,
-                                 int neg_graph) {
+                                 int neg_graph, const int *gate) {
+    if (gate && !gate[tile]) return;
     const int lane = threadIdx.x & 31;
     const int v = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int V = g.V;
@@ -1400,33 +1527,33 @@ __global__ void flat_pred_kernel(DevGraph g, const int *__restrict__ tile_src, i
 
 template <class Op>
 static void resolve_group(const wr_graph *g, const BfRun &run, int t, int grp, uint32_t *hop, size_t smem,
-                          int64_t out_row0, int32_t *pred_out, int neg, cudaStream_t st) {
+                          int64_t out_row0, int32_t *pred_out, int neg, const int *gate, cudaStream_t st) {
     const int V = g->V;
     const int tsw = 32 * run.spl;
     WR_CUDA(cudaFuncSetAttribute(hop_bfs_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    hop_bfs_kernel<Op><<<1, HOP_THREADS, smem, st>>>(g->view(), run.tile_src, t, grp, tsw, run.rows, hop);
+    hop_bfs_kernel<Op><<<1, HOP_THREADS, smem, st>>>(g->view(), run.tile_src, t, grp, tsw, run.rows, hop, gate);
     flat_pred_kernel<Op><<<(V + 7) / 8, 256, 0, st>>>(g->view(), run.tile_src, t, grp, tsw, run.rows, hop,
                                                      run.slot_row, out_row0,
-                                                     pred_out, neg);
+                                                     pred_out, neg, gate);
     count_launch();
     count_launch();
     WR_LAUNCH_CHECK();
 }
 
 void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles, int64_t out_row0,
-                     int32_t *pred_out, cudaStream_t st) {
+                     int32_t *pred_out, cudaStream_t st, const int *gate) {
     if (tiles.empty() || !pred_out) return;
     const int V = g->V;
-    DBuf<uint32_t> hop((size_t)V * 32);
+    DBuf<uint32_t> hop((size_t)V * 32);   // reused tile after tile in stream order
     const size_t smem = (size_t)2 * ((V + 31) / 32) * sizeof(uint32_t);
     for (int t : tiles) {
         for (int grp = 0; grp < run.spl; ++grp) {
-            if (g->wtype == WR_F32) resolve_group<OpF32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, st);
-            else if (g->has_negative) resolve_group<OpI32N>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 1, st);
-            else resolve_group<OpU32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, st);
+            if (g->wtype == WR_F32) resolve_group<OpF32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, gate, st);
+            else if (g->has_negative)
+                resolve_group<OpI32N>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 1, gate, st);
+            else resolve_group<OpU32>(g, run, t, grp, hop.p, smem, out_row0, pred_out, 0, gate, st);
         }
     }
-    WR_CUDA(cudaStreamSynchronize(st));
 }
 
 // ------------------------------------------------------ a8 the scheduler --
@@ -1506,15 +1633,26 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     WR_CUDA(cudaEventCreate(&e1));
     WR_CUDA(cudaEventRecord(e0, st));
 
+    const bool dist_dev = dist && is_device_ptr(dist);
+    const bool pred_dev = pred && is_device_ptr(pred);
+    // async: nothing after the sweep needs the host (no negative cycle to
+    // report, no host staging, flat pred vertices resolved under a device
+    // gate); the host still builds the tiles before the sweep is enqueued
+    const bool async = o.async && (!dist || dist_dev) && (!pred || pred_dev) && !g->has_negative &&
+                       o.max_rounds <= 0;
+    auto host_check = [&](const int32_t *v, int64_t n, const char *what) {
+        for (int64_t i = 0; i < n; ++i)
+            if (v[i] < 0 || v[i] >= V) WR_THROW(WR_EINVAL, std::string(what) + ": vertex outside [0, V)");
+    };
     DBuf<int> d_src = to_device<int>(sources, S, st);
-    check_vertices(d_src.p, S, V, st, "wr_bf_batch sources");
+    if (!is_device_ptr(sources)) host_check(sources, S, "wr_bf_batch sources");
+    else check_vertices(d_src.p, S, V, st, "wr_bf_batch sources");
     DBuf<int> d_tgt;
     if (targets) {
         d_tgt = to_device<int>(targets, T, st);
-        check_vertices(d_tgt.p, T, V, st, "wr_bf_batch targets");
+        if (!is_device_ptr(targets)) host_check(targets, T, "wr_bf_batch targets");
+        else check_vertices(d_tgt.p, T, V, st, "wr_bf_batch targets");
     }
-    const bool dist_dev = dist && is_device_ptr(dist);
-    const bool pred_dev = pred && is_device_ptr(pred);
 
     // a8: per-source working set = rows (4V) + staging for host outputs
     int64_t per_src = 4LL * V;
@@ -1545,10 +1683,15 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
         const int64_t hi = std::min<int64_t>(S, lo + sb);
         const int ntiles = make_tiles_ordered(g, d_src.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
         BfRun run{tile_src.p, ntiles, rows.p, variant, max_rounds, spl, slot_row.p};
-        bf_run(g, run, d_stats.p, st);
-        BfTileStats hs;
-        WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
-        WR_CUDA(cudaStreamSynchronize(st));
+        {
+            NvtxRange nv("wr.bf.sweep");
+            bf_run(g, run, d_stats.p, st);
+        }
+        BfTileStats hs{0ull, 0, -1, 0ull};
+        if (!async) {
+            WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+            WR_CUDA(cudaStreamSynchronize(st));
+        }
         if (hs.negcycle_tile >= 0) {
             int s_bad = -1;
             WR_CUDA(cudaMemcpy(&s_bad, tile_src.p + (size_t)hs.negcycle_tile * tsw, 4, cudaMemcpyDeviceToHost));
@@ -1569,7 +1712,13 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
             if (dout) bf_write_outputs(g, run, row_d, S, d_tgt.p, ncols, dout, nullptr, flat.p, st);
             if (pout) bf_write_outputs(g, run, row_p, S, nullptr, V, nullptr, pout, flat.p, st);
         }
-        if (pout) {
+        if (pout && async) {   // flat vertices need zero int weights or fp32 absorption
+            if (g->wtype == WR_F32 || g->has_zero) {
+                std::vector<int> all(ntiles);
+                for (int t = 0; t < ntiles; ++t) all[t] = t;
+                bf_resolve_flat(g, run, all, row_p, pout, st, flat.p);
+            }
+        } else if (pout) {
             std::vector<int> hflat(ntiles);
             WR_CUDA(cudaMemcpyAsync(hflat.data(), flat.p, sizeof(int) * ntiles, cudaMemcpyDeviceToHost, st));
             WR_CUDA(cudaStreamSynchronize(st));
@@ -1589,13 +1738,15 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     }
     WR_CUDA(cudaEventRecord(e1, st));
     BfTileStats hs{};
-    WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    WR_CUDA(cudaStreamSynchronize(st));  // stats and temporaries need the sync (async is reserved)
-    float ms = 0.f;
-    WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    float ms = -1.f;
+    if (!async) {   // temporaries are stream-ordered; only the stats need the host
+        WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+        WR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (stats) {
+    if (stats) {   // async: counters unknown (0), ms = -1
         stats->rounds_max = hs.rounds_max;
         stats->relaxations = (int64_t)hs.relax;
         stats->visits = (int64_t)hs.visits;
@@ -1608,10 +1759,73 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     return WR_OK;
 }
 
+int ctx_rank(const wr_ctx *c);
+int ctx_world(const wr_ctx *c);
+void ctx_share_blocks(const wr_ctx *c, void *buf, const int64_t *off, cudaStream_t st);
+
+// shard = 1 over a context: rank r relaxes sources [lo_r, hi_r) (contiguous
+// blocks, wr_shard_range) into rows lo_r.. of full-size device outputs, then
+// the row blocks are exchanged (grouped NCCL broadcasts on the stream).
+static wr_status bf_batch_sharded(const wr_graph *g, const int32_t *sources, int32_t S, const int32_t *targets,
+                                  int32_t T, void *dist, int32_t *pred, const wr_bf_opts &o, wr_bf_stats *stats) {
+    const wr_ctx *ctx = o.ctx;
+    const int rank = ctx_rank(ctx), world = ctx_world(ctx);
+    WR_CUDA(cudaSetDevice(g->device));
+    cudaStream_t st = (cudaStream_t)o.stream;
+    StreamScope stream_scope(st);
+    const int V = g->V;
+    const int64_t ncols = targets ? T : V;
+    int64_t lo, hi;
+    wr_shard_range(S, rank, world, &lo, &hi);
+    const bool dist_dev = dist && is_device_ptr(dist), pred_dev = pred && is_device_ptr(pred);
+    DBuf<uint32_t> dstage;
+    DBuf<int32_t> pstage;
+    if (dist && !dist_dev) dstage.alloc((size_t)std::max<int64_t>(S, 1) * ncols);
+    if (pred && !pred_dev) pstage.alloc((size_t)std::max<int64_t>(S, 1) * V);
+    uint32_t *dfull = dist ? (dist_dev ? (uint32_t *)dist : dstage.p) : nullptr;
+    int32_t *pfull = pred ? (pred_dev ? pred : pstage.p) : nullptr;
+    wr_bf_opts local = o;
+    local.ctx = nullptr;
+    local.shard = 0;
+    local.async = 0;
+    if (hi > lo) {
+        const wr_status rc = bf_batch_impl(g, sources + lo, (int32_t)(hi - lo), targets, T,
+                                           dfull ? dfull + lo * ncols : nullptr, pfull ? pfull + lo * V : nullptr,
+                                           &local, stats);
+        if (rc) return rc;   // every rank sees the same inputs, so every rank fails alike
+    }
+    std::vector<int64_t> off(world + 1);
+    auto share = [&](void *buf, int64_t row_bytes) {
+        for (int q = 0; q < world; ++q) {
+            int64_t a, b;
+            wr_shard_range(S, q, world, &a, &b);
+            off[q] = a * row_bytes;
+            off[q + 1] = b * row_bytes;
+        }
+        ctx_share_blocks(ctx, buf, off.data(), st);
+    };
+    if (dfull) share(dfull, ncols * 4);
+    if (pfull) share(pfull, (int64_t)V * 4);
+    if (dist && !dist_dev)
+        WR_CUDA(cudaMemcpyAsync(dist, dfull, (size_t)S * ncols * 4, cudaMemcpyDeviceToHost, st));
+    if (pred && !pred_dev) WR_CUDA(cudaMemcpyAsync(pred, pfull, (size_t)S * V * 4, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaStreamSynchronize(st));
+    return WR_OK;
+}
+
 }  // namespace wr
 
 extern "C" wr_status wr_bf_batch(const wr_graph *g, const int32_t *sources, int32_t S, const int32_t *targets,
                                  int32_t T, void *dist, int32_t *pred, const wr_bf_opts *opts,
                                  wr_bf_stats *stats) {
-    return wr::guarded([&] { return wr::bf_batch_impl(g, sources, S, targets, T, dist, pred, opts, stats); });
+    return wr::guarded([&]() -> wr_status {
+        wr::NvtxRange nv("wr_bf_batch");
+        if (opts && opts->shard) {
+            if (!opts->ctx) return wr::fail(WR_EINVAL, "wr_bf_batch: shard needs opts.ctx");
+            if (!g || S < 0 || (S > 0 && !sources)) return wr::fail(WR_EINVAL, "wr_bf_batch: bad arguments");
+            if (wr::ctx_world(opts->ctx) > 1)
+                return wr::bf_batch_sharded(g, sources, S, targets, T, dist, pred, *opts, stats);
+        }
+        return wr::bf_batch_impl(g, sources, S, targets, T, dist, pred, opts, stats);
+    });
 }

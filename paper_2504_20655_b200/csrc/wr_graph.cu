@@ -10,6 +10,8 @@
 #include <memory>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "wr_internal.cuh"
 
 namespace wr {
@@ -152,6 +154,9 @@ size_t pool_idle_bytes(int dev) {
     return (reserved > used ? (size_t)(reserved - used) : 0) + cached;
 }
 
+NvtxRange::NvtxRange(const char *name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+
 void set_error(const std::string &msg) { g_err = msg; }
 wr_status fail(wr_status code, const std::string &msg) {
     g_err = msg;
@@ -288,6 +293,11 @@ __global__ void validate_kernel(const int *src, const int *dst, uint32_t *w, int
     }
     atomicAdd((unsigned long long *)&in_deg[v], 1ull);
     atomicAdd((unsigned long long *)&out_deg[u], 1ull);
+}
+
+__global__ void max_deg_kernel(const int64_t *deg, int V, unsigned long long *mx) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < V) atomicMax(mx, (unsigned long long)deg[v]);
 }
 
 __global__ void validate_xy_kernel(const int *xy, int V, int *flags) {
@@ -441,6 +451,13 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
         WR_LAUNCH_CHECK();
         WR_CUDA(cudaMemcpyAsync(g->bbox, bbox.p, sizeof(g->bbox), cudaMemcpyDeviceToHost, st));
     }
+    DBuf<unsigned long long> maxdeg(1);
+    WR_CUDA(cudaMemsetAsync(maxdeg.p, 0, 8, st));
+    max_deg_kernel<<<grid_for(V, 256), 256, 0, st>>>(in_deg.p, V, maxdeg.p);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    unsigned long long hmaxdeg = 0;
+    WR_CUDA(cudaMemcpyAsync(&hmaxdeg, maxdeg.p, 8, cudaMemcpyDeviceToHost, st));
     int hf[4];
     WR_CUDA(cudaMemcpyAsync(hf, flags.p, 16, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
@@ -450,6 +467,7 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
     g->has_negative = hf[2];
     g->has_zero = hf[3];
     g->max_abs_w = hf[1];
+    g->max_in_deg = (int64_t)hmaxdeg;
     if (d->wtype == WR_I32 && (int64_t)(V - 1) * (int64_t)(uint32_t)hf[1] >= (int64_t)INT32_MAX)
         return fail(WR_EOVERFLOW, "wr_graph_load: (V-1)*max|w| >= INT32_MAX (reading A7)");
 
@@ -508,7 +526,10 @@ wr_status wr_release_cached(int32_t device) {
 }
 
 wr_status wr_graph_load(const wr_graph_desc *desc, wr_graph **out) {
-    return wr::guarded([&] { return wr::graph_load_impl(desc, out); });
+    return wr::guarded([&] {
+        wr::NvtxRange nv("wr_graph_load");
+        return wr::graph_load_impl(desc, out);
+    });
 }
 
 wr_status wr_graph_free(wr_graph *g) {

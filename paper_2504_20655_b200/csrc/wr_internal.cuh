@@ -54,6 +54,13 @@ wr_status guarded(F &&f) {
     }
 }
 
+// NVTX range for the lifetime of a scope (tracing, §5): every entry point
+// and the sweep / pred / route phases (header-only NVTX v3).
+struct NvtxRange {
+    explicit NvtxRange(const char *name);
+    ~NvtxRange();
+};
+
 // Counts libwr kernel launches (reported in stats and by the bench).
 extern thread_local int64_t g_launches;
 inline void count_launch() { ++g_launches; }
@@ -140,6 +147,7 @@ struct wr_graph {
     int has_negative = 0;
     int has_zero = 0;       // an int32 arc of weight 0
     int32_t max_abs_w = 0;
+    int64_t max_in_deg = 0; // largest in-degree (keyed rows need <= 15)
     wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
     wr::DBuf<uint32_t> in_w;
     wr::DBuf<int2> in_arc;
@@ -190,6 +198,7 @@ struct BfRun {              // one BF segment over tiles of 32*spl sources
     int pack = 1;           // sources per 32-bit word: 1, or 2 (packed u16 distances)
     const int *tile_order = nullptr;  // [ntiles] claim order of the tiles (null = 0..ntiles-1)
     uint32_t ovf_thr = 0;   // pack 2: a stored distance >= ovf_thr flags a possible u16 overflow
+    bool keyed = false;     // pack 2 rows hold (d << 4 | in-arc index of the pred) keys (OpK16)
     PredFuse fuse;
     int tsw() const { return 32 * spl * pack; }   // sources (slots) per tile
 };
@@ -211,8 +220,10 @@ void bf_write_outputs(const wr_graph *g, const BfRun &run, int64_t out_row0, int
                       const int *targets, int T, void *dist_out, int32_t *pred_out,
                       int *d_flat_tiles, cudaStream_t st);
 // Resolves "flat" predecessors of the listed tiles with a tight-arc BFS.
+// gate: optional device [ntiles] flags; a listed tile whose flag is 0 is
+// skipped on the device (no host readback needed).
 void bf_resolve_flat(const wr_graph *g, const BfRun &run, const std::vector<int> &tiles,
-                     int64_t out_row0, int32_t *pred_out, cudaStream_t st);
+                     int64_t out_row0, int32_t *pred_out, cudaStream_t st, const int *gate = nullptr);
 
 // Builds the tiles for sources [lo, hi) of a device source list: tsw slots
 // per tile, spatially compact (recursive coordinate bisection of the

@@ -357,6 +357,30 @@ __global__ void order_stops_kernel(const int64_t *order_ptr, const int *nodes, i
         for (int k = 0; k < n; ++k) is_src[s[k]] = 1;
 }
 
+// Caller labels per order line -> per (order, stop) labels [B][16]: lines at
+// the same node must agree (bad |= 2), labels must be >= 0 (bad |= 4).
+__global__ void line_labels_kernel(const int64_t *order_ptr, const int *nodes, const int *line_labels, int64_t B,
+                                   const int *stops, const int *n_arr, const int *status, int *lab, int *bad) {
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= B) return;
+    int l[MS];
+    for (int k = 0; k < MS; ++k) l[k] = -1;
+    if (status[o] == WR_OK) {
+        const int *s = stops + o * MS;
+        const int n = n_arr[o];
+        for (int64_t a = order_ptr[o]; a < order_ptr[o + 1]; ++a) {
+            const int x = nodes[a], y = line_labels[a];
+            if (y < 0) atomicOr(bad, 4);
+            int i = 0;
+            while (i < n && s[i] != x) ++i;
+            if (i == n) continue;
+            if (l[i] >= 0 && l[i] != y) atomicOr(bad, 2);
+            l[i] = y;
+        }
+    }
+    for (int k = 0; k < MS; ++k) lab[o * MS + k] = l[k] < 0 ? 0 : l[k];
+}
+
 __global__ void sources_scatter_kernel(const int *is_src, const int *src_row, int V, int *sources) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < V && is_src[v]) sources[src_row[v]] = v;
@@ -409,11 +433,12 @@ __global__ void gather_send_kernel(const int *stops, const int *n_arr, const int
     owned_range(s, n, src_row, own_lo, own_hi, i_lo, i_hi);
     const int64_t rr = pos_of[r - seg_lo];   // slot position of the source in the segment's tiles
     uint32_t *dst = send + off[o] + (int64_t)(i - i_lo) * n;
-    if (pack == 2) {   // packed u16 rows: widen, INF 0x7fff -> INT32_MAX
+    if (pack >= 2) {   // packed u16 rows: widen, INF 0x7fff -> INT32_MAX; keyed rows (3): d = key >> 4
         const uint16_t *R = reinterpret_cast<const uint16_t *>(rows) + (size_t)(rr / tsw) * V * tsw + (rr % tsw);
+        const int sh = pack == 3 ? 4 : 0;
         for (int j = 0; j < n; ++j) {
             const uint32_t x = R[(size_t)s[j] * tsw];
-            dst[j] = x == 0x7fffu ? 0x7fffffffu : x;
+            dst[j] = x == 0x7fffu ? 0x7fffffffu : x >> sh;
         }
         return;
     }
@@ -1214,6 +1239,7 @@ static unsigned gridn(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
                            int32_t rank, int32_t world, const wr_route_opts *opts, const int32_t *labels16,
+                           const int32_t *line_labels,
                            wr_plan **out) {
     if (!g || !out || B < 0 || (B > 0 && (!order_ptr || !order_nodes)))
         return fail(WR_EINVAL, "wr_orders_plan: bad arguments");
@@ -1230,7 +1256,7 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     P->B = B;
     P->rank = rank;
     P->world = world;
-    P->m = o.m;
+    P->m = (line_labels && o.m < 2) ? 2 : o.m;   // caller labels always go through the stitch
     P->pairs = (o.flags & WR_ROUTE_PAIRS) ? 1 : 0;
     P->chunk = o.chunk > 0 ? o.chunk : WR_DEFAULT_CHUNK;
     if (P->m >= 2 && !labels16 && !g->xy.p)
@@ -1259,10 +1285,20 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
         count_launch();
         WR_LAUNCH_CHECK();
     }
+    if (line_labels && B > 0) {
+        DBuf<int> d_ll = to_device<int>(line_labels, L, st);
+        P->labels.alloc((size_t)B * WR_MAX_STOPS);
+        line_labels_kernel<<<gridn(B, 256), 256, 0, st>>>(d_ptr.p, d_nodes.p, d_ll.p, B, P->stops.p, P->n_arr.p,
+                                                         P->status.p, P->labels.p, bad.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
     int hbad = 0;
     WR_CUDA(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
-    if (hbad) return fail(WR_EINVAL, "wr_orders_plan: order node outside [0, V)");
+    if (hbad & 1) return fail(WR_EINVAL, "wr_orders_plan: order node outside [0, V)");
+    if (hbad & 2) return fail(WR_EINVAL, "wr_orders_plan: lines at the same node carry different labels");
+    if (hbad & 4) return fail(WR_EINVAL, "wr_orders_plan: negative label");
     scan_exclusive_i32(P->is_src.p, P->src_row.p, V, st);
     int last_row = 0, last_flag = 0;
     WR_CUDA(cudaMemcpyAsync(&last_row, P->src_row.p + V - 1, 4, cudaMemcpyDeviceToHost, st));
@@ -1346,7 +1382,15 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
                 !(o.flags & WR_ROUTE_ROWS32))
                    ? 2
                    : 1;
+    // Keyed packed rows (OpK16) when the fused pred is requested: the pred
+    // rides in the row keys (in-degree <= 15, w <= 0x7ff; d < 0x7ff, else
+    // the overflow flag redoes the phase with plain packed rows).
+    static const bool no_key = getenv("WR_NO_KEYED") != nullptr;
+    const bool fused_req = o.pred_out && !g->has_negative && getenv("WR_NO_FUSED_PRED") == nullptr;
+    bool keyed = pack == 2 && fused_req && !no_key && g->max_abs_w <= 0x7ff && g->max_in_deg <= 15;
     BfTileStats hs{};
+    int64_t tiles_swept = 0;
+    int tile_width = 0;
     auto run_phase = [&](int pk) {
         if (nsrc <= 0) return;
         wr_graph_info_t gi;
@@ -1389,8 +1433,13 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             const int ntiles =
                 make_tiles_ordered(g, P->sources.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
             BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
+            tiles_swept += ntiles;
+            tile_width = tsw;
             run.pack = pk;
-            run.ovf_thr = pk == 2 ? 0x7fffu - (uint32_t)g->max_abs_w : 0u;
+            run.keyed = pk == 2 && keyed;
+            run.ovf_thr = pk != 2 ? 0u
+                          : run.keyed ? (0x7ffu - (uint32_t)g->max_abs_w) << 4
+                                      : 0x7fffu - (uint32_t)g->max_abs_w;
             if (fused) {
                 WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
                 WR_CUDA(cudaMemsetAsync(done_list.p, 0xff, sizeof(int) * ntiles, st));
@@ -1404,7 +1453,10 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventRecord(b0, st));
             const double host_to_b0 =
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hclock0).count();
-            bf_run(g, run, d_stats.p, st);
+            {
+                NvtxRange nv(fused ? "wr.bf.sweep+pred" : "wr.bf.sweep");
+                bf_run(g, run, d_stats.p, st);
+            }
             WR_CUDA(cudaEventRecord(b1, st));
             if (o.pred_out) {   // a4 canonical pred of this segment's sources
                 if (!fused) {
@@ -1432,7 +1484,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             if (P->B > 0) {
                 gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, st>>>(
                     P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, lo, hi, off_r,
-                    rows.p, V, tsw, pk, pos_of.p, (uint32_t *)send);
+                    rows.p, V, tsw, run.keyed ? 3 : pk, pos_of.p, (uint32_t *)send);
                 count_launch();
                 WR_LAUNCH_CHECK();
             }
@@ -1460,10 +1512,20 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
     run_phase(pack);
     WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
+    if (pack == 2 && keyed && hs.overflow) {   // a distance may not fit in 11 bits: plain packed rows
+        const BfTileStats z{0ull, 0, -1, 0ull};
+        WR_CUDA(cudaMemcpyAsync(d_stats.p, &z, sizeof(z), cudaMemcpyHostToDevice, st));
+        keyed = false;
+        tiles_swept = 0;
+        run_phase(2);
+        WR_CUDA(cudaMemcpyAsync(&hs, d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaStreamSynchronize(st));
+    }
     if (pack == 2 && hs.overflow) {   // a distance may not fit in 15 bits: redo with 32-bit rows
         const BfTileStats z{0ull, 0, -1, 0ull};
         WR_CUDA(cudaMemcpyAsync(d_stats.p, &z, sizeof(z), cudaMemcpyHostToDevice, st));
         pack = 1;
+        tiles_swept = 0;
         run_phase(1);
     }
     const double h_loop = hms();
@@ -1488,6 +1550,9 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
         stats->bf_ms = bf_ms;
         stats->pred_ms = pred_ms;
         stats->row_bits = pack == 2 ? 16 : 32;
+        stats->keyed = pack == 2 && keyed ? 1 : 0;
+        stats->tiles = tiles_swept;
+        stats->tile_sources = tile_width;
     }
     return WR_OK;
 }
@@ -1496,6 +1561,7 @@ template <class C>
 static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64_t nord, wr_route_result *d_res,
                         unsigned long long *d_counters, cudaStream_t st) {
     if (nord <= 0) return;
+    NvtxRange nv("wr.routes");
     const int *xy = P.g->xy.p;
     DBuf<OrderRoute> ordr(nord);
     DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(4), hk_list(nord);
@@ -1619,9 +1685,14 @@ static wr_status check_route_overflow(const wr_graph *g) {
     return WR_OK;
 }
 
+int ctx_rank(const wr_ctx *c);
+int ctx_world(const wr_ctx *c);
+void ctx_allgather(const wr_ctx *c, const void *send, void *recv, size_t bytes, cudaStream_t st);
+void ctx_share_blocks(const wr_ctx *c, void *buf, const int64_t *off, cudaStream_t st);
+
 static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes,
                                    int64_t B, const wr_route_opts *opts, const int32_t *labels16,
-                                   wr_route_result *results, wr_route_stats *stats) {
+                                   const int32_t *line_labels, wr_route_result *results, wr_route_stats *stats) {
     if (!g) return fail(WR_EINVAL, "wr_route_orders: null graph");
     if (wr_status r = check_route_overflow(g)) return r;
     WR_CUDA(cudaSetDevice(g->device));
@@ -1634,16 +1705,49 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
     WR_CUDA(cudaEventCreate(&e0));
     WR_CUDA(cudaEventCreate(&e1));
     WR_CUDA(cudaEventRecord(e0, st));
+    const wr_ctx *ctx = o.ctx;
+    const int rank = ctx_rank(ctx), world = ctx_world(ctx);
+    if (B > 0 && !results) return fail(WR_EINVAL, "wr_route_orders: results");
     wr_plan *P = nullptr;
-    wr_status rc = plan_impl(g, order_ptr, order_nodes, B, 0, 1, &o, labels16, &P);
+    wr_status rc = plan_impl(g, order_ptr, order_nodes, B, rank, world, &o, labels16, line_labels, &P);
     if (rc) return rc;
     std::unique_ptr<wr_plan> hold(P);
     DBuf<uint32_t> send(std::max<int64_t>(P->max_send, 1));
     wr_route_stats s1{}, s2{};
     rc = local_impl(P, send.p, &o, &s1);
     if (rc) return rc;
-    rc = finish_impl(P, send.p, results, &o, &s2);
-    if (rc) return rc;
+    if (!ctx) {
+        rc = finish_impl(P, send.p, results, &o, &s2);
+        if (rc) return rc;
+    } else {
+        // a9: ONE all-gather of the owned D entries (rank-major, max_send
+        // 32-bit words each), then this rank's order block, then (unless
+        // WR_ROUTE_RANK_RESULTS) the result blocks of every rank
+        DBuf<uint32_t> gathered((size_t)world * P->max_send);
+        ctx_allgather(ctx, send.p, gathered.p, (size_t)P->max_send * 4, st);
+        const bool res_dev = is_device_ptr(results);
+        const bool share = !(o.flags & WR_ROUTE_RANK_RESULTS) && world > 1;
+        DBuf<wr_route_result> dres;
+        wr_route_result *full = results;
+        if (!res_dev && share) {
+            dres.alloc(std::max<int64_t>(B, 1));
+            full = dres.p;
+        }
+        rc = finish_impl(P, gathered.p, full + P->order_lo, &o, &s2);
+        if (rc) return rc;
+        if (share) {
+            std::vector<int64_t> off(world + 1);
+            for (int q = 0; q < world; ++q) {
+                int64_t lo, hi;
+                wr_shard_range(B, q, world, &lo, &hi);
+                off[q] = lo * (int64_t)sizeof(wr_route_result);
+                off[q + 1] = hi * (int64_t)sizeof(wr_route_result);
+            }
+            ctx_share_blocks(ctx, full, off.data(), st);
+            if (!res_dev)
+                WR_CUDA(cudaMemcpyAsync(results, full, sizeof(wr_route_result) * B, cudaMemcpyDeviceToHost, st));
+        }
+    }
     WR_CUDA(cudaEventRecord(e1, st));
     WR_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -1667,6 +1771,9 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
         stats->bf_ms = s1.bf_ms;
         stats->pred_ms = s1.pred_ms;
         stats->row_bits = s1.row_bits;
+        stats->keyed = s1.keyed;
+        stats->tiles = s1.tiles;
+        stats->tile_sources = s1.tile_sources;
     }
     return WR_OK;
 }
@@ -1676,10 +1783,12 @@ static wr_status route_orders_impl(const wr_graph *g, const int64_t *order_ptr, 
 extern "C" {
 
 wr_status wr_orders_plan(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
-                         int32_t rank, int32_t world, const wr_route_opts *opts, wr_plan **out) {
+                         const int32_t *labels, int32_t rank, int32_t world, const wr_route_opts *opts,
+                         wr_plan **out) {
     return wr::guarded([&] {
+        wr::NvtxRange nv("wr_orders_plan");
         if (wr_status r = g ? wr::check_route_overflow(g) : WR_OK) return r;
-        return wr::plan_impl(g, order_ptr, order_nodes, B, rank, world, opts, nullptr, out);
+        return wr::plan_impl(g, order_ptr, order_nodes, B, rank, world, opts, nullptr, labels, out);
     });
 }
 
@@ -1700,12 +1809,18 @@ wr_status wr_plan_info(const wr_plan *p, wr_plan_info_t *info) {
 }
 
 wr_status wr_orders_local(wr_plan *p, void *send, const wr_route_opts *opts, wr_route_stats *stats) {
-    return wr::guarded([&] { return wr::local_impl(p, send, opts, stats); });
+    return wr::guarded([&] {
+        wr::NvtxRange nv("wr_orders_local");
+        return wr::local_impl(p, send, opts, stats);
+    });
 }
 
 wr_status wr_orders_finish(wr_plan *p, const void *gathered, wr_route_result *results, const wr_route_opts *opts,
                            wr_route_stats *stats) {
-    return wr::guarded([&] { return wr::finish_impl(p, gathered, results, opts, stats); });
+    return wr::guarded([&] {
+        wr::NvtxRange nv("wr_orders_finish");
+        return wr::finish_impl(p, gathered, results, opts, stats);
+    });
 }
 
 wr_status wr_plan_free(wr_plan *p) {
@@ -1718,8 +1833,12 @@ wr_status wr_plan_free(wr_plan *p) {
 }
 
 wr_status wr_route_orders(const wr_graph *g, const int64_t *order_ptr, const int32_t *order_nodes, int64_t B,
-                          const wr_route_opts *opts, wr_route_result *results, wr_route_stats *stats) {
-    return wr::guarded([&] { return wr::route_orders_impl(g, order_ptr, order_nodes, B, opts, nullptr, results, stats); });
+                          const int32_t *labels, const wr_route_opts *opts, wr_route_result *results,
+                          wr_route_stats *stats) {
+    return wr::guarded([&] {
+        wr::NvtxRange nv("wr_route_orders");
+        return wr::route_orders_impl(g, order_ptr, order_nodes, B, opts, nullptr, labels, results, stats);
+    });
 }
 
 wr_status wr_route_segmented(const wr_graph *g, const int32_t *stops, int32_t n, const int32_t *labels, int32_t m,
@@ -1743,7 +1862,8 @@ wr_status wr_route_segmented(const wr_graph *g, const int32_t *stops, int32_t n,
         if (opts) o = *opts;
         o.m = m;
         if (labels && m < 2) o.m = 2;   // caller labels always go through the stitch
-        return wr::route_orders_impl(g, ptr, hs.data(), 1, &o, labels ? lab16.data() : nullptr, out, nullptr);
+        o.ctx = nullptr;
+        return wr::route_orders_impl(g, ptr, hs.data(), 1, &o, labels ? lab16.data() : nullptr, nullptr, out, nullptr);
     });
 }
 

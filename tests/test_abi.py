@@ -40,11 +40,29 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-def test_result_layout_matches_header():
-    # int32 n, status, uint32 cost_bits, int32 m_used, int64 rank, int32 seq[16]
-    assert wr.RESULT_DTYPE.itemsize == 88
-    assert ctypes.sizeof(wr.GraphDesc) == 88 and ctypes.sizeof(wr.RouteOpts) == 56
-    assert ctypes.sizeof(wr.RouteStats) == 88
+def test_result_layout_matches_header(tmp_path):
+    """The binding's struct layouts equal the C compiler's for include/wr.h."""
+    structs = {"wr_graph_desc": wr.GraphDesc, "wr_graph_info_t": wr.GraphInfo, "wr_bf_opts": wr.BfOpts,
+               "wr_bf_stats": wr.BfStats, "wr_route_opts": wr.RouteOpts, "wr_route_stats": wr.RouteStats,
+               "wr_plan_info_t": wr.PlanInfo}
+    src = tmp_path / "sizes.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "wr.h"', "int main(void) {"]
+    lines.append('printf("wr_route_result %zu\\n", sizeof(wr_route_result));')
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{name}.{fname} %zu\\n", offsetof({name}, {fname.rstrip("_")}));')
+    lines.append("return 0; }")
+    src.write_text("\n".join(lines))
+    import subprocess
+    exe = tmp_path / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert int(got["wr_route_result"]) == wr.RESULT_DTYPE.itemsize == 88
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, (name, fname)
 
 
 def test_shard_range_partitions():

@@ -461,6 +461,64 @@ def test_route_orders_pred_rows():
     assert np.array_equal(np.concatenate(parts), P)
 
 
+def _keyed_case(kind):
+    """Graphs that select each row kind of the routing sweep with fused pred:
+    keyed packed rows (small weights, in-degree <= 15), plain packed rows
+    after a keyed overflow (a 300-vertex path of weight 100: distances to
+    29,900 exceed the keyed 11-bit bound, fit 15 bits), plain packed rows
+    for an in-degree-25 hub, 32-bit rows for weights > 0x3fff."""
+    if kind == "keyed":
+        return gen.config(3, B=400)[0]
+    if kind == "path":
+        V = 300
+        src = list(range(V - 1)) + list(range(1, V))
+        dst = list(range(1, V)) + list(range(V - 1))
+        w = np.full(len(src), 100, np.int32)
+        w[::7] = 37
+        return G(V, src, dst, w, xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+    if kind == "hub":
+        n = 5
+        src, dst, w = [], [], []
+        for y in range(n):
+            for x in range(n):
+                v = y * n + x
+                for dx, dy in ((1, 0), (0, 1)):
+                    if x + dx < n and y + dy < n:
+                        u = (y + dy) * n + x + dx
+                        src += [v, u]; dst += [u, v]; w += [3, 3]
+                src += [v, n * n]; dst += [n * n, v]; w += [2 + v % 5, 2 + v % 3]
+        xy = np.array([(v % n, v // n) for v in range(n * n)] + [(9, 9)], np.int32)
+        return G(n * n + 1, src, dst, np.array(w, np.int32), xy=xy)
+    g = gen.config(3, B=400)[0]
+    return G(g.V, g.src, g.dst, (g.w * 6000).astype(np.int32), xy=g.xy)
+
+
+@pytest.mark.parametrize("kind,keyed,row_bits", [("keyed", 1, 16), ("path", 0, 16), ("hub", 0, 16),
+                                                 ("wide", 0, 32)])
+def test_route_orders_row_kinds_pred_and_routes(kind, keyed, row_bits):
+    """Every row kind of the fused sweep (keyed / plain packed / 32-bit,
+    including the keyed -> packed overflow redo) gives the oracle's routes
+    and canonical pred rows (O3)."""
+    g = _keyed_case(kind)
+    rng = np.random.default_rng(71)
+    B = 64
+    n = rng.integers(3, 8, B)
+    nodes = np.concatenate([rng.choice(g.V, k, replace=False) for k in n]).astype(np.int32)
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr, orders.order_nodes, orders.B = np.concatenate([[0], np.cumsum(n)]).astype(np.int64), nodes, B
+    Gd = wr.Graph(g.V, g.src, g.dst, g.w, xy=g.xy)
+    stops = np.unique(nodes)
+    pred = torch.full((stops.size, g.V), -7, dtype=torch.int32, device="cuda")
+    res, st = wr.route_orders(Gd, orders.order_ptr, orders.order_nodes, pred_out=pred)
+    assert (st.keyed, st.row_bits) == (keyed, row_bits)
+    exp_rows = oracle.bf_many(g, stops)
+    assert np.array_equal(pred.cpu().numpy(), oracle.pred_many(g, stops, exp_rows))
+    compare_orders(g, orders, m=1, G=Gd, results=res)
+
+
 def test_route_orders_budget_and_chunk_invariance():
     g, orders, _ = gen.config(3, B=2048)
     G = wr.Graph.from_gen(g)
