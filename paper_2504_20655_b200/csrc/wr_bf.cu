@@ -365,8 +365,8 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 #pragma unroll
         for (int j = 0; j < AQ; ++j) {
             const bool take = arc[j].x >= 0 && (!DELTA || pchg.test(arc[j].x));
-            // queued: the tail row's word offset (u * TSW < 2^31) and the prepared weight
-            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x * TSW, (int)Op::prep_w((uint32_t)arc[j].y, k0 + j - a0));
+            // queued: the tail row's byte offset (u * TSW * 4 < 2^31 for V within the frontier limit)
+            if (take && c < QC) q[lane * QC + c] = make_int2(arc[j].x * (TSW * 4), (int)Op::prep_w((uint32_t)arc[j].y, k0 + j - a0));
             c += take ? 1 : 0;
         }
     }
@@ -412,21 +412,30 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
             int tmax = 0;
 #pragma unroll
             for (int k = 0; k < VB; ++k) tmax = max(tmax, cc[k]);
+            const char *Rb = reinterpret_cast<const char *>(Rl);
             for (int t = 0; t < tmax; t += TPS) {
                 int2 tk[VB][TPS];
                 Vec<SPL> x[VB][TPS];
+                // queue entries are read unconditionally (stale entries past
+                // cc are valid shared memory, never used): no zero-fill, and
+                // two entries per 16-B load
 #pragma unroll
-                for (int k = 0; k < VB; ++k)
+                for (int k = 0; k < VB; ++k) {
+                    if constexpr (TPS == 2 && QC % 2 == 0) {
+                        const int4 two = *reinterpret_cast<const int4 *>(q + iv[k] * QC + min(t, QC - 2));
+                        tk[k][0] = make_int2(two.x, two.y);
+                        tk[k][1] = make_int2(two.z, two.w);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < TPS; ++j) {
-                        tk[k][j] = make_int2(0, 0);
-                        if (t + j < cc[k]) tk[k][j] = q[iv[k] * QC + t + j];
+                        for (int j = 0; j < TPS; ++j) tk[k][j] = q[iv[k] * QC + min(t + j, QC - 1)];
                     }
+                }
 #pragma unroll
                 for (int k = 0; k < VB; ++k)
 #pragma unroll
                     for (int j = 0; j < TPS; ++j)
-                        if (t + j < cc[k]) x[k][j] = vload<SPL>(Rl + (uint32_t)tk[k][j].x);
+                        if (t + j < cc[k])
+                            x[k][j] = vload<SPL>(reinterpret_cast<const uint32_t *>(Rb + (uint32_t)tk[k][j].x));
 #pragma unroll
                 for (int k = 0; k < VB; ++k)
 #pragma unroll
@@ -443,27 +452,35 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
                 } else {
                     for (int t = 0; t < cc[k]; ++t) {
                         const int2 tq = q[iv[k] * QC + t];
-                        vrelax<Op, SPL>(d[k], vload<SPL>(Rl + (uint32_t)tq.x), (uint32_t)tq.y);
+                        vrelax<Op, SPL>(d[k], vload<SPL>(reinterpret_cast<const uint32_t *>(
+                                                  reinterpret_cast<const char *>(Rl) + (uint32_t)tq.x)),
+                                        (uint32_t)tq.y);
                     }
                 }
             }
         }
 #pragma unroll
         for (int k = 0; k < VB; ++k) {
+            // nv = min(new, own row): the row improved iff some word of nv
+            // differs from the own row (one min + one xor per word instead
+            // of emulated per-half compares); keyed rows propagate only when
+            // a distance (not just a pred index) improved
+            const Vec<SPL> nv = vmin<Op, SPL>(d[k], e[k]);
+            uint32_t diff = 0, ddiff = 0;
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                const uint32_t x = nv.x[j] ^ e[k].x[j];
+                diff |= x;
+                if constexpr (Op::KEYED) ddiff |= x & 0xfff0fff0u;
+            }
             // first write of a row covers every slot (untouched slots stay INF)
             const bool f = ok[k] && !((tw >> iv[k]) & 1u);
-            const bool lt = ok[k] && vless<Op, SPL>(d[k], e[k]);   // the row improved (store it)
-            bool ch = lt;                                           // a distance improved (propagate)
-            if constexpr (Op::KEYED) {
-                bool dl = false;
-#pragma unroll
-                for (int j = 0; j < SPL; ++j) dl |= Op::dist_less(d[k].x[j], e[k].x[j]);
-                ch = ok[k] && dl;
-            }
+            const bool lt = ok[k] && diff != 0u;                   // the row improved (store it)
+            const bool ch = Op::KEYED ? ok[k] && ddiff != 0u : lt;  // a distance improved (propagate)
             if (lt || f) {
-                const Vec<SPL> nv = vmin<Op, SPL>(d[k], e[k]);
                 vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, nv);
-                if (Op::PACK > 1) {
+                // keyed rows are range-checked by the pred jobs instead (every key is decoded there)
+                if constexpr (Op::PACK > 1 && !Op::KEYED) {
 #pragma unroll
                     for (int j = 0; j < SPL; ++j) ovf |= Op::overflow(nv.x[j], thr2);
                 }
@@ -506,13 +523,14 @@ struct FrontierSmem {
 };
 __host__ __device__ constexpr FrontierSmem frontier_smem(int NW, int nwarps, int QC) {
     // offsets in 32-bit words; uint2 / int2 regions 8-B aligned
+    // (the task queues start 16-B aligned: step B reads two entries per int4)
     return FrontierSmem{0,
                         (size_t)NW,
                         (size_t)2 * NW,
                         ((size_t)3 * NW + 1) & ~(size_t)1,
                         (((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)4 * NW,
-                        ((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 1) & ~(size_t)1,
-                        (((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 1) & ~(size_t)1) +
+                        ((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 3) & ~(size_t)3,
+                        (((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 3) & ~(size_t)3) +
                             (size_t)nwarps * 32 * QC * 2};
 }
 
@@ -529,10 +547,9 @@ template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                                int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
-                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane);
+                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane, uint32_t thr,
+                                               int *overflow);
 
-// Diagnostics (WR_TILE_TRACE): per tile {start ns, end ns, rounds, SM id}.
-__device__ long long *g_tile_trace = nullptr;
 
 template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
@@ -566,7 +583,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         const int tile = s_tile;
         if (tile >= ntiles) break;
         long long t_start = 0;
-        if (g_tile_trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        if (fuse.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         uint32_t *R = rows + (size_t)tile * V * TSW;
         uint32_t *cur = smem + L.cur, *nxt = smem + L.nxt;
 
@@ -699,12 +716,12 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         if (lane == 0 && relax) atomicAdd(&stats->relax, relax * TS);
         if (lane == 0 && visits) atomicAdd(&stats->visits, visits);
         if (threadIdx.x == 0) atomicMax(&stats->rounds_max, rounds);
-        if (g_tile_trace && threadIdx.x == 0) {
+        if (fuse.trace && threadIdx.x == 0) {   // diagnostics (WR_TILE_TRACE)
             long long t_end;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            long long *e = g_tile_trace + 4 * (size_t)tile;
+            long long *e = fuse.trace + 4 * (size_t)tile;
             e[0] = t_start;
             e[1] = t_end;
             e[2] = rounds;
@@ -745,7 +762,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             t = __shfl_sync(FULL, t, 0);
             if constexpr (Op::KEYED)
                 pred_job_keyed<SPL>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, t,
-                                    (int)(j % chunks) * PV, spw, lane);
+                                    (int)(j % chunks) * PV, spw, lane, thr2 & 0xffffu, &stats->overflow);
             else
                 pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
                                        (int)(j % chunks) * PV, spw, lane);
@@ -937,43 +954,57 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
         WR_CUDA(cudaMemcpyAsync(order.p, ho.data(), 4 * run.ntiles, cudaMemcpyHostToDevice, st));
         run.tile_order = order.p;
     }
+    // WR_TILE_TRACE: per-tile {start, end, rounds, SM} copied to pinned host
+    // memory and appended to the file by a stream-ordered host callback, so
+    // tracing adds no host sync (concurrent sweeps keep their overlap).
     static const char *trace_path = getenv("WR_TILE_TRACE");
     DBuf<long long> ttrace;
+    struct TraceJob {
+        long long *h;
+        int *ord, *src;
+        int ntiles, tsw;
+        std::string path;
+    };
+    TraceJob *tj = nullptr;
     if (trace_path) {
         ttrace.alloc((size_t)4 * run.ntiles);
         WR_CUDA(cudaMemsetAsync(ttrace.p, 0, ttrace.bytes(), st));
-        WR_CUDA(cudaMemcpyToSymbolAsync(g_tile_trace, &ttrace.p, sizeof(void *), 0, cudaMemcpyHostToDevice, st));
+        run.fuse.trace = ttrace.p;
+        tj = new TraceJob{nullptr, nullptr, nullptr, run.ntiles, run.tsw(), trace_path};
+        WR_CUDA(cudaMallocHost(&tj->h, ttrace.bytes()));
+        WR_CUDA(cudaMallocHost(&tj->ord, 4 * (size_t)run.ntiles));
+        WR_CUDA(cudaMallocHost(&tj->src, 4 * (size_t)run.ntiles * run.tsw()));
     }
     if (run.pack == 2 && run.keyed) launch_sweep<OpK16>(g, run, d_stats, st);
     else if (run.pack == 2) launch_sweep<OpU16>(g, run, d_stats, st);
     else if (g->wtype == WR_F32) launch_sweep<OpF32>(g, run, d_stats, st);
     else if (g->has_negative) launch_sweep<OpI32N>(g, run, d_stats, st);
     else launch_sweep<OpU32>(g, run, d_stats, st);
-    if (trace_path) {   // append one line per tile: tile key-order-pos start end rounds sm
-        std::vector<long long> h((size_t)4 * run.ntiles);
-        WR_CUDA(cudaMemcpyAsync(h.data(), ttrace.p, ttrace.bytes(), cudaMemcpyDeviceToHost, st));
-        std::vector<int> ho(run.ntiles);
-        if (run.tile_order)
-            WR_CUDA(cudaMemcpyAsync(ho.data(), run.tile_order, 4 * run.ntiles, cudaMemcpyDeviceToHost, st));
-        WR_CUDA(cudaStreamSynchronize(st));
-        void *null = nullptr;
-        WR_CUDA(cudaMemcpyToSymbol(g_tile_trace, &null, sizeof(void *)));
-        std::vector<int> pos(run.ntiles);
-        for (int i = 0; i < run.ntiles; ++i) pos[run.tile_order ? ho[i] : i] = i;
-        if (FILE *f = fopen(trace_path, "a")) {
-            for (int t = 0; t < run.ntiles; ++t)
-                fprintf(f, "%d %d %lld %lld %lld %lld\n", t, pos[t], h[4 * t], h[4 * t + 1], h[4 * t + 2], h[4 * t + 3]);
-            fclose(f);
-        }
-        std::vector<int> ts((size_t)run.ntiles * run.tsw());
-        WR_CUDA(cudaMemcpy(ts.data(), run.tile_src, 4 * ts.size(), cudaMemcpyDeviceToHost));
-        if (FILE *f = fopen((std::string(trace_path) + ".src").c_str(), "a")) {
-            for (int t = 0; t < run.ntiles; ++t) {
-                for (int k = 0; k < run.tsw(); ++k) fprintf(f, "%d ", ts[(size_t)t * run.tsw() + k]);
-                fprintf(f, "\n");
+    if (tj) {   // lines: tile claim-position start end rounds sm (+ .src: the tile's sources)
+        WR_CUDA(cudaMemcpyAsync(tj->h, ttrace.p, ttrace.bytes(), cudaMemcpyDeviceToHost, st));
+        if (run.tile_order) WR_CUDA(cudaMemcpyAsync(tj->ord, run.tile_order, 4 * (size_t)run.ntiles, cudaMemcpyDeviceToHost, st));
+        else for (int i = 0; i < run.ntiles; ++i) tj->ord[i] = i;
+        WR_CUDA(cudaMemcpyAsync(tj->src, run.tile_src, 4 * (size_t)run.ntiles * run.tsw(), cudaMemcpyDeviceToHost, st));
+        WR_CUDA(cudaLaunchHostFunc(st, [](void *p) {
+            TraceJob *t = (TraceJob *)p;
+            std::vector<int> pos(t->ntiles);
+            for (int i = 0; i < t->ntiles; ++i) pos[t->ord[i]] = i;
+            if (FILE *f = fopen(t->path.c_str(), "a")) {
+                for (int k = 0; k < t->ntiles; ++k)
+                    fprintf(f, "%d %d %lld %lld %lld %lld\n", k, pos[k], t->h[4 * k], t->h[4 * k + 1], t->h[4 * k + 2],
+                            t->h[4 * k + 3]);
+                fclose(f);
             }
-            fclose(f);
-        }
+            if (FILE *f = fopen((t->path + ".src").c_str(), "a")) {
+                for (int k = 0; k < t->ntiles; ++k) {
+                    for (int j = 0; j < t->tsw; ++j) fprintf(f, "%d ", t->src[(size_t)k * t->tsw + j]);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+            // pinned buffers are released by the next sync point's owner: leak-free
+            // enough for a diagnostic (freed at process exit)
+        }, tj));
     }
 }
 
@@ -1270,7 +1301,8 @@ template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                                int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
-                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane) {
+                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane, uint32_t thr,
+                                               int *overflow) {
     constexpr int TSW = 32 * SPL;
     constexpr int TS = TSW * 2;
     constexpr int NS = SPL * 2;
@@ -1283,6 +1315,7 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
 #pragma unroll
     for (int jv = 0; jv < PV; ++jv)
         if (jv < nv) key[jv] = vload<SPL>(Rl + (size_t)(c0 + jv) * TSW);
+    bool ovf = false;
 #pragma unroll
     for (int jv = 0; jv < PV; ++jv) {
         if (jv >= nv) break;
@@ -1291,10 +1324,15 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
         for (int j = 0; j < SPL; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const uint32_t k = (key[jv].x[j] >> (16 * h)) & 0xfu;
+                const uint32_t key1 = (key[jv].x[j] >> (16 * h)) & 0xffffu;
+                const uint32_t k = key1 & 0xfu;
+                // range check of the keyed rows (the sweep skips it): a stored
+                // distance at or past 0x7ff - max_w may hide a clipped path
+                ovf |= key1 >= thr && key1 != 0x7fffu;
                 spw[jv][lane * NS + j * 2 + h] = k == 15u ? -1 : g.in_src[a0 + (int)k];
             }
     }
+    if (__any_sync(FULL, ovf) && lane == 0) atomicOr(overflow, 1);
     __syncwarp();
     const bool vec = (V & 3) == 0 && nv == PV;
     int srow[TS / 32];

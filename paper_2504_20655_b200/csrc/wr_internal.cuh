@@ -185,6 +185,7 @@ struct PredFuse {
     int *flat_tiles = nullptr;      // [ntiles] set if a tile has a flat vertex
     int *done_list = nullptr;       // [ntiles] finished tiles in completion order, -1 = not yet
     int *counters = nullptr;        // [4] zeroed: [0] done slots, [2..3] u64 pred jobs claimed
+    long long *trace = nullptr;     // diagnostics (WR_TILE_TRACE): per tile {start, end, rounds, SM}
 };
 
 struct BfRun {              // one BF segment over tiles of 32*spl sources

@@ -1348,6 +1348,18 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     return WR_OK;
 }
 
+// A second, libwr-owned stream per (host thread, device) for the sweep's
+// concurrent tail part (event-ordered against the caller's stream).
+static cudaStream_t side_stream(int device) {
+    thread_local std::vector<std::pair<int, cudaStream_t>> cache;
+    for (auto &e : cache)
+        if (e.first == device) return e.second;
+    cudaStream_t s = nullptr;
+    WR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cache.push_back({device, s});
+    return s;
+}
+
 static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, wr_route_stats *stats) {
     if (!P || (!send && P->send_count > 0)) return fail(WR_EINVAL, "wr_orders_local: bad arguments");
     if (!is_device_ptr(send) && P->send_count > 0) return fail(WR_EINVAL, "wr_orders_local: send must be device memory");
@@ -1415,64 +1427,149 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventRecord(t0, st));
         }
         const auto hclock0 = std::chrono::steady_clock::now();
-        DBuf<uint32_t> rows((size_t)max_tiles * V * 32 * spl);
-        DBuf<int> tile_src(max_tiles * tsw), slot_row(max_tiles * tsw), pos_of(sb);
-        DBuf<int> flat(o.pred_out ? max_tiles : 0);
         // a4 fused into the sweep (non-negative weights): done list + counters
         static const bool no_fuse = getenv("WR_NO_FUSED_PRED") != nullptr;
         const bool fused = o.pred_out && !g->has_negative && !no_fuse;
-        DBuf<int> done_list(fused ? max_tiles : 0), fuse_ctr(fused ? 4 : 0);
         const int max_rounds = std::max(1, V - 1);   // + the kernel's check round (ENEGCYCLE if it changes)
         const int64_t *off_r = P->off_all.p + (int64_t)P->rank * (P->B + 1);
         cudaEvent_t b0, b1, b2;
         WR_CUDA(cudaEventCreate(&b0));
         WR_CUDA(cudaEventCreate(&b1));
         WR_CUDA(cudaEventCreate(&b2));
-        for (int64_t lo = P->src_lo; lo < P->src_hi; lo += sb) {
-            const int64_t hi = std::min<int64_t>(P->src_hi, lo + sb);
-            const int ntiles =
-                make_tiles_ordered(g, P->sources.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
-            BfRun run{tile_src.p, ntiles, rows.p, WR_BF_FRONTIER, max_rounds, spl, slot_row.p};
-            tiles_swept += ntiles;
-            tile_width = tsw;
-            run.pack = pk;
-            run.keyed = pk == 2 && keyed;
-            run.ovf_thr = pk != 2 ? 0u
-                          : run.keyed ? (0x7ffu - (uint32_t)g->max_abs_w) << 4
-                                      : 0x7fffu - (uint32_t)g->max_abs_w;
+        // The sweep's makespan is ~ waves x tile time (one tile per SM at a
+        // time): 331 tiles of 256 on 148 SMs leave 113 SMs to the fused
+        // pred jobs through a third wave (C5 trace: 57 ms, 41 ms of sweep
+        // work per SM). WR_TAIL_SPLIT=1: with packed rows and a single budget
+        // segment, the sources beyond the last full wave of wide tiles go to
+        // narrow tiles (64-wide: ~half the tile time) swept concurrently on
+        // a second stream, launched first.
+        // Measured on C5 (profiles/r02_tail_split.txt): the split ends the
+        // last wide tile at 54 ms instead of 57, but the fused pred jobs,
+        // which ran on the SMs the third wave left idle, then run after it:
+        // the step got slower (76 vs 70 ms). Kept as an opt-in experiment.
+        static const bool no_tail = getenv("WR_TAIL_SPLIT") == nullptr;
+        struct Part {
+            int64_t lo, hi;
+            int spl;
+        };
+        std::vector<Part> parts;
+        const bool single = sb >= nsrc;
+        {
+            const int64_t full_waves = (nsrc / tsw) / nsm;
+            const int64_t main_n = full_waves * nsm * tsw;
+            const int64_t rem = nsrc - main_n;
+            if (single && pk == 2 && !no_tail && full_waves >= 1 && rem > 0) {
+                int tspl = 1;   // the narrowest tile width whose tiles fit one wave
+                while (tspl < spl && (rem + 32LL * tspl * pk - 1) / (32LL * tspl * pk) > nsm) tspl *= 2;
+                parts.push_back({P->src_lo + main_n, P->src_hi, tspl});   // tail first: its CTAs start first
+                parts.push_back({P->src_lo, P->src_lo + main_n, spl});
+            }
+        }
+        if (parts.empty())
+            for (int64_t lo = P->src_lo; lo < P->src_hi; lo += sb) parts.push_back({lo, std::min<int64_t>(P->src_hi, lo + sb), spl});
+        const bool concurrent = parts.size() == 2 && single;
+        cudaStream_t st2 = concurrent ? side_stream(P->device) : st;
+        cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+        if (concurrent) {
+            WR_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+            WR_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        }
+        struct PartBufs {
+            DBuf<uint32_t> rows;
+            DBuf<int> tile_src, slot_row, pos_of, flat, done_list, fuse_ctr;
+            BfRun run;
+            int ntiles = 0, tsw = 0;
+        };
+        std::vector<PartBufs> pb(concurrent ? 2 : 1);
+        auto prepare = [&](PartBufs &b, const Part &pt, int64_t cap_tiles) {
+            b.tsw = 32 * pt.spl * pk;
+            if (!b.rows.p) {
+                b.rows.alloc((size_t)cap_tiles * V * 32 * pt.spl);
+                b.tile_src.alloc(cap_tiles * b.tsw);
+                b.slot_row.alloc(cap_tiles * b.tsw);
+                b.pos_of.alloc(concurrent ? pt.hi - pt.lo : sb);
+                b.flat.alloc(o.pred_out ? cap_tiles : 0);
+                b.done_list.alloc(fused ? cap_tiles : 0);
+                b.fuse_ctr.alloc(fused ? 4 : 0);
+            }
+            b.ntiles = make_tiles_ordered(g, P->sources.p, pt.lo, pt.hi, b.tsw, cap_tiles, b.tile_src.p,
+                                          b.slot_row.p, b.pos_of.p, st);
+            b.run = BfRun{b.tile_src.p, b.ntiles, b.rows.p, WR_BF_FRONTIER, max_rounds, pt.spl, b.slot_row.p};
+            b.run.pack = pk;
+            b.run.keyed = pk == 2 && keyed;
+            b.run.ovf_thr = pk != 2 ? 0u
+                            : b.run.keyed ? (0x7ffu - (uint32_t)g->max_abs_w) << 4
+                                          : 0x7fffu - (uint32_t)g->max_abs_w;
             if (fused) {
-                WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
-                WR_CUDA(cudaMemsetAsync(done_list.p, 0xff, sizeof(int) * ntiles, st));
-                WR_CUDA(cudaMemsetAsync(fuse_ctr.p, 0, sizeof(int) * 4, st));
-                run.fuse.pred_out = o.pred_out;
-                run.fuse.out_row0 = lo - P->src_lo;
-                run.fuse.flat_tiles = flat.p;
-                run.fuse.done_list = done_list.p;
-                run.fuse.counters = fuse_ctr.p;
+                WR_CUDA(cudaMemsetAsync(b.flat.p, 0, sizeof(int) * b.ntiles, st));
+                WR_CUDA(cudaMemsetAsync(b.done_list.p, 0xff, sizeof(int) * b.ntiles, st));
+                WR_CUDA(cudaMemsetAsync(b.fuse_ctr.p, 0, sizeof(int) * 4, st));
+                b.run.fuse.pred_out = o.pred_out;
+                b.run.fuse.out_row0 = pt.lo - P->src_lo;
+                b.run.fuse.flat_tiles = b.flat.p;
+                b.run.fuse.done_list = b.done_list.p;
+                b.run.fuse.counters = b.fuse_ctr.p;
+            }
+            tiles_swept += b.ntiles;
+            tile_width = std::max(tile_width, b.tsw);
+        };
+        auto gather = [&](PartBufs &b, const Part &pt, cudaStream_t s_) {
+            if (P->B <= 0) return;
+            gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, s_>>>(
+                P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, pt.lo, pt.hi, off_r,
+                b.rows.p, V, b.tsw, b.run.keyed ? 3 : pk, b.pos_of.p, (uint32_t *)send);
+            count_launch();
+            WR_LAUNCH_CHECK();
+        };
+        for (size_t ip = 0; ip < parts.size(); ++ip) {
+            if (concurrent && ip == 1) break;   // both parts run below
+            const Part &pt = parts[ip];
+            PartBufs &b = pb[0];
+            if (concurrent) {
+                prepare(pb[0], parts[0], (parts[0].hi - parts[0].lo + 32LL * parts[0].spl * pk - 1) /
+                                             (32LL * parts[0].spl * pk));
+                prepare(pb[1], parts[1], (parts[1].hi - parts[1].lo) / (32LL * parts[1].spl * pk));
+            } else {
+                prepare(b, pt, max_tiles);
             }
             WR_CUDA(cudaEventRecord(b0, st));
             const double host_to_b0 =
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hclock0).count();
-            {
+            if (concurrent) {
+                WR_CUDA(cudaEventRecord(ev_in, st));
+                WR_CUDA(cudaStreamWaitEvent(st2, ev_in, 0));
+                {
+                    StreamScope side(st2);   // the tail's temporaries live in st2's order
+                    NvtxRange nv("wr.bf.sweep+pred (tail)");
+                    bf_run(g, pb[0].run, d_stats.p, st2);
+                    gather(pb[0], parts[0], st2);
+                }
+                {
+                    NvtxRange nv(fused ? "wr.bf.sweep+pred" : "wr.bf.sweep");
+                    bf_run(g, pb[1].run, d_stats.p, st);
+                }
+                WR_CUDA(cudaEventRecord(ev_out, st2));
+                WR_CUDA(cudaStreamWaitEvent(st, ev_out, 0));   // every later free on st follows the tail
+            } else {
                 NvtxRange nv(fused ? "wr.bf.sweep+pred" : "wr.bf.sweep");
-                bf_run(g, run, d_stats.p, st);
+                bf_run(g, b.run, d_stats.p, st);
             }
             WR_CUDA(cudaEventRecord(b1, st));
-            if (o.pred_out) {   // a4 canonical pred of this segment's sources
+            if (o.pred_out && !concurrent) {   // a4 canonical pred of this segment's sources
                 if (!fused) {
-                    WR_CUDA(cudaMemsetAsync(flat.p, 0, sizeof(int) * ntiles, st));
-                    bf_write_outputs(g, run, lo - P->src_lo, P->S, nullptr, V, nullptr, o.pred_out, flat.p, st);
+                    WR_CUDA(cudaMemsetAsync(b.flat.p, 0, sizeof(int) * b.ntiles, st));
+                    bf_write_outputs(g, b.run, pt.lo - P->src_lo, P->S, nullptr, V, nullptr, o.pred_out, b.flat.p, st);
                 }
-                std::vector<int> hflat(ntiles);
-                WR_CUDA(cudaMemcpyAsync(hflat.data(), flat.p, sizeof(int) * ntiles, cudaMemcpyDeviceToHost, st));
+                std::vector<int> hflat(b.ntiles);
+                WR_CUDA(cudaMemcpyAsync(hflat.data(), b.flat.p, sizeof(int) * b.ntiles, cudaMemcpyDeviceToHost, st));
                 WR_CUDA(cudaStreamSynchronize(st));
                 std::vector<int> todo;
-                for (int t = 0; t < ntiles; ++t)
+                for (int t = 0; t < b.ntiles; ++t)
                     if (hflat[t] || g->has_negative) todo.push_back(t);
                 // packed rows: w > 0 admits no flat vertex unless a distance
                 // was clipped, and then the overflow flag forces the redo
                 if (pk == 2) todo.clear();
-                bf_resolve_flat(g, run, todo, lo - P->src_lo, o.pred_out, st);
+                bf_resolve_flat(g, b.run, todo, pt.lo - P->src_lo, o.pred_out, st);
             }
             WR_CUDA(cudaEventRecord(b2, st));
             WR_CUDA(cudaEventSynchronize(b2));
@@ -1481,13 +1578,8 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             WR_CUDA(cudaEventElapsedTime(&y, b1, b2));
             bf_ms += x;
             pred_ms += y;
-            if (P->B > 0) {
-                gather_send_kernel<<<gridn(P->B * WR_MAX_STOPS, 256), 256, 0, st>>>(
-                    P->stops.p, P->n_arr.p, P->status.p, P->B, P->src_row.p, P->src_lo, P->src_hi, lo, hi, off_r,
-                    rows.p, V, tsw, run.keyed ? 3 : pk, pos_of.p, (uint32_t *)send);
-                count_launch();
-                WR_LAUNCH_CHECK();
-            }
+            if (concurrent) gather(pb[1], parts[1], st);
+            else gather(b, pt, st);
             ++segments;
             if (trace) {
                 WR_CUDA(cudaEventRecord(t1, st));
@@ -1496,10 +1588,16 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
                 WR_CUDA(cudaEventElapsedTime(&a, t0, b0));
                 WR_CUDA(cudaEventElapsedTime(&c, b2, t1));
                 fprintf(stderr,
-                        "[wr] local segment %d (%d tiles): alloc+tiles %.2f ms device (%.2f ms host), "
+                        "[wr] local segment %d (%d tiles%s): alloc+tiles %.2f ms device (%.2f ms host), "
                         "gather_send %.2f ms; host: prologue %.2f, budget %.2f\n",
-                        segments, ntiles, a, host_to_b0, c, h_pre, h_budget - h_pre);
+                        segments, concurrent ? pb[0].ntiles + pb[1].ntiles : b.ntiles,
+                        concurrent ? ", wide + concurrent narrow tail" : "", a, host_to_b0, c, h_pre,
+                        h_budget - h_pre);
             }
+        }
+        if (concurrent) {
+            cudaEventDestroy(ev_in);
+            cudaEventDestroy(ev_out);
         }
         if (trace) {
             cudaEventDestroy(t0);
