@@ -61,7 +61,12 @@ def lib():
         L.orc_bf_many.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int]
         L.orc_pred_many.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
         L.orc_route_orders.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, vp, C.c_longlong,
-                                       C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int]
+                                       C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_int]
+        L.orc_closed_route_cost.argtypes = [C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, vp]
+        L.orc_exact_closed_route.argtypes = [C.c_int, vp, vp, vp, C.c_int, vp, vp, lp]
+        L.orc_held_karp_closed_route.argtypes = [C.c_int, vp, vp, vp, C.c_int, vp, vp, lp]
+        L.orc_segmented_closed_route.argtypes = [C.c_int, vp, vp, vp, C.c_int, vp, vp, vp, vp]
+        L.orc_segmented_pairs_closed_route.argtypes = [C.c_int, vp, vp, vp, C.c_int, vp, vp, vp, vp]
         L.orc_certificate.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, C.c_int]
         L.orc_certificate.restype = C.c_longlong
         L.orc_pred_certificate.argtypes = [C.c_int, C.c_longlong, vp, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, lp]
@@ -271,6 +276,58 @@ def perm_rank(seq) -> int:
     return lib().orc_perm_rank(_p(seq), seq.size)
 
 
+def _legs(D, din, dout):
+    D, wt, n = _D(D)
+    din = np.ascontiguousarray(din, dtype=_vdt(wt)).reshape(n)
+    dout = np.ascontiguousarray(dout, dtype=_vdt(wt)).reshape(n)
+    return D, wt, n, din, dout
+
+
+def closed_route_cost(D, din, dout, seq):
+    """NEXT-4: cost of the closed tour depot -> seq -> depot (left to right)."""
+    D, wt, n, din, dout = _legs(D, din, dout)
+    seq = np.ascontiguousarray(seq, dtype=np.int32)
+    out = np.zeros(1, dtype=_vdt(wt))
+    rc = lib().orc_closed_route_cost(wt, _p(D), _p(din), _p(dout), n, _p(seq), seq.size, _p(out))
+    if rc:
+        raise OracleError(rc, "closed_route_cost")
+    return out[0]
+
+
+def _closed_call(fn, name, D, din, dout, *extra):
+    D, wt, n, din, dout = _legs(D, din, dout)
+    seq = np.zeros(n, dtype=np.int32)
+    cost = np.zeros(1, dtype=_vdt(wt))
+    tail = np.zeros(2, dtype=np.int64)
+    args = [wt, _p(D), _p(din), _p(dout), n] + [_p(np.ascontiguousarray(e, dtype=np.int32)) for e in extra]
+    rc = fn(*args, _p(seq), _p(cost), _p(tail) if extra else C.cast(C.c_void_p(tail.ctypes.data), C.POINTER(C.c_longlong)))
+    if rc:
+        raise OracleError(rc, name)
+    return cost[0], seq, tail
+
+
+def exact_closed_route(D, din, dout):
+    """NEXT-4 exact closed tour over all n! orders: (cost, rank, seq)."""
+    c, s, t = _closed_call(lib().orc_exact_closed_route, "exact_closed_route", D, din, dout)
+    return c, int(t[0]), s
+
+
+def held_karp_closed_route(D, din, dout):
+    c, s, t = _closed_call(lib().orc_held_karp_closed_route, "held_karp_closed_route", D, din, dout)
+    return c, int(t[0]), s
+
+
+def segmented_closed_route(D, din, dout, labels):
+    c, s, t = _closed_call(lib().orc_segmented_closed_route, "segmented_closed_route", D, din, dout, labels)
+    return c, s, (int(t[0]), int(t[1]))
+
+
+def segmented_pairs_closed_route(D, din, dout, labels):
+    c, s, t = _closed_call(lib().orc_segmented_pairs_closed_route, "segmented_pairs_closed_route", D, din, dout,
+                           labels)
+    return c, s, (int(t[0]), int(t[1]))
+
+
 def route_count_reduction(n_j):
     n_j = np.ascontiguousarray(n_j, dtype=np.int32)
     red, brute = C.c_ulonglong(0), C.c_ulonglong(0)
@@ -278,8 +335,9 @@ def route_count_reduction(n_j):
     return red.value, brute.value
 
 
-def route_orders(g, orders, m: int = 1, nthreads: int = None, pairs: bool = False):
-    """a2..a7 composed. Returns dict(n, seq [B,16] node ids, cost, rank, rc)."""
+def route_orders(g, orders, m: int = 1, nthreads: int = None, pairs: bool = False, depot: int = -1):
+    """a2..a7 composed. Returns dict(n, seq [B,16] node ids, cost, rank, rc).
+    depot >= 0: the NEXT-4 closed tour through that node (reading R4)."""
     V, src, dst, w = _graph(g)
     wt = _wt(w)
     B = orders.B
@@ -293,7 +351,7 @@ def route_orders(g, orders, m: int = 1, nthreads: int = None, pairs: bool = Fals
     out_rc = np.zeros(B, dtype=np.int32)
     rc = lib().orc_route_orders(V, src.size, _p(src), _p(dst), _p(w), wt, _p(ptr), _p(nodes), B, m,
                                 _p(xy), nthreads or os.cpu_count(), _p(out_n), _p(out_seq),
-                                _p(out_cost), _p(out_rank), _p(out_rc), 1 if pairs else 0)
+                                _p(out_cost), _p(out_rank), _p(out_rc), 1 if pairs else 0, int(depot))
     return dict(rc=rc, n=out_n, seq=out_seq, cost=out_cost, rank=out_rank, order_rc=out_rc)
 
 

@@ -42,6 +42,16 @@
  *                     reproducers (tests/golden/hk_absorption.txt); == O5 on
  *                     n <= 9 incl. tie-heavy matrices; cost == the tests'
  *                     independent Python Held-Karp for n up to 13.
+ *   orc_closed_route_cost / orc_exact_closed_route / orc_held_karp_closed_route
+ *   / orc_segmented_closed_route / orc_segmented_pairs_closed_route
+ *                     NEXT-4 closed tour through a depot (reading R4, P320 §3:
+ *                     the paper leaves entrance/exit out; the closed variant
+ *                     adds the two depot legs) pinned: hand-checked tour of the
+ *                     3-aisle example (cost 32, rank 1, 8 optima); itertools
+ *                     brute force (cost, rank, order) incl. fp32 absorption;
+ *                     zero legs == every open counterpart bit for bit;
+ *                     singletons == exact; pairs == brute force over
+ *                     segment-contiguous closed orders (int).
  *   orc_kmeans        O8 deterministic integer K-means   pinned: hand-made
  *                     separated clusters, brute-force Lloyd fixpoint check.
  *   orc_order_stops   a2 stop projection (P226-238 §2.4) pinned: numpy unique.
@@ -402,11 +412,23 @@ static float f32_inv(float d, float m)
     return f32_of_bits(lo);
 }
 
+/* din / dout (NEXT-4 closed tour, reading R4): NULL for the open route, or  */
+/* the n depot legs D[depot][j] and D[i][depot]: the tour is depot -> pi ->  */
+/* depot, summed left to right from the first depot leg.                     */
+static int held_karp_impl(int wtype, const void *D, const void *din, const void *dout, int n,
+                          int *seq_out, void *cost_out, long long *rank_out);
+
 int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cost_out,
                         long long *rank_out)
 {
+    return held_karp_impl(wtype, D, NULL, NULL, n, seq_out, cost_out, rank_out);
+}
+
+static int held_karp_impl(int wtype, const void *D, const void *din, const void *dout, int n,
+                          int *seq_out, void *cost_out, long long *rank_out)
+{
     if (n < 1 || n > 16) return ORC_EINVAL;
-    if (n == 1) {
+    if (n == 1 && !din) {
         seq_out[0] = 0;
         memset(cost_out, 0, 4);
         *rank_out = 0;
@@ -426,7 +448,15 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
         for (int j = 0; j < n; ++j) {
             if (!((S >> j) & 1)) continue;
             const size_t P = S & ~((size_t)1 << j), st = S * n + j;
-            if (P == 0) { if (ci) ci[st] = 0; else cf[st] = 0.0f; continue; }
+            if (P == 0) {   /* first stop: prefix cost 0, or the depot leg */
+                if (ci) {
+                    const int leg = din ? ((const int *)din)[j] : 0;
+                    ci[st] = leg == I32_INF ? IINF : leg;
+                } else {
+                    cf[st] = din ? ((const float *)din)[j] : 0.0f;
+                }
+                continue;
+            }
             int first = 1;
             for (int i = 0; i < n; ++i) {
                 if (!((P >> i) & 1)) continue;
@@ -445,9 +475,18 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
     }
     int64_t cstar_i = 0;
     float cstar_f = 0.0f;
-    for (int j = 0; j < n; ++j) {
-        if (ci) { if (j == 0 || ci[F * n + j] < cstar_i) cstar_i = ci[F * n + j]; }
-        else { if (j == 0 || cf[F * n + j] < cstar_f) cstar_f = cf[F * n + j]; }
+    for (int j = 0; j < n; ++j) {   /* closed: + the return leg */
+        if (ci) {
+            int64_t c = ci[F * n + j];
+            if (dout) {
+                const int leg = ((const int *)dout)[j];
+                c = (leg == I32_INF || c >= IINF) ? IINF : c + leg;
+            }
+            if (j == 0 || c < cstar_i) cstar_i = c;
+        } else {
+            const float c = dout ? cf[F * n + j] + ((const float *)dout)[j] : cf[F * n + j];
+            if (j == 0 || c < cstar_f) cstar_f = c;
+        }
     }
     int all_inf = ci ? cstar_i >= IINF : isinf(cstar_f);
     if (all_inf) {                                   /* every order costs INF: O5 keeps rank 0 */
@@ -462,7 +501,16 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
         for (int j = 0; j < n; ++j) {
             if (!((S >> j) & 1)) continue;
             const size_t st = S * n + j;
-            if (S == F) { if (ci) ci[st] = cstar_i; else cf[st] = cstar_f; continue; }
+            if (S == F) {   /* M(all, j) = C*, or the largest prefix whose return leg stays <= C* */
+                if (!dout) { if (ci) ci[st] = cstar_i; else cf[st] = cstar_f; }
+                else if (ci) {
+                    const int leg = ((const int *)dout)[j];
+                    ci[st] = leg == I32_INF ? NONE : cstar_i - leg;
+                } else {
+                    cf[st] = f32_inv(((const float *)dout)[j], cstar_f);
+                }
+                continue;
+            }
             int64_t bi = NONE;
             float bf = -1.0f;
             for (int k = 0; k < n; ++k) {
@@ -494,10 +542,12 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
             if ((S >> k) & 1) continue;
             const size_t nx = (S | ((size_t)1 << k)) * n + k;
             if (ci) {
-                const int64_t c = t == 0 ? 0 : (Di[(size_t)j * n + k] == I32_INF ? IINF : pi + Di[(size_t)j * n + k]);
+                const int first = din ? ((const int *)din)[k] : 0;
+                const int64_t c = t == 0 ? (first == I32_INF ? IINF : first)
+                                         : (Di[(size_t)j * n + k] == I32_INF ? IINF : pi + Di[(size_t)j * n + k]);
                 if (ci[nx] != NONE && c < IINF && c <= ci[nx]) { pick = k; pi = c; }
             } else {
-                const float c = t == 0 ? 0.0f : pf + Df[(size_t)j * n + k];
+                const float c = t == 0 ? (din ? ((const float *)din)[k] : 0.0f) : pf + Df[(size_t)j * n + k];
                 if (cf[nx] >= 0.0f && c <= cf[nx]) { pick = k; pf = c; }
             }
         }
@@ -505,6 +555,10 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
         seq_out[t] = pick;
         S |= (size_t)1 << pick;
         j = pick;
+    }
+    if (dout) {   /* the return leg */
+        if (ci) pi += ((const int *)dout)[j];
+        else pf = pf + ((const float *)dout)[j];
     }
     int rc = ORC_OK;
     if (ci) {
@@ -516,6 +570,87 @@ int orc_held_karp_route(int wtype, const void *D, int n, int *seq_out, void *cos
     *rank_out = orc_perm_rank(seq_out, n);
     free(ci); free(cf);
     return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4 closed tour (reading R4 in DESIGN.md). The    */
+/* paper assumes "the entrance and exit are the same in the warehouse, and   */
+/* that these are not part of the route" (P320 §3); the closed variant puts  */
+/* them back: the picker leaves the depot, visits every stop, and returns.   */
+/* cost(pi) = left-to-right sum over the n + 2 legs depot -> pi_0 -> ... ->  */
+/* pi_{n-1} -> depot: c = D[dep][pi_0], c = fl(c + D[pi_{t-1}][pi_t]), then  */
+/* fl(c + D[pi_{n-1}][dep]). It is O4 on the augmented matrix whose index n */
+/* is the depot as the first stop and n + 1 the depot as the last, so the    */
+/* arithmetic is O4's. din[j] = D[dep][j], dout[i] = D[i][dep].              */
+/* ------------------------------------------------------------------------ */
+static void *closed_aug(const void *D, const void *din, const void *dout, int n)
+{
+    const int m = n + 2;
+    char *A = (char *)calloc((size_t)m * m, 4);
+    if (!A) return NULL;
+    for (int i = 0; i < n; ++i) {
+        memcpy(A + 4 * ((size_t)i * m), (const char *)D + 4 * ((size_t)i * n), 4 * (size_t)n);
+        memcpy(A + 4 * ((size_t)n * m + i), (const char *)din + 4 * (size_t)i, 4);        /* depot -> i */
+        memcpy(A + 4 * ((size_t)i * m + n + 1), (const char *)dout + 4 * (size_t)i, 4);   /* i -> depot */
+    }
+    return A;
+}
+
+static int closed_cost_aug(int wtype, const void *A, int n, const int *seq, int len, void *cost_out)
+{
+    int aug[40];
+    aug[0] = n;
+    for (int t = 0; t < len; ++t) aug[t + 1] = seq[t];
+    aug[len + 1] = n + 1;
+    return orc_route_cost(wtype, A, n + 2, aug, len + 2, cost_out);
+}
+
+int orc_closed_route_cost(int wtype, const void *D, const void *din, const void *dout, int n,
+                          const int *seq, int len, void *cost_out)
+{
+    if (n < 1 || n > 32 || len < 0 || len > 32) return ORC_EINVAL;
+    void *A = closed_aug(D, din, dout, n);
+    if (!A) return ORC_ENOMEM;
+    int rc = closed_cost_aug(wtype, A, n, seq, len, cost_out);
+    free(A);
+    return rc;
+}
+
+/* Exact closed tour: all n! orders (std::next_permutation order), first     */
+/* minimum (strict <): ties -> the lexicographically smallest order (O5).     */
+int orc_exact_closed_route(int wtype, const void *D, const void *din, const void *dout, int n,
+                           int *seq_out, void *cost_out, long long *rank_out)
+{
+    if (n < 1 || n > 12) return ORC_EINVAL;
+    void *A = closed_aug(D, din, dout, n);
+    if (!A) return ORC_ENOMEM;
+    int perm[32];
+    for (int k = 0; k < n; ++k) perm[k] = k;
+    char best[4] = {0}, cur[4] = {0};
+    long long r = 0, best_rank = -1;
+    do {
+        int rc = closed_cost_aug(wtype, A, n, perm, n, cur);
+        if (rc) { free(A); return rc; }
+        if (best_rank < 0 || cost_less(wtype, cur, best)) {
+            memcpy(best, cur, 4);
+            best_rank = r;
+            memcpy(seq_out, perm, sizeof(int) * (size_t)n);
+        }
+        ++r;
+    } while (next_perm(perm, n));
+    free(A);
+    memcpy(cost_out, best, 4);
+    *rank_out = best_rank;
+    return ORC_OK;
+}
+
+/* Held-Karp closed tour for up to 16 stops: the same three steps as         */
+/* orc_held_karp_route with the depot legs folded in (first state cost =     */
+/* D[dep][j]; C* and the backward bound include the return leg).             */
+int orc_held_karp_closed_route(int wtype, const void *D, const void *din, const void *dout, int n,
+                               int *seq_out, void *cost_out, long long *rank_out)
+{
+    return held_karp_impl(wtype, D, din, dout, n, seq_out, cost_out, rank_out);
 }
 
 /* O6 combine: chunks of <= C permutations, (cost, rank) lexicographic min. */
@@ -560,8 +695,26 @@ int orc_exact_route_chunked(int wtype, const void *D, int n, long long chunk,
 /* counts_out[0] = sum n_j! segment sequences, counts_out[1] = m'! 2^m'      */
 /* stitch candidates (twice Thm 3.1's undirected counts, reading A2).        */
 /* ------------------------------------------------------------------------ */
+static int segmented_impl(int wtype, const void *D, const void *din, const void *dout, int n,
+                          const int *labels, int *seq_out, void *cost_out, long long *counts_out);
+
 int orc_segmented_route(int wtype, const void *D, int n, const int *labels,
                         int *seq_out, void *cost_out, long long *counts_out)
+{
+    return segmented_impl(wtype, D, NULL, NULL, n, labels, seq_out, cost_out, counts_out);
+}
+
+/* NEXT-4 (reading R4): O7 for the closed tour - the segments' own routes    */
+/* stay open (Theorem 3.1 clusters), the stitch costs each concatenation as  */
+/* the full closed tour (depot legs included).                               */
+int orc_segmented_closed_route(int wtype, const void *D, const void *din, const void *dout, int n,
+                               const int *labels, int *seq_out, void *cost_out, long long *counts_out)
+{
+    return segmented_impl(wtype, D, din, dout, n, labels, seq_out, cost_out, counts_out);
+}
+
+static int segmented_impl(int wtype, const void *D, const void *din, const void *dout, int n,
+                          const int *labels, int *seq_out, void *cost_out, long long *counts_out)
 {
     if (n < 1 || n > 32) return ORC_EINVAL;
     int seg_of[32], nseg = 0, map_lab[32], map_id[32], nmap = 0;
@@ -606,7 +759,8 @@ int orc_segmented_route(int wtype, const void *D, int n, const int *labels,
                 for (int a = 0; a < nj; ++a)
                     cand[pos++] = ((b >> k) & 1) ? seg_route[j][nj - 1 - a] : seg_route[j][a];
             }
-            int rc = orc_route_cost(wtype, D, n, cand, n, cur);
+            int rc = din ? orc_closed_route_cost(wtype, D, din, dout, n, cand, n, cur)
+                         : orc_route_cost(wtype, D, n, cand, n, cur);
             if (rc) return rc;
             ++stitched;
             int better = !have || cost_less(wtype, cur, best);
@@ -641,8 +795,25 @@ int orc_segmented_route(int wtype, const void *D, int n, const int *labels,
 /* Candidates m! * prod_j pairs_j <= 2^26, else ETOOLARGE (as the GPU).      */
 /* counts_out = {segment orders evaluated, stitch candidates}.               */
 /* ------------------------------------------------------------------------ */
+static int pairs_impl(int wtype, const void *D, const void *din, const void *dout, int n, const int *labels,
+                      int *seq_out, void *cost_out, long long *counts_out);
+
 int orc_segmented_pairs_route(int wtype, const void *D, int n, const int *labels,
                               int *seq_out, void *cost_out, long long *counts_out)
+{
+    return pairs_impl(wtype, D, NULL, NULL, n, labels, seq_out, cost_out, counts_out);
+}
+
+/* NEXT-4 x NEXT-1: the pair stitch of a closed tour (segment paths open,    */
+/* every stitch candidate costed as the full closed tour).                   */
+int orc_segmented_pairs_closed_route(int wtype, const void *D, const void *din, const void *dout, int n,
+                                     const int *labels, int *seq_out, void *cost_out, long long *counts_out)
+{
+    return pairs_impl(wtype, D, din, dout, n, labels, seq_out, cost_out, counts_out);
+}
+
+static int pairs_impl(int wtype, const void *D, const void *din, const void *dout, int n, const int *labels,
+                      int *seq_out, void *cost_out, long long *counts_out)
 {
     if (n < 1 || n > 16) return ORC_EINVAL;
     int seg_of[16], nseg = 0, map_lab[16], map_id[16], nmap = 0;
@@ -705,7 +876,10 @@ int orc_segmented_pairs_route(int wtype, const void *D, int n, const int *labels
                 const int a = pair_a[j][choice[k]], b = pair_b[j][choice[k]];
                 for (int t = 0; t < nj; ++t) cand[pos++] = path[j][a][b][t];
             }
-            if (n >= 2) {
+            if (din) {
+                int rc = orc_closed_route_cost(wtype, D, din, dout, n, cand, n, cur);
+                if (rc) return rc;
+            } else if (n >= 2) {
                 int rc = orc_route_cost(wtype, D, n, cand, n, cur);
                 if (rc) return rc;
             } else {
@@ -908,7 +1082,7 @@ typedef struct {
     const long long *order_ptr; const int *order_nodes; long long B;
     int m; const int *xy; const int *labels_in;
     int *out_n; int *out_seq; void *out_cost; long long *out_rank; int *out_rc;
-    long long next; pthread_mutex_t mu; int pairs;
+    long long next; pthread_mutex_t mu; int pairs; int depot;
 } route_job;
 
 static void *route_worker(void *arg)
@@ -934,12 +1108,28 @@ static void *route_worker(void *arg)
                 if (!finite_at(j->wtype, row, stops[b])) unreachable = 1;
             }
         }
+        /* NEXT-4 closed tour: the depot legs, from the depot's row and the   */
+        /* stops' rows at the depot column                                    */
+        char din[16 * 4], dout[16 * 4];
+        const int closed = j->depot >= 0;
+        if (closed) {
+            const char *drow = (const char *)j->rows + (size_t)4 * j->V * j->row_of[j->depot];
+            for (int a = 0; a < n; ++a) {
+                memcpy(din + 4 * a, drow + 4 * (size_t)stops[a], 4);
+                const char *row = (const char *)j->rows + (size_t)4 * j->V * j->row_of[stops[a]];
+                memcpy(dout + 4 * a, row + 4 * (size_t)j->depot, 4);
+                if (!finite_at(j->wtype, drow, stops[a]) || !finite_at(j->wtype, row, j->depot)) unreachable = 1;
+            }
+        }
         if (unreachable) { j->out_rc[o] = ORC_EUNREACHABLE; continue; }
         int seq[32], rc;
         char cost[4];
         long long rank = 0;
         if (j->m <= 1) {
-            if (n > 12) rc = orc_held_karp_route(j->wtype, D, n, seq, cost, &rank);   /* NEXT-2 */
+            if (closed)
+                rc = n > 12 ? orc_held_karp_closed_route(j->wtype, D, din, dout, n, seq, cost, &rank)
+                            : orc_exact_closed_route(j->wtype, D, din, dout, n, seq, cost, &rank);
+            else if (n > 12) rc = orc_held_karp_route(j->wtype, D, n, seq, cost, &rank);   /* NEXT-2 */
             else rc = orc_exact_route(j->wtype, D, n, seq, cost, &rank);
         } else {
             int labels[32], xy[64];
@@ -950,7 +1140,9 @@ static void *route_worker(void *arg)
                 orc_kmeans(xy, n, j->m, labels);
             }
             long long counts[2];
-            if (j->pairs) rc = orc_segmented_pairs_route(j->wtype, D, n, labels, seq, cost, counts);
+            if (closed && j->pairs) rc = orc_segmented_pairs_closed_route(j->wtype, D, din, dout, n, labels, seq, cost, counts);
+            else if (closed) rc = orc_segmented_closed_route(j->wtype, D, din, dout, n, labels, seq, cost, counts);
+            else if (j->pairs) rc = orc_segmented_pairs_route(j->wtype, D, n, labels, seq, cost, counts);
             else rc = orc_segmented_route(j->wtype, D, n, labels, seq, cost, counts);
             rank = orc_perm_rank(seq, n);
         }
@@ -971,12 +1163,14 @@ int orc_route_orders(int V, long long E, const int *src, const int *dst, const v
                      int wtype, const long long *order_ptr, const int *order_nodes,
                      long long B, int m, const int *xy, int nthreads,
                      int *out_n, int *out_seq, void *out_cost, long long *out_rank,
-                     int *out_rc, int pairs)
+                     int *out_rc, int pairs, int depot)
 {
+    if (depot >= V) return ORC_EINVAL;
     int *row_of = (int *)malloc(sizeof(int) * (size_t)V);
     for (int v = 0; v < V; ++v) row_of[v] = -1;
     long long L = order_ptr[B];
     for (long long a = 0; a < L; ++a) row_of[order_nodes[a]] = 1;
+    if (depot >= 0) row_of[depot] = 1;   /* NEXT-4: the depot is a BF source too */
     int S = 0;
     for (int v = 0; v < V; ++v) if (row_of[v] >= 0) row_of[v] = S++;
     int *sources = (int *)malloc(sizeof(int) * (size_t)(S > 0 ? S : 1));
@@ -986,7 +1180,7 @@ int orc_route_orders(int V, long long E, const int *src, const int *dst, const v
     int rc = orc_bf_many(V, E, src, dst, w, wtype, sources, S, rows, nthreads);
     if (rc == ORC_OK) {
         route_job j = {wtype, V, row_of, rows, order_ptr, order_nodes, B, m, xy, NULL,
-                       out_n, out_seq, out_cost, out_rank, out_rc, 0, PTHREAD_MUTEX_INITIALIZER, pairs};
+                       out_n, out_seq, out_cost, out_rank, out_rc, 0, PTHREAD_MUTEX_INITIALIZER, pairs, depot};
         pthread_t th[256];
         if (nthreads < 1) nthreads = 1;
         if (nthreads > 256) nthreads = 256;

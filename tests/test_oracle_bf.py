@@ -154,6 +154,9 @@ def load_three_aisle():
         elif k == "segmented":
             rec["segmented"].append(([int(x) for x in rest[0].split(",")], int(rest[1]),
                                      [int(x) for x in rest[2].split(",")]))
+        elif k == "closed":
+            rec["closed"] = (int(rest[0]), [int(x) for x in rest[1].split(",")], int(rest[2]),
+                             [int(x) for x in rest[3].split(",")], int(rest[4]), int(rest[5]))
         elif k in ("dist", "pred"):
             rec[k].append(tuple(int(x) for x in rest))
     rec["D"] = np.array(rec["D"], dtype=np.int32)

@@ -521,3 +521,153 @@ def test_route_orders_composition_c2():
         c, r, s = oracle.exact_route(D)
         assert res["cost"][o] == c and res["rank"][o] == r
         assert res["seq"][o, :len(stops)].tolist() == stops[s].tolist()
+
+
+# ------------------------------------------------ NEXT-4 closed tour (R4)
+def lr_closed(D, din, dout, seq):
+    """Closed tour depot -> seq -> depot written independently: the first
+    leg, then each stop leg, then the return leg, left to right."""
+    fp = D.dtype == np.float32
+    c = din[seq[0]]
+    legs = [D[a, b] for a, b in zip(seq[:-1], seq[1:])] + [dout[seq[-1]]]
+    for x in legs:
+        if fp:
+            c = np.float32(c + x)
+        else:
+            c = np.int32(INF) if (c == INF or x == INF) else np.int32(int(c) + int(x))
+    return c
+
+
+def brute_closed(D, din, dout):
+    best, nopt = None, 0
+    for r, p in enumerate(itertools.permutations(range(D.shape[0]))):
+        c = lr_closed(D, din, dout, p)
+        if best is None or c < best[0]:
+            best, nopt = (c, r, p), 1
+        elif c == best[0]:
+            nopt += 1
+    return best, nopt
+
+
+def legs_for(rng, n, kind):
+    if kind == "int":
+        return rng.integers(0, 30, n).astype(np.int32), rng.integers(0, 30, n).astype(np.int32)
+    return rng.uniform(0, 10, n).astype(np.float32), rng.uniform(0, 10, n).astype(np.float32)
+
+
+def test_closed_three_aisle_worked_example():
+    rec = load_three_aisle()
+    depot, din, cost, seq, rank, nopt = rec["closed"]
+    g = gen.aisle(3, 4, 2, ws=1, wa=3, wd=2)
+    picks = rec["picks"]
+    assert oracle.bf(g, depot)[picks].tolist() == din                 # the legs, by BF
+    assert [int(oracle.bf(g, p)[depot]) for p in picks] == din        # undirected: dout = din
+    D = rec["D"]
+    c, r, s = oracle.exact_closed_route(D, din, din)
+    assert (int(c), r, s.tolist()) == (cost, rank, seq)
+    (bc, br, bp), bn = brute_closed(D, np.array(din, np.int32), np.array(din, np.int32))
+    assert (int(bc), br, list(bp), bn) == (cost, rank, seq, nopt)
+    assert oracle.closed_route_cost(D, din, din, [0, 2, 1, 3, 4]) == 34   # the open optimum, closed
+    hc, hr, hs = oracle.held_karp_closed_route(D, din, din)
+    assert (int(hc), hr, hs.tolist()) == (cost, rank, seq)
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_closed_exact_and_held_karp_equal_brute_force(kind):
+    rng = np.random.default_rng(404 if kind == "int" else 405)
+    for trial in range(60):
+        n = int(rng.integers(1, 7))
+        D = random_D(rng, n, kind)
+        din, dout = legs_for(rng, n, kind)
+        (bc, br, bp), _ = brute_closed(D, din, dout)
+        c, r, s = oracle.exact_closed_route(D, din, dout)
+        assert c.tobytes() == np.asarray(bc).tobytes() and r == br and tuple(s) == bp, trial
+        hc, hr, hs = oracle.held_karp_closed_route(D, din, dout)
+        assert hc.tobytes() == c.tobytes() and hr == r and tuple(hs) == tuple(s), trial
+
+
+def test_closed_held_karp_fp32_absorption_vs_brute():
+    """Rounding ties with a far stop (reading A16) and far depot legs."""
+    rng = np.random.default_rng(406)
+    for trial in range(40):
+        n = int(rng.integers(3, 8))
+        D = absorption_D(rng, n)
+        din = (np.float32(1e8) + rng.integers(0, 4, n) * 8).astype(np.float32)
+        dout = rng.choice(np.array([0.5, 1, 2], np.float32), n).astype(np.float32)
+        (bc, br, bp), _ = brute_closed(D, din, dout)
+        hc, hr, hs = oracle.held_karp_closed_route(D, din, dout)
+        assert hc.tobytes() == np.asarray(bc).tobytes() and hr == br and tuple(hs) == bp, trial
+
+
+def test_closed_with_zero_legs_is_the_open_route():
+    """Zero depot legs reduce every closed function to its open counterpart
+    bit for bit (fl(0 + c) = c, fl(c + 0) = c): exact, Held-Karp, O7 and the
+    pair stitch."""
+    rng = np.random.default_rng(407)
+    for kind in ("int", "fp32"):
+        for trial in range(25):
+            n = int(rng.integers(2, 8))
+            D = random_D(rng, n, kind)
+            z = np.zeros(n, D.dtype)
+            a, b = oracle.exact_closed_route(D, z, z), oracle.exact_route(D)
+            assert a[0].tobytes() == b[0].tobytes() and a[1] == b[1] and np.array_equal(a[2], b[2])
+            h = oracle.held_karp_closed_route(D, z, z)
+            assert h[0].tobytes() == b[0].tobytes() and h[1] == b[1]
+            labels = rng.integers(0, 3, n).astype(np.int32)
+            sc, ss, sn = oracle.segmented_closed_route(D, z, z, labels)
+            oc, os_, on = oracle.segmented_route(D, labels)
+            assert sc.tobytes() == np.asarray(oc).tobytes() and np.array_equal(ss, os_) and sn == on
+            pc, ps, pn = oracle.segmented_pairs_closed_route(D, z, z, labels)
+            qc, qs, qn = oracle.segmented_pairs_route(D, labels)
+            assert pc.tobytes() == np.asarray(qc).tobytes() and np.array_equal(ps, qs) and pn == qn
+
+
+@pytest.mark.parametrize("kind", ["int", "fp32"])
+def test_closed_segmented_invariants(kind):
+    """O7 / pair stitch of a closed tour (segments routed open, the stitch
+    costs the closed tour): all-singleton labelings equal the exact closed
+    tour; one segment gives the better orientation of the open O5 route,
+    closed; any labeling costs >= the exact closed tour; the pair stitch
+    never costs more than O7 for int weights; an int instance equals brute
+    force over all segment-contiguous closed orders (the pair stitch's
+    definition)."""
+    rng = np.random.default_rng(408 if kind == "int" else 409)
+    for trial in range(25):
+        n = int(rng.integers(2, 8))
+        D = random_D(rng, n, kind)
+        din, dout = legs_for(rng, n, kind)
+        ec, er, es = oracle.exact_closed_route(D, din, dout)
+        c, s, _ = oracle.segmented_closed_route(D, din, dout, np.arange(n, dtype=np.int32))
+        assert c.tobytes() == ec.tobytes() and np.array_equal(s, es)
+        _, _, op = oracle.exact_route(D)
+        cands = sorted([(lr_closed(D, din, dout, q), tuple(q)) for q in (list(op), list(op)[::-1])])
+        c, s, _ = oracle.segmented_closed_route(D, din, dout, np.zeros(n, np.int32))
+        assert c.tobytes() == np.asarray(cands[0][0]).tobytes() and tuple(s) == cands[0][1]
+        labels = rng.integers(0, 3, n).astype(np.int32)
+        c, s, _ = oracle.segmented_closed_route(D, din, dout, labels)
+        assert c >= ec and lr_closed(D, din, dout, s).tobytes() == c.tobytes()
+        pc, ps, _ = oracle.segmented_pairs_closed_route(D, din, dout, labels)
+        assert lr_closed(D, din, dout, ps).tobytes() == pc.tobytes()
+        if kind == "int":
+            assert pc <= c
+            # brute force over orders whose segments are contiguous
+            best = None
+            for p in itertools.permutations(range(n)):
+                segs = [labels[i] for i in p]
+                runs = [k for k in range(n) if k == 0 or segs[k] != segs[k - 1]]
+                if len(runs) != len(set(labels.tolist())):
+                    continue
+                cc = lr_closed(D, din, dout, p)
+                if best is None or cc < best[0] or (cc == best[0] and p < best[1]):
+                    best = (cc, p)
+            assert int(pc) == int(best[0]) and tuple(ps) == best[1]
+
+
+def test_closed_reversal_invariance_int_symmetric():
+    rng = np.random.default_rng(410)
+    for _ in range(30):
+        n = int(rng.integers(2, 8))
+        D = random_D(rng, n, "int", symmetric=True)
+        din, _ = legs_for(rng, n, "int")
+        c, r, s = oracle.exact_closed_route(D, din, din)
+        assert lr_closed(D, din, din, s[::-1]) == c
