@@ -227,7 +227,7 @@ typedef struct {
                                 (world 1: 0..S-1; rank r: its own block)    */
     int64_t pred_rows;       /* rows available in pred_out (>= src_hi-src_lo) */
     int32_t flags;           /* WR_ROUTE_* bits, 0 = defaults               */
-    int32_t reserved;        /* must be 0                                   */
+    int32_t depot;           /* with WR_ROUTE_CLOSED: the depot node         */
     wr_ctx *ctx;             /* wr_route_orders only: NULL = this GPU alone;
                                 a context shards the sources and orders over
                                 its world (collective call, see below)      */
@@ -249,6 +249,15 @@ typedef struct {
 /* wr_route_opts.flags, with a context: write only this rank's block
  * [order_lo, order_hi) of the results (skips the result exchange). */
 #define WR_ROUTE_RANK_RESULTS 4
+/* wr_route_opts.flags: NEXT-4 closed tour (reading R4:
+ * the paper leaves entrance/exit out of the route, P320 §3). Every order is
+ * routed depot -> stops -> depot (opts.depot, a graph node), cost summed left
+ * to right from the first depot leg; exact orders minimise the closed cost
+ * over all orders of the stops (Held-Karp for 13-16), segmented ones keep the
+ * segments' routes open and cost every stitch candidate as the closed tour.
+ * The depot becomes a BF source; a closed order may hold at most 15 stops
+ * other than the depot (WR_ETOOLARGE). Results list the order's own stops. */
+#define WR_ROUTE_CLOSED 8
 
 typedef struct {
     int32_t n;               /* stops (distinct nodes, ascending before routing) */

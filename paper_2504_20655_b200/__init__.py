@@ -25,6 +25,7 @@ WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE = 0, 1, 2
 WR_ROUTE_ROWS32 = 1
 WR_ROUTE_PAIRS = 2
 WR_ROUTE_RANK_RESULTS = 4
+WR_ROUTE_CLOSED = 8
 NCCL_UID_BYTES = 128
 MAX_STOPS = 16
 DEFAULT_CHUNK = 2903040
@@ -71,7 +72,7 @@ class BfStats(C.Structure):
 class RouteOpts(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("async_", C.c_int32), ("m", C.c_int32), ("chunk", C.c_int64),
                 ("hbm_budget", C.c_int64), ("pred_out", C.c_void_p), ("pred_rows", C.c_int64),
-                ("flags", C.c_int32), ("reserved", C.c_int32), ("ctx", C.c_void_p)]
+                ("flags", C.c_int32), ("depot", C.c_int32), ("ctx", C.c_void_p)]
 
 
 class RouteStats(C.Structure):
@@ -310,14 +311,17 @@ def route_segmented(g: Graph, stops, labels=None, m: int = 1, chunk: int = 0, st
 
 def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, results=None,
                  hbm_budget: int = 0, stream=None, pred_out=None, flags: int = 0, labels=None,
-                 ctx: "Ctx" = None):
+                 ctx: "Ctx" = None, depot: int = None):
     """a2..a9: route every order. Returns (results, stats); results is a
     RESULT_DTYPE numpy array unless a device buffer is passed. pred_out: an
     optional device int32 tensor (>= S rows x V) receiving the canonical
     predecessor rows (a4) of the distinct stops in ascending order (with a
     ctx: the rank's own block of sources, row 0 = its src_lo). labels: an
     optional segment label per order line (stitched routes over the
-    caller's segments). ctx: shard over the context's ranks (collective)."""
+    caller's segments). ctx: shard over the context's ranks (collective).
+    depot: route closed tours through this node (WR_ROUTE_CLOSED, NEXT-4)."""
+    if depot is not None:
+        flags |= WR_ROUTE_CLOSED
     ptr = _arr(order_ptr, np.int64)
     nodes = _arr(order_nodes, np.int32)
     lab = _arr(labels, np.int32) if labels is not None else None
@@ -325,8 +329,8 @@ def route_orders(g: Graph, order_ptr, order_nodes, m: int = 1, chunk: int = 0, r
     if results is None:
         results = np.zeros(B, dtype=RESULT_DTYPE)
     o = RouteOpts(_stream_ptr(stream), 0, m, chunk, hbm_budget, _ptr(pred_out),
-                  int(pred_out.shape[0]) if pred_out is not None else 0, flags, 0,
-                  ctx.handle if ctx is not None else None)
+                  int(pred_out.shape[0]) if pred_out is not None else 0, flags,
+                  int(depot) if depot is not None else 0, ctx.handle if ctx is not None else None)
     st = RouteStats()
     _check(lib.wr_route_orders(g.handle, _ptr(ptr), _ptr(nodes), B, _ptr(lab), C.byref(o), _ptr(results),
                                C.byref(st)))

@@ -813,7 +813,10 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
     // 232 ms, 640 static 240, 768 lists 254 (the list order lets more
     // suboptimal values propagate: 4.4 vs 3.6 x S*E relaxations).
     // (the other shapes measured there - 384 x 2, 896, 704/768 with lists -
-    // were dropped from the build; WR_BF_CONFIG picks 8 or 11)
+    // were dropped from the build; WR_BF_CONFIG picks 8 or 11. Round 2,
+    // after the leaner task loop, keyed C5: 640 x (2 vertices x 2 tasks)
+    // 62.1 ms/step; 640 x 3x2 65.7 (spills), 512 x 3x2 63.9, 512 x 4x2 70.3,
+    // 768 x 2x2 63.4 - more gathers per warp do not pay at 96 registers)
     static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 11);
     bool ok = false;
     switch (cfg) {

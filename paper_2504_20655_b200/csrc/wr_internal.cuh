@@ -243,6 +243,7 @@ int64_t tiles_to_allocate(int64_t sb, int tsw, int64_t extra_bytes, int64_t tile
 struct RouteProblem {       // one exhaustive search (an order or a segment)
     int order;              // index into the D array
     int n;                  // stops in this problem (<= WR_MAX_EXACT)
+    int dep;                // -1 open; else the order-stop index of the depot (closed tour, NEXT-4)
     uint64_t map;           // 4-bit local -> order-stop index, position k at bits 4k
     int item0;              // first work item
     int nitems;

@@ -116,71 +116,80 @@ __device__ __forceinline__ void leaf(uint32_t cost, Best &best, uint32_t &rank) 
     ++rank;
 }
 
-template <class C, int L>
+// Ds rows have stride ns. CL (closed tour, NEXT-4): the depot is local
+// index ns - 1; the walk starts there (prev = ns - 1, cost 0) and every
+// leaf adds the return leg to it.
+template <class C, bool CL>
+__device__ __forceinline__ uint32_t ret_leg(const uint32_t *Ds, int ns, int last, uint32_t cost) {
+    if constexpr (CL) return C::add(cost, Ds[last * ns + ns - 1]);
+    return cost;
+}
+
+template <class C, int L, bool CL>
 struct Dfs {
-    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         uint32_t rem = unused;
         while (rem) {
             const int x = __ffs(rem) - 1;
             rem &= rem - 1;
-            Dfs<C, L - 1>::run(Ds, n, unused & ~(1u << x), x, C::add(cost, Ds[prev * n + x]), best, rank);
+            Dfs<C, L - 1, CL>::run(Ds, ns, unused & ~(1u << x), x, C::add(cost, Ds[prev * ns + x]), best, rank);
         }
     }
 };
-template <class C>
-struct Dfs<C, 2> {   // two stops left, a < b: leaves (a, b) then (b, a)
-    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+template <class C, bool CL>
+struct Dfs<C, 2, CL> {   // two stops left, a < b: leaves (a, b) then (b, a)
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
         const int b = __ffs(unused & (unused - 1)) - 1;
-        const uint32_t cab = C::add(C::add(cost, Ds[prev * n + a]), Ds[a * n + b]);
-        const uint32_t cba = C::add(C::add(cost, Ds[prev * n + b]), Ds[b * n + a]);
-        leaf<C>(cab, best, rank);
-        leaf<C>(cba, best, rank);
+        const uint32_t cab = C::add(C::add(cost, Ds[prev * ns + a]), Ds[a * ns + b]);
+        const uint32_t cba = C::add(C::add(cost, Ds[prev * ns + b]), Ds[b * ns + a]);
+        leaf<C>(ret_leg<C, CL>(Ds, ns, b, cab), best, rank);
+        leaf<C>(ret_leg<C, CL>(Ds, ns, a, cba), best, rank);
     }
 };
-template <class C>
-struct Dfs<C, 3> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
-    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+template <class C, bool CL>
+struct Dfs<C, 3, CL> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
         const uint32_t u2 = unused & (unused - 1);
         const int b = __ffs(u2) - 1;
         const int c = __ffs(u2 & (u2 - 1)) - 1;
-        const uint32_t *Dp = Ds + prev * n, *Da = Ds + a * n, *Db = Ds + b * n, *Dc = Ds + c * n;
+        const uint32_t *Dp = Ds + prev * ns, *Da = Ds + a * ns, *Db = Ds + b * ns, *Dc = Ds + c * ns;
         const uint32_t pa = C::add(cost, Dp[a]), pb = C::add(cost, Dp[b]), pc = C::add(cost, Dp[c]);
         const uint32_t ab = C::add(pa, Da[b]), ac = C::add(pa, Da[c]);
         const uint32_t ba = C::add(pb, Db[a]), bc = C::add(pb, Db[c]);
         const uint32_t ca = C::add(pc, Dc[a]), cb = C::add(pc, Dc[b]);
-        leaf<C>(C::add(ab, Db[c]), best, rank);   // a b c
-        leaf<C>(C::add(ac, Dc[b]), best, rank);   // a c b
-        leaf<C>(C::add(ba, Da[c]), best, rank);   // b a c
-        leaf<C>(C::add(bc, Dc[a]), best, rank);   // b c a
-        leaf<C>(C::add(ca, Da[b]), best, rank);   // c a b
-        leaf<C>(C::add(cb, Db[a]), best, rank);   // c b a
+        leaf<C>(ret_leg<C, CL>(Ds, ns, c, C::add(ab, Db[c])), best, rank);   // a b c
+        leaf<C>(ret_leg<C, CL>(Ds, ns, b, C::add(ac, Dc[b])), best, rank);   // a c b
+        leaf<C>(ret_leg<C, CL>(Ds, ns, c, C::add(ba, Da[c])), best, rank);   // b a c
+        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(bc, Dc[a])), best, rank);   // b c a
+        leaf<C>(ret_leg<C, CL>(Ds, ns, b, C::add(ca, Da[b])), best, rank);   // c a b
+        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(cb, Db[a])), best, rank);   // c b a
     }
 };
-template <class C>
-struct Dfs<C, 1> {
-    __device__ __forceinline__ static void run(const uint32_t *Ds, int n, uint32_t unused, int prev, uint32_t cost,
+template <class C, bool CL>
+struct Dfs<C, 1, CL> {
+    __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
-        leaf<C>(C::add(cost, Ds[prev * n + a]), best, rank);
+        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(cost, Ds[prev * ns + a])), best, rank);
     }
 };
 
-template <class C>
-__device__ __forceinline__ void walk_subtree(int L, const uint32_t *Ds, int n, uint32_t unused, int prev,
+template <class C, bool CL>
+__device__ __forceinline__ void walk_subtree(int L, const uint32_t *Ds, int ns, uint32_t unused, int prev,
                                              uint32_t cost, Best &best, uint32_t &rank) {
     switch (L) {
-        case 1: Dfs<C, 1>::run(Ds, n, unused, prev, cost, best, rank); break;
-        case 2: Dfs<C, 2>::run(Ds, n, unused, prev, cost, best, rank); break;
-        case 3: Dfs<C, 3>::run(Ds, n, unused, prev, cost, best, rank); break;
-        case 4: Dfs<C, 4>::run(Ds, n, unused, prev, cost, best, rank); break;
-        case 5: Dfs<C, 5>::run(Ds, n, unused, prev, cost, best, rank); break;
-        case 6: Dfs<C, 6>::run(Ds, n, unused, prev, cost, best, rank); break;
-        default: Dfs<C, 7>::run(Ds, n, unused, prev, cost, best, rank); break;
+        case 1: Dfs<C, 1, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 2: Dfs<C, 2, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 3: Dfs<C, 3, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 4: Dfs<C, 4, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 5: Dfs<C, 5, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 6: Dfs<C, 6, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        default: Dfs<C, 7, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
     }
 }
 
@@ -191,18 +200,21 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
                                                                      const RouteWorkItem *__restrict__ items,
                                                                      int nitems, const uint32_t *__restrict__ Dall,
                                                                      uint64_t *item_best) {
-    __shared__ uint32_t sD[ENUM_WARPS][WR_MAX_EXACT * WR_MAX_EXACT];
+    __shared__ uint32_t sD[ENUM_WARPS][(WR_MAX_EXACT + 1) * (WR_MAX_EXACT + 1)];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int it = blockIdx.x * ENUM_WARPS + warp;
     if (it >= nitems) return;
     const RouteWorkItem item = items[it];
     const RouteProblem pr = probs[item.problem];
     const int n = pr.n;
+    const bool closed = pr.dep >= 0;
+    const int ns = n + (closed ? 1 : 0);   // closed: local index n is the depot
     const uint32_t *D = Dall + (size_t)pr.order * DSTRIDE;
     uint32_t *Ds = sD[warp];
-    for (int e = lane; e < n * n; e += 32) {
-        const int a = e / n, b = e % n;
-        Ds[e] = D[nib(pr.map, a) * MS + nib(pr.map, b)];
+    for (int e = lane; e < ns * ns; e += 32) {
+        const int a = e / ns, b = e % ns;
+        const int ia = a < n ? nib(pr.map, a) : pr.dep, ib = b < n ? nib(pr.map, b) : pr.dep;
+        Ds[e] = D[ia * MS + ib];
     }
     __syncwarp();
     const int p = prefix_depth(n);
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
         // decode prefix q (mixed radix n, n-1, ..., n-p+1), lexicographic
         uint32_t unused = (1u << n) - 1u;
         uint32_t rem = (uint32_t)q, div = div0;
-        int prev = -1;
+        int prev = closed ? n : -1;   // a closed tour leaves the depot first
         uint32_t cost = 0;
         for (int k = 0; k < p; ++k) {
             const uint32_t digit = rem / div;
@@ -224,11 +236,12 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
             for (uint32_t t = 0; t < digit; ++t) m &= m - 1;
             const int x = __ffs(m) - 1;
             unused &= ~(1u << x);
-            if (prev >= 0) cost = C::add(cost, Ds[prev * n + x]);
+            cost = prev >= 0 ? C::add(cost, Ds[prev * ns + x]) : cost;
             prev = x;
         }
         uint32_t rank = (uint32_t)q * sub;
-        walk_subtree<C>(L, Ds, n, unused, prev, cost, best, rank);
+        if (closed) walk_subtree<C, true>(L, Ds, ns, unused, prev, cost, best, rank);
+        else walk_subtree<C, false>(L, Ds, ns, unused, prev, cost, best, rank);
     }
     uint64_t packed = ((uint64_t)best.key << 32) | best.rank;
 #pragma unroll
@@ -325,8 +338,11 @@ __global__ void segment_plan_kernel(const int *xy, int n, int m, int *labels) {
 // --------------------------------------------------- a2 stop projection --
 // Per order: distinct location nodes sorted ascending (P226-238 §2.4);
 // status ETOOLARGE if more than 16 distinct stops. Marks source vertices.
+// depot >= 0 (closed tours, NEXT-4): the depot joins every order's stop set
+// (so it is a BF source and D holds its row and column); dep_info[o] = its
+// index in the sorted stops | 256 if the order itself has a line there.
 __global__ void order_stops_kernel(const int64_t *order_ptr, const int *nodes, int64_t B, int V, int *stops,
-                                   int *n_out, int *status, int *is_src, int *bad) {
+                                   int *n_out, int *status, int *is_src, int *bad, int depot, int *dep_info) {
     const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= B) return;
     int s[MS];
@@ -349,6 +365,26 @@ __global__ void order_stops_kernel(const int64_t *order_ptr, const int *nodes, i
         while (pos > 0 && s[pos - 1] > x) { s[pos] = s[pos - 1]; --pos; }
         s[pos] = x;
         ++n;
+    }
+    if (depot >= 0 && st == WR_OK) {
+        int at = -1;
+        for (int b = 0; b < n; ++b)
+            if (s[b] == depot) at = b;
+        const int genuine = at >= 0;
+        if (!genuine) {
+            if (n == MS) {
+                st = WR_ETOOLARGE;
+            } else {
+                int pos = n;
+                while (pos > 0 && s[pos - 1] > depot) { s[pos] = s[pos - 1]; --pos; }
+                s[pos] = depot;
+                at = pos;
+                ++n;
+            }
+        }
+        dep_info[o] = st == WR_OK ? (at | (genuine << 8)) : -1;
+    } else if (dep_info) {
+        dep_info[o] = -1;
     }
     for (int k = 0; k < MS; ++k) stops[o * MS + k] = k < n ? s[k] : -1;
     n_out[o] = n;
@@ -484,6 +520,9 @@ struct OrderRoute {        // per-order routing state (device)
     int seglen[WR_MAX_SEGMENTS];
     int hk;                // exact route of 13-16 stops by route_hk_kernel (NEXT-2)
     int noenum;            // no enumeration problems (Held-Karp or boundary-pair stitch)
+    int dep;               // closed tour (NEXT-4): order-stop index of the depot; -1 open
+    int ng;                // stops routed (the order's own: n, or n - 1 without a line at the depot)
+    uint64_t gmap;         // nibble list of those ng order-stop indices (ascending)
 };
 
 template <class C>
@@ -494,7 +533,7 @@ template <class C>
 __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
                                      int64_t nord, const uint32_t *Dall, int m, const int *xy,
                                      const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
-                                     int *item_cnt, int pairs, int *hk_count, int *hk_list) {
+                                     int *item_cnt, int pairs, int *hk_count, int *hk_list, const int *dep_info) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nord) return;
     const int64_t o = o_lo + t;
@@ -508,6 +547,17 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
     R.noenum = 0;
     int nitems = 0;
     const int n = R.n;
+    // closed tours (NEXT-4): the depot sits among the n stops of D; the
+    // routed stops are the order's own (the depot only if it has a line there)
+    const int di = dep_info ? dep_info[o] : -1;
+    R.dep = di >= 0 ? (di & 0xff) : -1;
+    const bool dep_routed = di >= 0 && (di >> 8);
+    int gs[MS], ng = 0;
+    for (int i = 0; i < n; ++i)
+        if (R.dep < 0 || i != R.dep || dep_routed) gs[ng++] = i;
+    R.ng = ng;
+    R.gmap = 0;
+    for (int a = 0; a < ng; ++a) R.gmap |= (uint64_t)gs[a] << (4 * a);
     if (R.status == WR_OK) {
         const uint32_t *D = Dall + (size_t)t * DSTRIDE;
         for (int i = 0; i < n && R.status == WR_OK; ++i)
@@ -515,48 +565,48 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 if (i != j && is_inf<C>(D[i * MS + j])) { R.status = WR_EUNREACHABLE; break; }
     }
     if (R.status == WR_OK) {
-        int lab[MS];
-        if (m <= 1 || n <= 1) {
-            for (int i = 0; i < n; ++i) lab[i] = 0;
+        int lab[MS];   // per routed stop (a = 0..ng-1 <-> order stop gs[a])
+        if (m <= 1 || ng <= 1) {
+            for (int a = 0; a < ng; ++a) lab[a] = 0;
         } else if (labels_in) {
-            for (int i = 0; i < n; ++i) lab[i] = labels_in[t * MS + i];
+            for (int a = 0; a < ng; ++a) lab[a] = labels_in[t * MS + gs[a]];
         } else {
             int pxy[2 * MS];
             const int *s = stops + o * MS;
-            for (int i = 0; i < n; ++i) {
-                pxy[2 * i] = xy[2 * s[i]];
-                pxy[2 * i + 1] = xy[2 * s[i] + 1];
+            for (int a = 0; a < ng; ++a) {
+                pxy[2 * a] = xy[2 * s[gs[a]]];
+                pxy[2 * a + 1] = xy[2 * s[gs[a]] + 1];
             }
-            kmeans_dev(pxy, n, m, lab);
+            kmeans_dev(pxy, ng, m, lab);
         }
         // relabel by first appearance (O7 step 1)
         int map_lab[MS], nseg = 0, seg_of[MS];
-        for (int i = 0; i < n; ++i) {
+        for (int a = 0; a < ng; ++a) {
             int id = -1;
             for (int k = 0; k < nseg; ++k)
-                if (map_lab[k] == lab[i]) id = k;
+                if (map_lab[k] == lab[a]) id = k;
             if (id < 0) {
                 if (nseg == WR_MAX_SEGMENTS) { R.status = WR_ETOOLARGE; break; }
-                map_lab[nseg] = lab[i];
+                map_lab[nseg] = lab[a];
                 id = nseg++;
             }
-            seg_of[i] = id;
+            seg_of[a] = id;
         }
         if (R.status == WR_OK) {
             R.mseg = nseg > 0 ? nseg : 1;
             for (int k = 0; k < WR_MAX_SEGMENTS; ++k) { R.seglen[k] = 0; R.segmap[k] = 0; }
-            for (int i = 0; i < n; ++i) {
-                const int k = seg_of[i];
-                R.segmap[k] |= (uint64_t)i << (4 * R.seglen[k]);
+            for (int a = 0; a < ng; ++a) {
+                const int k = seg_of[a];
+                R.segmap[k] |= (uint64_t)gs[a] << (4 * R.seglen[k]);
                 R.seglen[k]++;
             }
-            if (nseg == 1 && n > WR_MAX_EXACT) {
+            if (nseg == 1 && ng > WR_MAX_EXACT) {
                 // exact route of 13-16 stops: Held-Karp subset DP (NEXT-2)
                 R.hk = 1;
                 R.noenum = 1;
                 nseg = 0;
-                hk_list[atomicAdd(hk_count, 1)] = (int)t;   // [0] count, [2] max n
-                atomicMax(hk_count + 2, n);
+                hk_list[atomicAdd(hk_count, 1)] = (int)t;   // [0] count, [2] max routed stops
+                atomicMax(hk_count + 2, ng);
             }
             if (pairs && nseg >= 2) {
                 // boundary-pair stitch (NEXT-1): per-segment orders and the
@@ -609,6 +659,7 @@ __global__ void route_emit_kernel(int64_t nord, OrderRoute *ordr, const int *pro
         RouteProblem P;
         P.order = (int)t;
         P.n = nj;
+        P.dep = R.mseg == 1 ? R.dep : -1;   // segments of a stitched tour stay open (reading R4)
         P.map = R.segmap[k];
         P.item0 = ii;
         P.nitems = (npre + per - 1) / per;
@@ -635,7 +686,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     const int64_t t = (int64_t)blockIdx.x * 4 + warp;
     if (t >= nord) return;
     const OrderRoute R = ordr[t];
-    const int n = R.n;
+    const int n = R.ng;   // stops routed (closed tours: without a depot that has no line)
     const int *s = stops + (o_lo + t) * MS;
     wr_route_result res;
     res.n = n;
@@ -650,6 +701,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     }
     if (pairs && R.mseg >= 2) return;   // route_pairs_kernel writes these orders
     if (R.hk) return;                   // route_hk_kernel writes these orders
+    const int dep = R.dep;              // closed tour (NEXT-4): the depot's stop index, else -1
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     uint32_t *Ds = sD[warp];
     for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
@@ -677,7 +729,9 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     if (R.mseg == 1) {
         final_seq = segseq[0];
         if (n >= 2) {
-            final_cost = C::unkey((uint32_t)(prob_best[R.prob0] >> 32));
+            final_cost = C::unkey((uint32_t)(prob_best[R.prob0] >> 32));   // the closed cost for closed problems
+        } else if (dep >= 0) {   // one stop: out and back
+            final_cost = C::add(Ds[dep * MS + nib(final_seq, 0)], Ds[nib(final_seq, 0) * MS + dep]);
         } else {
             final_cost = 0u;
         }
@@ -701,8 +755,12 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
                     ++pos;
                 }
             }
-            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
+            // full left-to-right recompute; a closed tour starts with the
+            // depot leg and ends with the return leg (reading R4)
+            uint32_t cost = dep >= 0 ? C::add(Ds[dep * MS + nib(seq, 0)], Ds[nib(seq, 0) * MS + nib(seq, 1)])
+                                     : Ds[nib(seq, 0) * MS + nib(seq, 1)];
             for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
+            if (dep >= 0) cost = C::add(cost, Ds[nib(seq, n - 1) * MS + dep]);
             const uint32_t key = C::key(cost);
             // lexicographic key: first stop in the most significant nibble
             uint64_t lex = 0;
@@ -735,7 +793,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
             rank += smaller * fact(n - 1 - a);
         }
         res.rank = rank;
-        res.cost_bits = n >= 2 ? final_cost : 0u;
+        res.cost_bits = (n >= 2 || dep >= 0) ? final_cost : 0u;
         for (int a = 0; a < n; ++a) res.seq[a] = s[nib(final_seq, a)];
         out[t] = res;
         atomicAdd(&counters[0], perms);
@@ -762,7 +820,8 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
     if (t >= nord) return;
     const OrderRoute R = ordr[t];
     if (R.status != WR_OK || R.mseg < 2) return;   // route_finalize_kernel writes these
-    const int n = R.n;
+    const int n = R.ng;     // stops routed
+    const int dep = R.dep;  // closed tour (NEXT-4): the depot's stop index, else -1
     const int *s = stops + (o_lo + t) * MS;
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     for (int e = tid; e < DSTRIDE; e += PAIRS_THREADS) Ds[e] = D[e];
@@ -871,8 +930,12 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
                 pos += nj;
                 seq |= tab[j][a][b] << (4 * (n - pos));
             }
-            uint32_t cost = Ds[nib(seq, 0) * MS + nib(seq, 1)];
+            // full left-to-right recompute; a closed tour starts with the
+            // depot leg and ends with the return leg (reading R4)
+            uint32_t cost = dep >= 0 ? C::add(Ds[dep * MS + nib(seq, 0)], Ds[nib(seq, 0) * MS + nib(seq, 1)])
+                                     : Ds[nib(seq, 0) * MS + nib(seq, 1)];
             for (int a = 2; a < n; ++a) cost = C::add(cost, Ds[nib(seq, a - 1) * MS + nib(seq, a)]);
+            if (dep >= 0) cost = C::add(cost, Ds[nib(seq, n - 1) * MS + dep]);
             const uint32_t key = C::key(cost);
             uint64_t lex = 0;
             for (int a = 0; a < n; ++a) lex |= (uint64_t)nib(seq, a) << (4 * (15 - a));
@@ -1023,6 +1086,7 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
     const int tid = threadIdx.x;
     const int gtid = (int)crank * HK_THREADS + tid, gstride = HK_CL * HK_THREADS;
     __shared__ uint32_t Ds[DSTRIDE];
+    __shared__ uint32_t Din[MS], Dout[MS];   // closed tour (NEXT-4): the depot legs
     __shared__ int s_i;
     uint32_t *W = ws + (size_t)(blockIdx.x / HK_CL) * ws_stride;
     for (;;) {
@@ -1033,12 +1097,22 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
         if (i >= nhk) break;
         const int t = hk_list[i];
         const OrderRoute R = ordr[t];
-        const int n = R.n;
+        const int n = R.ng;   // stops routed; local stop a is order stop nib(R.gmap, a)
+        const bool closed = R.dep >= 0;
         const uint32_t *D = Dall + (size_t)t * DSTRIDE;
-        for (int e = tid; e < DSTRIDE; e += HK_THREADS) Ds[e] = D[e];
+        for (int e = tid; e < DSTRIDE; e += HK_THREADS) {
+            const int a = e / MS, b = e % MS;
+            Ds[e] = (a < n && b < n) ? D[nib(R.gmap, a) * MS + nib(R.gmap, b)] : 0u;
+        }
+        if (closed && tid < n) {
+            Din[tid] = D[R.dep * MS + nib(R.gmap, tid)];
+            Dout[tid] = D[nib(R.gmap, tid) * MS + R.dep];
+        }
         const uint16_t *sets = L.sets;
         const int *off = L.off[n - HK_MIN];
-        if (gtid < n) __stcg(W + (size_t)(1u << gtid) * HK_RS + gtid, 0u);   // F({j}, j) = 0
+        __syncthreads();
+        // F({j}, j) = 0, or the depot leg of a closed tour
+        if (gtid < n) __stcg(W + (size_t)(1u << gtid) * HK_RS + gtid, closed ? Din[gtid] : 0u);
         __syncthreads();
         cl.sync();
         // 1. forward layers |S| = 2..n
@@ -1064,10 +1138,13 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
             }
             cl.sync();
         }
-        // C* = min over the last stop of F(all, j)
+        // C* = min over the last stop of F(all, j) (+ the return leg)
         const uint32_t F = (1u << n) - 1u;
         uint32_t ck = 0xffffffffu;
-        for (int j = 0; j < n; ++j) ck = min(ck, C::key(__ldcg(W + (size_t)F * HK_RS + j)));
+        for (int j = 0; j < n; ++j) {
+            const uint32_t f = __ldcg(W + (size_t)F * HK_RS + j);
+            ck = min(ck, C::key(closed ? H::fwd(f, Dout[j]) : f));
+        }
         const uint32_t cstar = C::unkey(ck);
         cl.sync();   // every CTA has C* before M(all, .) overwrites F(all, .)
         wr_route_result res;
@@ -1079,14 +1156,15 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
                 res.m_used = 1;
                 res.cost_bits = C::INF;
                 res.rank = 0;
-                for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[a] : -1;
+                for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[nib(R.gmap, a)] : -1;
                 out[t] = res;
             }
             cl.sync();
             continue;
         }
-        // 2. backward bound, layers |S| = n .. 1
-        if (gtid < n) __stcg(W + (size_t)F * HK_RS + gtid, cstar);
+        // 2. backward bound, layers |S| = n .. 1 (closed: the largest prefix
+        //    whose return leg still ends <= C*)
+        if (gtid < n) __stcg(W + (size_t)F * HK_RS + gtid, closed ? H::inv(Dout[gtid], cstar) : cstar);
         cl.sync();
         for (int k = n - 1; k >= 1; --k) {
             const int base = off[k], items = (off[k + 1] - base) * k;
@@ -1117,8 +1195,9 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
                     if ((S >> q) & 1u) continue;
                     const uint32_t m = __ldcg(W + (size_t)(S | (1u << q)) * HK_RS + q);
                     uint32_t nx = 0;
-                    if (a == 0) {
-                        if (m != H::NONE && !H::gt(0u, m)) { pick = q; nx = 0u; }
+                    if (a == 0) {   // the first stop's prefix: 0, or the depot leg
+                        const uint32_t c0 = closed ? Din[q] : 0u;
+                        if (m != H::NONE && !H::gt(c0, m)) { pick = q; nx = c0; }
                     } else if (H::step(c, Ds[j * MS + q], m, nx)) {
                         pick = q;
                     }
@@ -1131,6 +1210,7 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
                 j = pick;
                 c = cn;
             }
+            if (ok && closed) c = H::fwd(c, Dout[j]);   // the return leg
             const int *s = stops + (o_lo + t) * MS;
             res.n = n;
             res.status = ok ? WR_OK : WR_EINTERNAL;
@@ -1143,7 +1223,7 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
                 rank += smaller * fact(n - 1 - a);
             }
             res.rank = rank;
-            for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[seq[a]] : -1;
+            for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[nib(R.gmap, seq[a])] : -1;
             out[t] = res;
             // work: forward transitions n (n-1) 2^(n-2), as many in the bound pass
             atomicAdd(&counters[0], 2ull * (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
@@ -1225,6 +1305,8 @@ struct Plan {               // wr_plan
     DBuf<int64_t> blk;      // world+1 source block boundaries
     DBuf<int64_t> off_all;  // world x (B+1)
     DBuf<int> labels;       // optional [B][16] labels override
+    DBuf<int> dep_info;     // closed tours: [B] depot stop index | 256 if a genuine stop; -1 open
+    int closed = 0;
     std::vector<int64_t> h_blk;
     int64_t launches = 0;
 };
@@ -1259,6 +1341,8 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     P->m = (line_labels && o.m < 2) ? 2 : o.m;   // caller labels always go through the stitch
     P->pairs = (o.flags & WR_ROUTE_PAIRS) ? 1 : 0;
     P->chunk = o.chunk > 0 ? o.chunk : WR_DEFAULT_CHUNK;
+    P->closed = (o.flags & WR_ROUTE_CLOSED) ? 1 : 0;
+    if (P->closed && (o.depot < 0 || o.depot >= g->V)) return fail(WR_EINVAL, "wr_orders_plan: depot outside [0, V)");
     if (P->m >= 2 && !labels16 && !g->xy.p)
         return fail(WR_EINVAL, "wr_orders_plan: segmented routing without labels needs graph xy (O8)");
     const int V = g->V;
@@ -1279,9 +1363,11 @@ static wr_status plan_impl(const wr_graph *g, const int64_t *order_ptr, const in
     DBuf<int> bad(1);
     WR_CUDA(cudaMemsetAsync(P->is_src.p, 0, 4LL * V, st));
     WR_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+    if (P->closed) P->dep_info.alloc(std::max<int64_t>(B, 1));
     if (B > 0) {
         order_stops_kernel<<<gridn(B, 256), 256, 0, st>>>(d_ptr.p, d_nodes.p, B, V, P->stops.p, P->n_arr.p,
-                                                         P->status.p, P->is_src.p, bad.p);
+                                                         P->status.p, P->is_src.p, bad.p,
+                                                         P->closed ? o.depot : -1, P->dep_info.p);
         count_launch();
         WR_LAUNCH_CHECK();
     }
@@ -1669,7 +1755,7 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
         P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
         P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs,
-        hk_ctr.p, hk_list.p);
+        hk_ctr.p, hk_list.p, P.closed ? P.dep_info.p : nullptr);
     count_launch();
     WR_LAUNCH_CHECK();
     scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
@@ -1961,6 +2047,7 @@ wr_status wr_route_segmented(const wr_graph *g, const int32_t *stops, int32_t n,
         o.m = m;
         if (labels && m < 2) o.m = 2;   // caller labels always go through the stitch
         o.ctx = nullptr;
+        o.flags &= ~WR_ROUTE_CLOSED;   // one stop set, open route (closed tours: wr_route_orders)
         return wr::route_orders_impl(g, ptr, hs.data(), 1, &o, labels ? lab16.data() : nullptr, nullptr, out, nullptr);
     });
 }
