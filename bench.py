@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--wtype", default="i32", choices=["i32", "f32"])
     ap.add_argument("--m", type=int, default=1, help="segments (1 = exact routes)")
     ap.add_argument("--pairs", action="store_true", help="segmented routes with the boundary-pair stitch (NEXT-1)")
+    ap.add_argument("--nearfar", action="store_true", help="near-far deferral in the fp32 sweep (NEXT-3)")
+    ap.add_argument("--depot", type=int, default=None, help="closed tours through this node (NEXT-4)")
     ap.add_argument("--no-pred", action="store_true", help="skip a4 (diagnostics only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -205,7 +207,7 @@ def main():
     d_nodes = torch.from_numpy(orders.order_nodes).to(dev)
     stream = torch.cuda.current_stream()
 
-    rflags = wr.WR_ROUTE_PAIRS if a.pairs else 0
+    rflags = (wr.WR_ROUTE_PAIRS if a.pairs else 0) | (wr.WR_ROUTE_NEARFAR if a.nearfar else 0)
     # N > 1: libwr's own context (NCCL communicator bootstrapped over the
     # process group): wr_route_orders shards sources and orders and runs the
     # all-gather of the owned D entries inside the call; each rank keeps its
@@ -229,7 +231,7 @@ def main():
 
     def step():
         _, st = wr.route_orders(G, d_ptr, d_nodes, m=a.m, results=d_res, stream=stream, pred_out=pred_buf,
-                                flags=rflags, ctx=ctx)
+                                flags=rflags, ctx=ctx, depot=a.depot)
         launches[0] += st.kernel_launches
         bf_ms[0] += st.bf_ms
         relax[0] += st.relaxations
@@ -274,7 +276,7 @@ def main():
 
         def e2e_step():
             wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream, flags=rflags,
-                            pred_out=pred_buf, ctx=ctx)
+                            pred_out=pred_buf, ctx=ctx, depot=a.depot)
 
         for _ in range(2):
             e2e_step()
@@ -325,7 +327,8 @@ def main():
     # DRAM bytes per launch from the committed ncu capture; that capture ran
     # the default workload (config 5, int32 weights, exact routes, fused pred),
     # so any other configuration reports null rather than someone else's bytes
-    captured = a.config == 5 and a.wtype == "i32" and a.m == 1 and not a.pairs and not a.no_pred
+    captured = (a.config == 5 and a.wtype == "i32" and a.m == 1 and not a.pairs and not a.no_pred
+                and a.depot is None and not a.nearfar)
     if captured and os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("bf_frontier_kernel", {}).get("dram_bytes")
     # ALU view: one DPX add+min (VIADDMNMX, ALU pipe: 64 lanes/clk/SM) per
@@ -340,6 +343,8 @@ def main():
         "config": {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]", "orders": B,
                    "sources": S, "V": g.V, "E": E, "m": a.m, "pred": not a.no_pred,
                    "stitch": "boundary pairs (NEXT-1)" if a.pairs else ("paper O7" if a.m >= 2 else "exact"),
+                   "tour": "open" if a.depot is None else f"closed through node {a.depot} (NEXT-4)",
+                   "sweep": "near-far (NEXT-3)" if a.nearfar else "frontier",
                    "bf_rows": ("packed u16x2, exact (15-bit bound checked per tile, else a 32-bit redo); "
                                "outputs int32") if rb == 16 else "32-bit",
                    "l2": ("working set (dist rows 4*V*S = %.1f GB) >> 126 MB L2; no flush needed" % (4 * g.V * S / 1e9))

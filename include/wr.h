@@ -146,6 +146,14 @@ wr_status wr_graph_info(const wr_graph *g, wr_graph_info_t *info);
 #define WR_BF_AUTO 0
 #define WR_BF_FRONTIER 1   /* frontier-pull sweep over tiles of 32 sources   */
 #define WR_BF_DENSE 2      /* every vertex every round (edge-parallel class) */
+#define WR_BF_NEARFAR 3    /* NEXT-3 near-far deferral (fp32 graphs; int graphs
+                              run WR_BF_FRONTIER): an improved vertex whose new
+                              distances all exceed the tile's threshold T keeps
+                              its row but propagates only once T reaches it; T
+                              grows by delta = WR_NF_DELTA (default 0.75) x the
+                              largest weight per round. Same results (O2
+                              fixpoint); fewer relaxations, more rounds
+                              (DESIGN §9 has the measured trade-off)        */
 
 typedef struct {
     void *stream;            /* cudaStream_t; NULL = default stream          */
@@ -258,6 +266,8 @@ typedef struct {
  * The depot becomes a BF source; a closed order may hold at most 15 stops
  * other than the depot (WR_ETOOLARGE). Results list the order's own stops. */
 #define WR_ROUTE_CLOSED 8
+/* wr_route_opts.flags: run the routing path's sweep with WR_BF_NEARFAR. */
+#define WR_ROUTE_NEARFAR 16
 
 typedef struct {
     int32_t n;               /* stops (distinct nodes, ascending before routing) */

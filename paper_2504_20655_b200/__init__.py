@@ -21,11 +21,12 @@ WR_OK, WR_EINVAL, WR_ENOMEM, WR_ENEGCYCLE, WR_EOVERFLOW, WR_EUNREACHABLE, WR_ETO
     WR_ENCCL, WR_EINTERNAL = range(10)
 WR_I32, WR_F32 = 0, 1
 WR_COO, WR_CSR = 0, 1
-WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE = 0, 1, 2
+WR_BF_AUTO, WR_BF_FRONTIER, WR_BF_DENSE, WR_BF_NEARFAR = 0, 1, 2, 3
 WR_ROUTE_ROWS32 = 1
 WR_ROUTE_PAIRS = 2
 WR_ROUTE_RANK_RESULTS = 4
 WR_ROUTE_CLOSED = 8
+WR_ROUTE_NEARFAR = 16
 NCCL_UID_BYTES = 128
 MAX_STOPS = 16
 DEFAULT_CHUNK = 2903040

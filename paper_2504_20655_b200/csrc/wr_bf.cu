@@ -336,11 +336,30 @@ constexpr int QCAP = WR_QCAP;
 #endif
 constexpr int FPA = WR_FUSED_PA;   // in-arcs per vertex per step in the fused pred jobs (1: 65.0 ms, 2: 64.0, 3: 65.6)
 
-template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST>
+// Near-far state of one CTA (NF kernels only): the deferred bitmap and the
+// inlist bitmaps live in shared memory, keys and word lists in global.
+struct NfState {
+    uint32_t *pend;      // [NW] deferred vertices
+    uint32_t *inl;       // [2][NWB] words already in list 0 / 1
+    uint32_t *keys;      // [V] min deferred key (fp32 bits)
+    int *plist;          // [2][NW] words with deferred vertices
+    int *plen;           // [2] (shared)
+    int cur;             // list being filled this round
+    float T;             // threshold
+};
+
+__device__ __forceinline__ void nf_append(NfState &nf, int which, int w, int NW) {
+    const uint32_t b = 1u << (w & 31);
+    if (!(atomicOr(&nf.inl[which * ((NW + 31) >> 5) + (w >> 5)], b) & b))
+        nf.plist[which * NW + atomicAdd(&nf.plen[which], 1)] = w;
+}
+
+template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST, bool NF = false>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const ChgView pchg,
                                                uint32_t *nxt, int *nlist, int *nlen, int2 *q,
-                                               uint32_t *touched, bool &ovf, uint32_t thr2) {
+                                               uint32_t *touched, bool &ovf, uint32_t thr2,
+                                               NfState *nfp = nullptr) {
     constexpr int TSW = 32 * SPL;
     const int v = (w << 5) + lane;
     const bool act = (m >> lane) & 1u;
@@ -381,7 +400,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
     for (int j = 0; j < SPL; ++j) infv.x[j] = Op::INF;
     const uint32_t slow = __ballot_sync(FULL, c > QC);
     uint32_t *Rl = R + lane * SPL;
-    uint32_t chg = 0;
+    uint32_t chg = 0, wrote = 0;
     unsigned long long dummy = 0;
     // ---- B: relax the queued vertices, VB per step, TPS tasks each per
     // step (VB*TPS row gathers in flight)
@@ -476,7 +495,33 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
             // first write of a row covers every slot (untouched slots stay INF)
             const bool f = ok[k] && !((tw >> iv[k]) & 1u);
             const bool lt = ok[k] && diff != 0u;                   // the row improved (store it)
-            const bool ch = Op::KEYED ? ok[k] && ddiff != 0u : lt;  // a distance improved (propagate)
+            bool ch = Op::KEYED ? ok[k] && ddiff != 0u : lt;        // a distance improved (propagate)
+            if (__any_sync(FULL, lt)) wrote |= 1u << iv[k];
+            if constexpr (NF) {
+                // near-far: defer the propagation while every improved slot
+                // is beyond T (the row is stored either way)
+                if (__any_sync(FULL, ch)) {
+                    uint32_t km = 0xffffffffu;   // fp32 >= 0: bit order = value order
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j)
+                        if (nv.x[j] != e[k].x[j]) km = min(km, nv.x[j]);
+                    km = __reduce_min_sync(FULL, km);
+                    NfState &nf = *nfp;
+                    const uint32_t bit = 1u << iv[k];
+                    const int vv = (w << 5) + iv[k];
+                    if (__uint_as_float(km) > nf.T) {
+                        ch = false;
+                        if (lane == 0) {   // this warp owns word w this round
+                            const uint32_t old = nf.pend[w];
+                            nf.keys[vv] = (old & bit) ? min(nf.keys[vv], km) : km;
+                            nf.pend[w] = old | bit;
+                            if (!old) nf_append(nf, nf.cur, w, (g.V + 31) >> 5);
+                        }
+                    } else if (lane == 0 && (nf.pend[w] & bit)) {
+                        nf.pend[w] &= ~bit;   // propagated now, with everything deferred before
+                    }
+                }
+            }
             if (lt || f) {
                 vstore<SPL>(Rl + (size_t)((w << 5) + iv[k]) * TSW, nv);
                 // keyed rows are range-checked by the pred jobs instead (every key is decoded there)
@@ -488,7 +533,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
             if (__any_sync(FULL, ch)) chg |= 1u << iv[k];
         }
     }
-    if (DELTA && lane == 0 && (chg & ~tw)) touched[w] = tw | chg;   // this warp owns word w
+    if (DELTA && lane == 0 && (wrote & ~tw)) touched[w] = tw | wrote;   // this warp owns word w
     // ---- C: improved vertices mark their out-neighbours, lane-parallel
     if (DELTA && ((chg >> lane) & 1u)) {
         for (int e = o0; e < o1; ++e) {
@@ -551,19 +596,21 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
                                                int *overflow);
 
 
-template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST, bool NF = false>
 __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const int *__restrict__ tile_src,
                                                                int ntiles, uint32_t *__restrict__ rows,
                                                                int *tile_counter, int max_rounds,
                                                                BfTileStats *stats, uint32_t thr2,
                                                                const int *__restrict__ tile_order, PredFuse fuse,
-                                                               const int *__restrict__ slot_row) {
+                                                               const int *__restrict__ slot_row, NearFar nfa) {
     constexpr int TSW = 32 * SPL;              // 32-bit words per row
     constexpr int TS = TSW * Op::PACK;         // sources per tile
     constexpr int NWARPS = NT / 32;
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ int s_tile;
     __shared__ int s_len[3], s_head[3];
+    __shared__ int s_plen[2], s_phead;
+    __shared__ uint32_t s_kmin;
     const int V = g.V;
     const int NW = (V + 31) >> 5;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -573,6 +620,15 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
     uint2 *const chg = reinterpret_cast<uint2 *>(smem + L.chg);
     int *const list = reinterpret_cast<int *>(smem + L.list);
     int2 *const q = reinterpret_cast<int2 *>(smem + L.queue) + warp * (32 * QC);
+    const int NWB = (NW + 31) >> 5;
+    NfState nf{};
+    if constexpr (NF) {   // after the queues: pend[NW], inl[2][NWB]
+        nf.pend = smem + L.words;
+        nf.inl = nf.pend + NW;
+        nf.keys = nfa.keys + (size_t)blockIdx.x * V;
+        nf.plist = nfa.plist + (size_t)blockIdx.x * 2 * NW;
+        nf.plen = s_plen;
+    }
 
     for (;;) {
         if (threadIdx.x == 0) {
@@ -599,6 +655,12 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         }
         for (size_t i = threadIdx.x; i < L.list; i += NT) smem[i] = 0u;
         if (threadIdx.x < 3) s_len[threadIdx.x] = s_head[threadIdx.x] = 0;
+        if constexpr (NF) {
+            for (int i = threadIdx.x; i < NW + 2 * NWB; i += NT) nf.pend[i] = 0u;
+            if (threadIdx.x < 2) s_plen[threadIdx.x] = 0;
+            nf.cur = 0;
+            nf.T = nfa.delta;
+        }
         __syncthreads();
         if (warp == 0) {   // seed: d[s][slot] = 0; the sources "changed" in round 0
             if (!DENSE) {  // the seed vertices' rows: INF everywhere first
@@ -653,9 +715,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     if (!m) continue;
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, false>(g, R, w, m, lane, relax, pc, nxt,
-                                                                                     nullptr, nullptr, q, touched, ovf,
-                                                                                     thr2);
+                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, false, NF>(
+                        g, R, w, m, lane, relax, pc, nxt, nullptr, nullptr, q, touched, ovf, thr2, &nf);
                     if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
@@ -679,14 +740,79 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     const uint32_t m = cur[w];
                     __syncwarp();
                     if (lane == 0) cur[w] = 0u;
-                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, true>(g, R, w, m, lane, relax, pc, nxt,
-                                                                                    ln, nlen, q, touched, ovf, thr2);
+                    const uint32_t c = relax_word<Op, true, SPL, QC, VB, TPS, true, NF>(
+                        g, R, w, m, lane, relax, pc, nxt, ln, nlen, q, touched, ovf, thr2, &nf);
                     if (lane == 0 && c) cc[w] = make_uint2(c, (uint32_t)r);
                     visits += (unsigned long long)__popc(m);
                     any |= c != 0;
                 }
             }
+            bool nf_released = false;
+            if constexpr (NF) {
+                uint2 *cc = chg + (r & 1) * NW;
+                int *ln = LIST ? list + ((r + 1) & 1) * NW : nullptr;
+                int *const nlen = LIST ? &s_len[(r + 1) % 3] : nullptr;
+                // near-far release: deferred vertices whose key is <= T
+                    // now propagate as if they had changed in round r (change
+                    // bits stamped r, out-neighbours into round r+1's list);
+                    // when nothing is near, T jumps to the nearest deferred key
+                    const bool near0 = __syncthreads_or(any) != 0;   // this round propagated something
+                    bool released = false;
+                    for (;;) {
+                        const int src = nf.cur, dst = nf.cur ^ 1;
+                        if (threadIdx.x == 0) { s_plen[dst] = 0; s_phead = 0; s_kmin = 0xffffffffu; }
+                        for (int i = threadIdx.x; i < NWB; i += NT) nf.inl[dst * NWB + i] = 0u;
+                        __syncthreads();
+                        const int plen = s_plen[src];
+                        for (;;) {
+                            int i = 0;
+                            if (lane == 0) i = atomicAdd(&s_phead, 1);
+                            i = __shfl_sync(FULL, i, 0);
+                            if (i >= plen) break;
+                            const int w = nf.plist[src * NW + i];
+                            const uint32_t bits = nf.pend[w];
+                            const int v = (w << 5) + lane;
+                            uint32_t key = 0xffffffffu;
+                            if ((bits >> lane) & 1u) key = nf.keys[v];
+                            const bool rel = ((bits >> lane) & 1u) && __uint_as_float(key) <= nf.T;
+                            const uint32_t relm = __ballot_sync(FULL, rel), keep = bits & ~relm;
+                            if (rel) {   // mark the out-neighbours for round r+1
+                                for (int e2 = g.out_ptr[v]; e2 < g.out_ptr[v + 1]; ++e2) {
+                                    const int x = g.out_dst[e2];
+                                    if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u && LIST) ln[atomicAdd(nlen, 1)] = x >> 5;
+                                }
+                            }
+                            const uint32_t kk = __reduce_min_sync(FULL, ((keep >> lane) & 1u) ? key : 0xffffffffu);
+                            if (lane == 0) {
+                                if (relm) {
+                                    const uint2 e0 = cc[w];
+                                    cc[w] = e0.y == (uint32_t)r ? make_uint2(e0.x | relm, (uint32_t)r)
+                                                                : make_uint2(relm, (uint32_t)r);
+                                }
+                                nf.pend[w] = keep;
+                                if (keep) {
+                                    nf_append(nf, dst, w, NW);
+                                    atomicMin(&s_kmin, kk);
+                                }
+                            }
+                            released |= relm != 0u;
+                        }
+                        __syncthreads();
+                        nf.cur = dst;
+                        // T advances by delta per round; with nothing near it
+                        // jumps to the nearest deferred key and releases again
+                        released = __syncthreads_or(released) != 0;
+                        const bool near = near0 || released, pending = s_plen[dst] > 0;
+                        if (near || !pending) {
+                            nf.T += nfa.delta;
+                            nf_released = released;
+                            break;
+                        }
+                        nf.T = fmaxf(nf.T + nfa.delta, __uint_as_float(s_kmin));
+                    }
+                }
             ++rounds;
+            any |= nf_released;
             more = __syncthreads_or(any) != 0;
             uint32_t *t = cur;
             cur = nxt;
@@ -772,11 +898,13 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
 
 // Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
 // WR_BF_CONFIG selects one (tuning knob; default measured best).
-template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool LIST = false, int VB = 2, int TPS = 2>
+template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool LIST = false, int VB = 2, int TPS = 2,
+          bool NF = false>
 static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
-    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, QC, VB, TPS, LIST && !DENSE>;
+    auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, QC, VB, TPS, LIST && !DENSE, NF>;
     const int NW = (g->V + 31) / 32;
     size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
+    if (NF) smem += (size_t)(NW + 2 * ((NW + 31) / 32)) * sizeof(uint32_t);   // deferred bitmap + inlist bitmaps
     if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
         smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV * (32 * SPL * Op::PACK + 1) * sizeof(int32_t));
     int max_optin = 0;
@@ -790,8 +918,18 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     const int grid = (int)std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
     DBuf<int> counter(1);
     WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+    NearFar nfa;
+    DBuf<uint32_t> nf_keys;
+    DBuf<int> nf_plist;
+    if (NF) {   // per persistent CTA: keys[V], two word lists
+        nf_keys.alloc((size_t)grid * g->V);
+        nf_plist.alloc((size_t)grid * 2 * NW);
+        nfa.keys = nf_keys.p;
+        nfa.plist = nf_plist.p;
+        nfa.delta = run.nf_delta;
+    }
     kern<<<grid, NT, smem, st>>>(g->view(), run.tile_src, run.ntiles, run.rows, counter.p, run.max_rounds, d_stats,
-                                 run.ovf_thr * 0x10001u, run.tile_order, run.fuse, run.slot_row);
+                                 run.ovf_thr * 0x10001u, run.tile_order, run.fuse, run.slot_row, nfa);
     count_launch();
     WR_LAUNCH_CHECK();
     return true;   // the counter goes back to the stream-ordered pool: no sync needed
@@ -819,6 +957,13 @@ static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_
     // 768 x 2x2 63.4 - more gathers per warp do not pay at 96 registers)
     static const int cfg = env_int("WR_BF_CONFIG", std::is_same<Op, OpF32>::value ? 8 : 11);
     bool ok = false;
+    if constexpr (std::is_same<Op, OpF32>::value && !DENSE) {   // near-far deferral (NEXT-3)
+        if (run.nf_delta > 0.f) {
+            static const int nfcfg = env_int("WR_NF_CONFIG", 8);
+            if (nfcfg == 8 && launch_shape<Op, DENSE, 768, 1, SPL, QCAP, false, 2, 2, true>(g, run, d_stats, st)) return;
+            if (launch_shape<Op, DENSE, 640, 1, SPL, QCAP, true, 2, 2, true>(g, run, d_stats, st)) return;
+        }
+    }
     switch (cfg) {
         case 8: ok = launch_shape<Op, DENSE, 768, 1, SPL>(g, run, d_stats, st); break;
         case 11: ok = launch_shape<Op, DENSE, 640, 1, SPL, QCAP, true>(g, run, d_stats, st); break;
@@ -1009,6 +1154,16 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
             // enough for a diagnostic (freed at process exit)
         }, tj));
     }
+}
+
+// C5 fp32 (bench, static 768 shape): delta 0.35 / 0.5 / 0.75 / 1.0 x max w:
+// relaxations 2.35 / 2.32 / 2.79 / 3.25 x S*E (off: 3.25), step 299 / 247 /
+// 223 / 231 ms (off: 216): the deferral saves work but adds rounds.
+float nf_delta_for(const wr_graph *g) {
+    if (g->wtype != WR_F32 || !(g->max_w_f > 0.f)) return 0.f;
+    static const char *e = getenv("WR_NF_DELTA");
+    const float mult = e ? (float)atof(e) : 0.75f;
+    return mult > 0.f ? mult * g->max_w_f : 0.f;
 }
 
 // Sources per lane for S sources; WR_BF_SPL forces a width.
@@ -1664,6 +1819,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
     // V-1 relaxation rounds (P724 §4.7) + the kernel's check round
     const int max_rounds = o.max_rounds > 0 ? o.max_rounds : std::max(1, V - 1);
     const int variant = o.variant == WR_BF_DENSE ? WR_BF_DENSE : WR_BF_FRONTIER;
+    const bool nearfar = o.variant == WR_BF_NEARFAR;
     int nsm = 0;
     WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
     const int spl = choose_spl(S, nsm, 1);
@@ -1724,6 +1880,7 @@ static wr_status bf_batch_impl(const wr_graph *g, const int32_t *sources, int32_
         const int64_t hi = std::min<int64_t>(S, lo + sb);
         const int ntiles = make_tiles_ordered(g, d_src.p, lo, hi, tsw, max_tiles, tile_src.p, slot_row.p, pos_of.p, st);
         BfRun run{tile_src.p, ntiles, rows.p, variant, max_rounds, spl, slot_row.p};
+        run.nf_delta = nearfar ? nf_delta_for(g) : 0.f;
         {
             NvtxRange nv("wr.bf.sweep");
             bf_run(g, run, d_stats.p, st);

@@ -284,6 +284,7 @@ __global__ void validate_kernel(const int *src, const int *dst, uint32_t *w, int
         const float x = __uint_as_float(bits);
         if (!(x >= 0.0f) || isinf(x)) atomicOr(flags, BAD_WEIGHT);  // NaN, -x, inf
         if (bits == 0x80000000u) w[e] = 0u;                            // -0.0 -> +0.0
+        else if (x >= 0.0f && !isinf(x)) atomicMax(max_abs, bits);     // fp32 >= 0: bit order = value order
     } else {
         const int x = (int)bits;
         if (x < 0) atomicOr(has_neg, 1);
@@ -466,7 +467,8 @@ static wr_status graph_load_impl(const wr_graph_desc *d, wr_graph **out) {
     if (hf[0] & BAD_XY) return fail(WR_EINVAL, "wr_graph_load: |xy| >= 2^20");
     g->has_negative = hf[2];
     g->has_zero = hf[3];
-    g->max_abs_w = hf[1];
+    g->max_abs_w = d->wtype == WR_I32 ? hf[1] : 0;
+    if (d->wtype == WR_F32) memcpy(&g->max_w_f, &hf[1], 4);
     g->max_in_deg = (int64_t)hmaxdeg;
     if (d->wtype == WR_I32 && (int64_t)(V - 1) * (int64_t)(uint32_t)hf[1] >= (int64_t)INT32_MAX)
         return fail(WR_EOVERFLOW, "wr_graph_load: (V-1)*max|w| >= INT32_MAX (reading A7)");

@@ -148,6 +148,7 @@ struct wr_graph {
     int has_zero = 0;       // an int32 arc of weight 0
     int32_t max_abs_w = 0;
     int64_t max_in_deg = 0; // largest in-degree (keyed rows need <= 15)
+    float max_w_f = 0.f;    // fp32 graphs: largest weight (near-far threshold step)
     wr::DBuf<int> in_ptr, in_src, out_ptr, out_dst;
     wr::DBuf<uint32_t> in_w;
     wr::DBuf<int2> in_arc;
@@ -175,6 +176,9 @@ int64_t sources_per_segment(int64_t budget, int64_t fixed_bytes, int64_t per_sou
                             int64_t S, int tsw);
 // Sources per lane (1, 2, 4) for S sources on nsm SMs (env WR_BF_SPL forces).
 int choose_spl(int64_t S, int nsm, int pack);
+// Near-far threshold step for an fp32 graph (0 = off): WR_NF_DELTA x the
+// largest weight (default measured).
+float nf_delta_for(const wr_graph *g);
 
 // The canonical-pred pass fused into the sweep: CTAs whose tile claims have
 // run out take pred jobs of finished tiles (in completion order) while the
@@ -186,6 +190,19 @@ struct PredFuse {
     int *done_list = nullptr;       // [ntiles] finished tiles in completion order, -1 = not yet
     int *counters = nullptr;        // [4] zeroed: [0] done slots, [2..3] u64 pred jobs claimed
     long long *trace = nullptr;     // diagnostics (WR_TILE_TRACE): per tile {start, end, rounds, SM}
+};
+
+// NEXT-3 near-far (§1.1 leaves Δ-stepping
+// for future work): a vertex improved to a distance beyond the tile's
+// threshold T (all improved slots > T) keeps its new row but defers its
+// propagation (no change bit, no out-neighbour marks) until T reaches it;
+// T grows by delta per round, and jumps to the nearest deferred key when a
+// round has nothing near. Per persistent CTA: keys[V] (min deferred key),
+// plist[2][ceil(V/32)] (words with deferred vertices, double-buffered).
+struct NearFar {
+    uint32_t *keys = nullptr;   // gridDim.x x V
+    int *plist = nullptr;       // gridDim.x x 2 x NW
+    float delta = 0.f;          // 0 = off
 };
 
 struct BfRun {              // one BF segment over tiles of 32*spl sources
@@ -200,6 +217,7 @@ struct BfRun {              // one BF segment over tiles of 32*spl sources
     const int *tile_order = nullptr;  // [ntiles] claim order of the tiles (null = 0..ntiles-1)
     uint32_t ovf_thr = 0;   // pack 2: a stored distance >= ovf_thr flags a possible u16 overflow
     bool keyed = false;     // pack 2 rows hold (d << 4 | in-arc index of the pred) keys (OpK16)
+    float nf_delta = 0.f;   // > 0: near-far deferral (fp32 rows), NearFar above
     PredFuse fuse;
     int tsw() const { return 32 * spl * pack; }   // sources (slots) per tile
 };

@@ -1583,6 +1583,7 @@ static wr_status local_impl(wr_plan *P, void *send, const wr_route_opts *opts, w
             b.run = BfRun{b.tile_src.p, b.ntiles, b.rows.p, WR_BF_FRONTIER, max_rounds, pt.spl, b.slot_row.p};
             b.run.pack = pk;
             b.run.keyed = pk == 2 && keyed;
+            b.run.nf_delta = (pk == 1 && (o.flags & WR_ROUTE_NEARFAR)) ? nf_delta_for(g) : 0.f;
             b.run.ovf_thr = pk != 2 ? 0u
                             : b.run.keyed ? (0x7ffu - (uint32_t)g->max_abs_w) << 4
                                           : 0x7fffu - (uint32_t)g->max_abs_w;
