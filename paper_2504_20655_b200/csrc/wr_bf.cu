@@ -588,12 +588,20 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
                                          int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
                                          int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane);
 
+// keyed staging rows: slot s at s + s / 32 (a skew that makes both the
+// per-lane writes of 8 consecutive slots and the per-slot reads conflict-free)
+template <int SPL>
+struct KeyedStage {
+    static constexpr int TS = 64 * SPL;
+    static constexpr int RS = TS + TS / 32 + 1;
+    __device__ static int at(int s) { return s + (s >> 5); }
+};
 template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                                int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
-                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane, uint32_t thr,
-                                               int *overflow);
+                                               int32_t *spw, int lane, uint32_t thr, int *overflow,
+                                               int (&srow)[2 * SPL], int &srow_tile);
 
 
 template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC, int VB, int TPS, bool LIST, bool NF = false>
@@ -863,6 +871,11 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         }
         __syncthreads();
     }
+    if (fuse.trace && threadIdx.x == 0) {   // diagnostics: this CTA's sweep end / pred-jobs end
+        long long t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        fuse.trace[4 * (size_t)ntiles + 2 * blockIdx.x] = t_now;
+    }
     if (fuse.pred_out && !DENSE) {
         // no tile left to claim: take pred jobs (tile in completion order k,
         // 8-vertex chunk) - a job waits only for a tile that a running CTA
@@ -871,6 +884,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         int32_t(*spw)[TS + 1] = reinterpret_cast<int32_t(*)[TS + 1]>(smem) + warp * PV;
         const int chunks = (V + PV - 1) / PV;
         const long long njobs = (long long)ntiles * chunks;
+        int srow_cache[2 * SPL], srow_tile = -1;   // keyed jobs: output rows of the current tile's slots
         for (;;) {
             long long j = 0;
             if (lane == 0) j = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(fuse.counters + 2), 1ull);
@@ -888,11 +902,18 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             t = __shfl_sync(FULL, t, 0);
             if constexpr (Op::KEYED)
                 pred_job_keyed<SPL>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, t,
-                                    (int)(j % chunks) * PV, spw, lane, thr2 & 0xffffu, &stats->overflow);
+                                    (int)(j % chunks) * PV,
+                                    reinterpret_cast<int32_t *>(smem) + warp * PV * KeyedStage<SPL>::RS, lane,
+                                    thr2 & 0xffffu, &stats->overflow, srow_cache, srow_tile);
             else
                 pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
                                        (int)(j % chunks) * PV, spw, lane);
         }
+    }
+    if (fuse.trace && threadIdx.x == 0) {
+        long long t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        fuse.trace[4 * (size_t)ntiles + 2 * blockIdx.x + 1] = t_now;
     }
 }
 
@@ -906,7 +927,8 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
     if (NF) smem += (size_t)(NW + 2 * ((NW + 31) / 32)) * sizeof(uint32_t);   // deferred bitmap + inlist bitmaps
     if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
-        smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV * (32 * SPL * Op::PACK + 1) * sizeof(int32_t));
+        smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV *
+                                  (Op::KEYED ? KeyedStage<SPL>::RS : 32 * SPL * Op::PACK + 1) * sizeof(int32_t));
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem > (size_t)max_optin) return false;
@@ -1115,7 +1137,7 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
     };
     TraceJob *tj = nullptr;
     if (trace_path) {
-        ttrace.alloc((size_t)4 * run.ntiles);
+        ttrace.alloc((size_t)4 * run.ntiles + 2 * 1024);   // + per-CTA {sweep end, exit}
         WR_CUDA(cudaMemsetAsync(ttrace.p, 0, ttrace.bytes(), st));
         run.fuse.trace = ttrace.p;
         tj = new TraceJob{nullptr, nullptr, nullptr, run.ntiles, run.tsw(), trace_path};
@@ -1141,6 +1163,12 @@ void bf_run(const wr_graph *g, const BfRun &run0, BfTileStats *d_stats, cudaStre
                 for (int k = 0; k < t->ntiles; ++k)
                     fprintf(f, "%d %d %lld %lld %lld %lld\n", k, pos[k], t->h[4 * k], t->h[4 * k + 1], t->h[4 * k + 2],
                             t->h[4 * k + 3]);
+                fclose(f);
+            }
+            if (FILE *f = fopen((t->path + ".cta").c_str(), "a")) {   // per CTA: sweep end, exit (ns)
+                const long long *c = t->h + 4 * (size_t)t->ntiles;
+                for (int b = 0; b < 1024; ++b)
+                    if (c[2 * b + 1]) fprintf(f, "%d %lld %lld\n", b, c[2 * b], c[2 * b + 1]);
                 fclose(f);
             }
             if (FILE *f = fopen((t->path + ".src").c_str(), "a")) {
@@ -1459,8 +1487,9 @@ template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                                int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
-                                               int32_t (*spw)[32 * SPL * 2 + 1], int lane, uint32_t thr,
-                                               int *overflow) {
+                                               int32_t *spw, int lane, uint32_t thr, int *overflow,
+                                               int (&srow)[2 * SPL], int &srow_tile) {
+    using KS = KeyedStage<SPL>;
     constexpr int TSW = 32 * SPL;
     constexpr int TS = TSW * 2;
     constexpr int NS = SPL * 2;
@@ -1468,36 +1497,47 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
     const int V = g.V;
     const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
     const int nv = min(PV, V - c0);
-    const int a_lane = lane < nv ? g.in_ptr[c0 + lane] : 0;
+    const int a_lane = lane <= nv ? g.in_ptr[c0 + lane] : 0;
     Vec<SPL> key[PV];
 #pragma unroll
     for (int jv = 0; jv < PV; ++jv)
         if (jv < nv) key[jv] = vload<SPL>(Rl + (size_t)(c0 + jv) * TSW);
     bool ovf = false;
 #pragma unroll
-    for (int jv = 0; jv < PV; ++jv) {
+    for (int jv = 0; jv < PV; jv += 2) {
         if (jv >= nv) break;
-        const int a0 = __shfl_sync(FULL, a_lane, jv);
+        // the in-arc tails of vertices jv (lanes 0-15) and jv + 1 (16-31) in
+        // registers (in-degree <= 15): a slot's pred is one shuffle away
+        const int half = lane >> 4, vj = min(jv + half, nv - 1);
+        const int lo = __shfl_sync(FULL, a_lane, vj), hi = __shfl_sync(FULL, a_lane, vj + 1);
+        const int tails = (lane & 15) < hi - lo ? g.in_src[lo + (lane & 15)] : -1;
 #pragma unroll
-        for (int j = 0; j < SPL; ++j)
+        for (int d = 0; d < 2; ++d) {
+            if (jv + d >= nv) break;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t key1 = (key[jv].x[j] >> (16 * h)) & 0xffffu;
-                const uint32_t k = key1 & 0xfu;
-                // range check of the keyed rows (the sweep skips it): a stored
-                // distance at or past 0x7ff - max_w may hide a clipped path
-                ovf |= key1 >= thr && key1 != 0x7fffu;
-                spw[jv][lane * NS + j * 2 + h] = k == 15u ? -1 : g.in_src[a0 + (int)k];
-            }
+            for (int j = 0; j < SPL; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t key1 = (key[jv + d].x[j] >> (16 * h)) & 0xffffu;
+                    const uint32_t k = key1 & 0xfu;
+                    // range check of the keyed rows (the sweep skips it): a stored
+                    // distance at or past 0x7ff - max_w may hide a clipped path
+                    ovf |= key1 >= thr && key1 != 0x7fffu;
+                    const int u = __shfl_sync(FULL, tails, 16 * d + (int)(k & 15u));
+                    spw[(jv + d) * KS::RS + KS::at(lane * NS + j * 2 + h)] = k == 15u ? -1 : u;
+                }
+        }
     }
     if (__any_sync(FULL, ovf) && lane == 0) atomicOr(overflow, 1);
     __syncwarp();
     const bool vec = (V & 3) == 0 && nv == PV;
-    int srow[TS / 32];
+    if (srow_tile != tile) {   // the slots' output rows, loaded once per tile by this warp
 #pragma unroll
-    for (int k = 0; k < TS / 32; ++k) {
-        const int sl = tile * TS + lane + 32 * k;
-        srow[k] = tile_src[sl] < 0 ? -1 : (slot_row ? slot_row[sl] : sl);
+        for (int k = 0; k < TS / 32; ++k) {
+            const int sl = tile * TS + lane + 32 * k;
+            srow[k] = tile_src[sl] < 0 ? -1 : (slot_row ? slot_row[sl] : sl);
+        }
+        srow_tile = tile;
     }
 #pragma unroll
     for (int k = 0; k < TS / 32; ++k) {
@@ -1505,12 +1545,12 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
         const int sl_in = lane + 32 * k;
         int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
         if (vec) {
-            reinterpret_cast<int4 *>(dst)[0] =
-                make_int4(spw[0][sl_in], spw[1][sl_in], spw[2][sl_in], spw[3][sl_in]);
+            const int a = KS::at(sl_in);
+            reinterpret_cast<int4 *>(dst)[0] = make_int4(spw[a], spw[KS::RS + a], spw[2 * KS::RS + a], spw[3 * KS::RS + a]);
             reinterpret_cast<int4 *>(dst)[1] =
-                make_int4(spw[4][sl_in], spw[5][sl_in], spw[6][sl_in], spw[7][sl_in]);
+                make_int4(spw[4 * KS::RS + a], spw[5 * KS::RS + a], spw[6 * KS::RS + a], spw[7 * KS::RS + a]);
         } else {
-            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv][sl_in];
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv * KS::RS + KS::at(sl_in)];
         }
     }
     __syncwarp();   // spw is reused by the warp's next job

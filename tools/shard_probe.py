@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--nvlink-gbs", type=float, default=700.0, help="assumed all-gather bus bandwidth")
+    ap.add_argument("--pred", action="store_true", help="also write each rank's pred rows (the bench's step)")
     a = ap.parse_args()
     import torch
 
@@ -40,6 +41,7 @@ def main():
         wr.route_orders(G, d_ptr, d_nodes, results=warm)
     torch.cuda.synchronize()
     base = None
+    pred_buf = [None]
     for W in a.worlds:
       for rep in range(2):   # the first pass of a world size warms allocations of its sizes
           per_rank = []
@@ -48,6 +50,14 @@ def main():
               e0, e1 = ev(), ev()
               e0.record()
               p = wr.OrdersPlan(G, d_ptr, d_nodes, r, W)
+              if a.pred:
+                  n_src = max(p.info.src_hi - p.info.src_lo, 1)
+                  if pred_buf[0] is None or pred_buf[0].shape[0] < n_src:
+                      pred_buf[0] = None
+                      torch.cuda.empty_cache()
+                      pred_buf[0] = torch.empty((n_src, g.V), dtype=torch.int32, device=dev)
+                  p.close()
+                  p = wr.OrdersPlan(G, d_ptr, d_nodes, r, W, pred_out=pred_buf[0])
               e1.record()
               torch.cuda.synchronize()
               plans.append((p, e0.elapsed_time(e1)))
@@ -77,7 +87,8 @@ def main():
                             "projected_efficiency": tput / (base * W), "rank_ms_max": max(per_rank),
                             "rank_ms_min": min(per_rank), "plan_ms": max(p[1] for p in plans),
                             "local_ms_max": max(loc), "finish_ms_max": max(fin), "allgather_ms_assumed": ag_ms,
-                            "max_send_bytes": max_send * 4, "measured_on": "1 GPU, ranks run sequentially"}),
+                            "max_send_bytes": max_send * 4, "pred": a.pred,
+                            "measured_on": "1 GPU, ranks run sequentially"}),
                 flush=True)
           for p, _ in plans:
               p.close()
