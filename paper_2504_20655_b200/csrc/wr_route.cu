@@ -119,13 +119,18 @@ __device__ __forceinline__ void leaf(uint32_t cost, Best &best, uint32_t &rank) 
 // Ds rows have stride ns. CL (closed tour, NEXT-4): the depot is local
 // index ns - 1; the walk starts there (prev = ns - 1, cost 0) and every
 // leaf adds the return leg to it.
-template <class C, bool CL>
+// The matrix is replicated per lane (element e of lane l at word e * 32 + l,
+// Ds already offset by the lane): the 32 lanes of a warp walk different
+// subtrees and read different elements, which in a single copy collide in
+// shared-memory banks; one copy per lane puts every lane in its own bank.
+#define DSL(e) Ds[(e) << SH]
+template <class C, bool CL, int SH>
 __device__ __forceinline__ uint32_t ret_leg(const uint32_t *Ds, int ns, int last, uint32_t cost) {
-    if constexpr (CL) return C::add(cost, Ds[last * ns + ns - 1]);
+    if constexpr (CL) return C::add(cost, DSL(last * ns + ns - 1));
     return cost;
 }
 
-template <class C, int L, bool CL>
+template <class C, int L, bool CL, int SH>
 struct Dfs {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
@@ -133,74 +138,77 @@ struct Dfs {
         while (rem) {
             const int x = __ffs(rem) - 1;
             rem &= rem - 1;
-            Dfs<C, L - 1, CL>::run(Ds, ns, unused & ~(1u << x), x, C::add(cost, Ds[prev * ns + x]), best, rank);
+            Dfs<C, L - 1, CL, SH>::run(Ds, ns, unused & ~(1u << x), x, C::add(cost, DSL(prev * ns + x)), best, rank);
         }
     }
 };
-template <class C, bool CL>
-struct Dfs<C, 2, CL> {   // two stops left, a < b: leaves (a, b) then (b, a)
+template <class C, bool CL, int SH>
+struct Dfs<C, 2, CL, SH> {   // two stops left, a < b: leaves (a, b) then (b, a)
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
         const int b = __ffs(unused & (unused - 1)) - 1;
-        const uint32_t cab = C::add(C::add(cost, Ds[prev * ns + a]), Ds[a * ns + b]);
-        const uint32_t cba = C::add(C::add(cost, Ds[prev * ns + b]), Ds[b * ns + a]);
-        leaf<C>(ret_leg<C, CL>(Ds, ns, b, cab), best, rank);
-        leaf<C>(ret_leg<C, CL>(Ds, ns, a, cba), best, rank);
+        const uint32_t cab = C::add(C::add(cost, DSL(prev * ns + a)), DSL(a * ns + b));
+        const uint32_t cba = C::add(C::add(cost, DSL(prev * ns + b)), DSL(b * ns + a));
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, b, cab), best, rank);
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, cba), best, rank);
     }
 };
-template <class C, bool CL>
-struct Dfs<C, 3, CL> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
+template <class C, bool CL, int SH>
+struct Dfs<C, 3, CL, SH> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
         const uint32_t u2 = unused & (unused - 1);
         const int b = __ffs(u2) - 1;
         const int c = __ffs(u2 & (u2 - 1)) - 1;
-        const uint32_t *Dp = Ds + prev * ns, *Da = Ds + a * ns, *Db = Ds + b * ns, *Dc = Ds + c * ns;
-        const uint32_t pa = C::add(cost, Dp[a]), pb = C::add(cost, Dp[b]), pc = C::add(cost, Dp[c]);
-        const uint32_t ab = C::add(pa, Da[b]), ac = C::add(pa, Da[c]);
-        const uint32_t ba = C::add(pb, Db[a]), bc = C::add(pb, Db[c]);
-        const uint32_t ca = C::add(pc, Dc[a]), cb = C::add(pc, Dc[b]);
-        leaf<C>(ret_leg<C, CL>(Ds, ns, c, C::add(ab, Db[c])), best, rank);   // a b c
-        leaf<C>(ret_leg<C, CL>(Ds, ns, b, C::add(ac, Dc[b])), best, rank);   // a c b
-        leaf<C>(ret_leg<C, CL>(Ds, ns, c, C::add(ba, Da[c])), best, rank);   // b a c
-        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(bc, Dc[a])), best, rank);   // b c a
-        leaf<C>(ret_leg<C, CL>(Ds, ns, b, C::add(ca, Da[b])), best, rank);   // c a b
-        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(cb, Db[a])), best, rank);   // c b a
+        const int p0 = prev * ns, a0 = a * ns, b0 = b * ns, c0 = c * ns;
+        const uint32_t pa = C::add(cost, DSL(p0 + a)), pb = C::add(cost, DSL(p0 + b)), pc = C::add(cost, DSL(p0 + c));
+        const uint32_t ab = C::add(pa, DSL(a0 + b)), ac = C::add(pa, DSL(a0 + c));
+        const uint32_t ba = C::add(pb, DSL(b0 + a)), bc = C::add(pb, DSL(b0 + c));
+        const uint32_t ca = C::add(pc, DSL(c0 + a)), cb = C::add(pc, DSL(c0 + b));
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, c, C::add(ab, DSL(b0 + c))), best, rank);   // a b c
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, b, C::add(ac, DSL(c0 + b))), best, rank);   // a c b
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, c, C::add(ba, DSL(a0 + c))), best, rank);   // b a c
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, C::add(bc, DSL(c0 + a))), best, rank);   // b c a
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, b, C::add(ca, DSL(a0 + b))), best, rank);   // c a b
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, C::add(cb, DSL(b0 + a))), best, rank);   // c b a
     }
 };
-template <class C, bool CL>
-struct Dfs<C, 1, CL> {
+template <class C, bool CL, int SH>
+struct Dfs<C, 1, CL, SH> {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
                                                Best &best, uint32_t &rank) {
         const int a = __ffs(unused) - 1;
-        leaf<C>(ret_leg<C, CL>(Ds, ns, a, C::add(cost, Ds[prev * ns + a])), best, rank);
+        leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, C::add(cost, DSL(prev * ns + a))), best, rank);
     }
 };
 
-template <class C, bool CL>
+template <class C, bool CL, int SH>
 __device__ __forceinline__ void walk_subtree(int L, const uint32_t *Ds, int ns, uint32_t unused, int prev,
                                              uint32_t cost, Best &best, uint32_t &rank) {
     switch (L) {
-        case 1: Dfs<C, 1, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 2: Dfs<C, 2, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 3: Dfs<C, 3, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 4: Dfs<C, 4, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 5: Dfs<C, 5, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 6: Dfs<C, 6, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        default: Dfs<C, 7, CL>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 1: Dfs<C, 1, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 2: Dfs<C, 2, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 3: Dfs<C, 3, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 4: Dfs<C, 4, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 5: Dfs<C, 5, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 6: Dfs<C, 6, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        default: Dfs<C, 7, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
     }
 }
 
 // One warp per work item (problem, prefix range). D submatrix staged in smem.
 constexpr int ENUM_WARPS = 8;
-template <class C>
+// SH = 5: dynamic shared memory holds per warp ns_max^2 elements x 32 lane
+// copies (large problems: 9-13 stops, where bank conflicts of a single copy
+// dominate); SH = 0: one copy per warp (6-8 stops: occupancy matters more).
+template <class C, int SH>
 __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const RouteProblem *__restrict__ probs,
                                                                      const RouteWorkItem *__restrict__ items,
                                                                      int nitems, const uint32_t *__restrict__ Dall,
-                                                                     uint64_t *item_best) {
-    __shared__ uint32_t sD[ENUM_WARPS][(WR_MAX_EXACT + 1) * (WR_MAX_EXACT + 1)];
+                                                                     uint64_t *item_best, int ns_max) {
+    extern __shared__ uint32_t sDyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int it = blockIdx.x * ENUM_WARPS + warp;
     if (it >= nitems) return;
@@ -210,13 +218,26 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
     const bool closed = pr.dep >= 0;
     const int ns = n + (closed ? 1 : 0);   // closed: local index n is the depot
     const uint32_t *D = Dall + (size_t)pr.order * DSTRIDE;
-    uint32_t *Ds = sD[warp];
-    for (int e = lane; e < ns * ns; e += 32) {
-        const int a = e / ns, b = e % ns;
-        const int ia = a < n ? nib(pr.map, a) : pr.dep, ib = b < n ? nib(pr.map, b) : pr.dep;
-        Ds[e] = D[ia * MS + ib];
+    uint32_t *Dw = sDyn + (size_t)warp * ns_max * ns_max * (SH ? 32 : 1);
+    // stage: lane l loads element e = l, l + 32, ...; replicated: every
+    // element is then broadcast to the 32 lane copies by a shuffle
+    for (int e0 = 0; e0 < ns * ns; e0 += 32) {
+        const int e = e0 + lane;
+        uint32_t v = 0;
+        if (e < ns * ns) {
+            const int a = e / ns, b = e % ns;
+            const int ia = a < n ? nib(pr.map, a) : pr.dep, ib = b < n ? nib(pr.map, b) : pr.dep;
+            v = D[ia * MS + ib];
+        }
+        if constexpr (SH) {
+            const int cnt = min(32, ns * ns - e0);
+            for (int k = 0; k < cnt; ++k) Dw[(e0 + k) * 32 + lane] = __shfl_sync(0xffffffffu, v, k);
+        } else if (e < ns * ns) {
+            Dw[e] = v;
+        }
     }
     __syncwarp();
+    const uint32_t *Ds = Dw + (SH ? lane : 0);   // element e at Ds[e << SH]
     const int p = prefix_depth(n);
     const int L = n - p;
     const uint32_t sub = c_fact[L];
@@ -236,12 +257,12 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
             for (uint32_t t = 0; t < digit; ++t) m &= m - 1;
             const int x = __ffs(m) - 1;
             unused &= ~(1u << x);
-            cost = prev >= 0 ? C::add(cost, Ds[prev * ns + x]) : cost;
+            cost = prev >= 0 ? C::add(cost, DSL(prev * ns + x)) : cost;
             prev = x;
         }
         uint32_t rank = (uint32_t)q * sub;
-        if (closed) walk_subtree<C, true>(L, Ds, ns, unused, prev, cost, best, rank);
-        else walk_subtree<C, false>(L, Ds, ns, unused, prev, cost, best, rank);
+        if (closed) walk_subtree<C, true, SH>(L, Ds, ns, unused, prev, cost, best, rank);
+        else walk_subtree<C, false, SH>(L, Ds, ns, unused, prev, cost, best, rank);
     }
     uint64_t packed = ((uint64_t)best.key << 32) | best.rank;
 #pragma unroll
@@ -625,6 +646,7 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 if (R.seglen[k] > WR_MAX_EXACT) { R.status = WR_ETOOLARGE; break; }
                 if (R.seglen[k] >= 2) {
                     const int nj = R.seglen[k];
+                    atomicMax(hk_count + 3, nj + (nseg == 1 && R.dep >= 0 ? 1 : 0));   // enum staging size
                     const int p = prefix_depth(nj);
                     const int64_t npre = fact(nj) / fact(nj - p);
                     const int64_t per = chunk / fact(nj - p) > 0 ? chunk / fact(nj - p) : 1;
@@ -1796,8 +1818,21 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     count_launch();
     WR_LAUNCH_CHECK();
     if (nitems > 0) {
-        route_enum_kernel<C><<<gridn(nitems, ENUM_WARPS), ENUM_WARPS * 32, 0, st>>>(probs.p, items.p, nitems, Dall,
-                                                                                    item_best.p);
+        // measured: replicated copies halve an 11-stop exact batch (C4 m = 1:
+        // 164 -> 82 ms/step) but cost ~2 ms on C5's 6-8-stop orders (lower
+        // occupancy), so they serve launches whose largest problem has >= 9
+        const int ns_max = std::max(2, hkc[3]);
+        const bool rep = ns_max >= 9;
+        const size_t esmem = (size_t)ENUM_WARPS * ns_max * ns_max * (rep ? 32 : 1) * sizeof(uint32_t);
+        if (rep) {
+            WR_CUDA(cudaFuncSetAttribute(route_enum_kernel<C, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)esmem));
+            route_enum_kernel<C, 5><<<gridn(nitems, ENUM_WARPS), ENUM_WARPS * 32, esmem, st>>>(
+                probs.p, items.p, nitems, Dall, item_best.p, ns_max);
+        } else {
+            route_enum_kernel<C, 0><<<gridn(nitems, ENUM_WARPS), ENUM_WARPS * 32, esmem, st>>>(
+                probs.p, items.p, nitems, Dall, item_best.p, ns_max);
+        }
         problem_reduce_kernel<<<gridn(nprob, 128), 128, 0, st>>>(probs.p, nprob, item_best.p, prob_best.p);
         count_launch();
         count_launch();
