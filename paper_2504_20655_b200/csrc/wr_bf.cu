@@ -905,11 +905,14 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             const int k = (int)(j / chunks);
             if (k != kcur) {   // wait until tile k (in completion order) is done
                 if (lane == 0) {
+                    // poll relaxed (an acquire load invalidates the SM's L1 on
+                    // every try), then one acquire once the tile is published
                     for (;;) {
-                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(t) : "l"(fuse.done_list + k) : "memory");
+                        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(t) : "l"(fuse.done_list + k) : "memory");
                         if (t >= 0) break;
                         __nanosleep(256);
                     }
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(t) : "l"(fuse.done_list + k) : "memory");
                 }
                 t = __shfl_sync(FULL, t, 0);
                 kcur = k;
