@@ -586,16 +586,18 @@ template <class Op, int SPL, int PA>
 __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restrict__ tile_src,
                                          const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                          int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
-                                         int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane);
+                                         int c0, int32_t *spw, int lane);
 
 // keyed staging rows: slot s at s + s / 32 (a skew that makes both the
 // per-lane writes of 8 consecutive slots and the per-slot reads conflict-free)
-template <int SPL>
-struct KeyedStage {
-    static constexpr int TS = 64 * SPL;
+template <int TS_>
+struct SkewStage {
+    static constexpr int TS = TS_;
     static constexpr int RS = TS + TS / 32 + 1;
     __device__ static int at(int s) { return s + (s >> 5); }
 };
+template <int SPL>
+using KeyedStage = SkewStage<64 * SPL>;
 template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
@@ -881,7 +883,6 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
         // 8-vertex chunk) - a job waits only for a tile that a running CTA
         // is still relaxing; the shared memory is free for the staging rows
         constexpr int PV = PredShape::PV;
-        int32_t(*spw)[TS + 1] = reinterpret_cast<int32_t(*)[TS + 1]>(smem) + warp * PV;
         const int chunks = (V + PV - 1) / PV;
         const long long njobs = (long long)ntiles * chunks;
         int srow_cache[2 * SPL], srow_tile = -1;   // keyed jobs: output rows of the current tile's slots
@@ -924,7 +925,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                                     thr2 & 0xffffu, &stats->overflow, srow_cache, srow_tile);
             else
                 pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
-                                       (int)(j % chunks) * PV, spw, lane);
+                                       (int)(j % chunks) * PV,
+                                       reinterpret_cast<int32_t *>(smem) + warp * PV * SkewStage<TS>::RS, lane);
         }
     }
     if (fuse.trace && threadIdx.x == 0) {
@@ -945,7 +947,7 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     if (NF) smem += (size_t)(NW + 2 * ((NW + 31) / 32)) * sizeof(uint32_t);   // deferred bitmap + inlist bitmaps
     if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
         smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV *
-                                  (Op::KEYED ? KeyedStage<SPL>::RS : 32 * SPL * Op::PACK + 1) * sizeof(int32_t));
+                                  SkewStage<32 * SPL * Op::PACK>::RS * sizeof(int32_t));
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem > (size_t)max_optin) return false;
@@ -1329,7 +1331,8 @@ template <class Op, int SPL, int PA>
 __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restrict__ tile_src,
                                          const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
                                          int64_t out_row0, int32_t *__restrict__ pred_out, int *flat_tiles, int tile,
-                                         int c0, int32_t (*spw)[32 * SPL * Op::PACK + 1], int lane) {
+                                         int c0, int32_t *spw, int lane) {
+    using SK = SkewStage<32 * SPL * Op::PACK>;   // skewed staging rows (bank-conflict-free)
     constexpr int TSW = 32 * SPL;           // 32-bit words per row
     static_assert(PredShape::PV == 8, "the output stores write 8 columns per slot");
     constexpr int P = Op::PACK;
@@ -1463,8 +1466,8 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
         flat |= (need0 | need1) != 0;   // reachable, no steep tight in-arc: flat
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            spw[jv][lane * NS + j] = best0[j];
-            if (two) spw[jv1][lane * NS + j] = best1[j];
+            spw[jv * SK::RS + SK::at(lane * NS + j)] = best0[j];
+            if (two) spw[jv1 * SK::RS + SK::at(lane * NS + j)] = best1[j];
         }
     }
     __syncwarp();
@@ -1484,12 +1487,12 @@ __device__ __forceinline__ void pred_job(const DevGraph &g, const int *__restric
         const int sl_in = lane + 32 * k;
         int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
         if (vec) {
-            reinterpret_cast<int4 *>(dst)[0] =
-                make_int4(spw[0][sl_in], spw[1][sl_in], spw[2][sl_in], spw[3][sl_in]);
+            const int a = SK::at(sl_in);
+            reinterpret_cast<int4 *>(dst)[0] = make_int4(spw[a], spw[SK::RS + a], spw[2 * SK::RS + a], spw[3 * SK::RS + a]);
             reinterpret_cast<int4 *>(dst)[1] =
-                make_int4(spw[4][sl_in], spw[5][sl_in], spw[6][sl_in], spw[7][sl_in]);
+                make_int4(spw[4 * SK::RS + a], spw[5 * SK::RS + a], spw[6 * SK::RS + a], spw[7 * SK::RS + a]);
         } else {
-            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv][sl_in];
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv * SK::RS + SK::at(sl_in)];
         }
     }
     if (__any_sync(FULL, flat) && lane == 0) atomicOr(&flat_tiles[tile], 1);
@@ -1580,13 +1583,13 @@ __global__ void __launch_bounds__(PW * 32, MINB) bf_pred_kernel(DevGraph g, cons
                                                       int32_t *__restrict__ pred_out, int *flat_tiles) {
     constexpr int TS = 32 * SPL * Op::PACK;
     constexpr int PV = PredShape::PV;
-    __shared__ int32_t sp[PW][PV][TS + 1];
+    __shared__ int32_t sp[PW][PV][SkewStage<TS>::RS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int chunks = (g.V + PV - 1) / PV;
     const int64_t job = (int64_t)blockIdx.x * PW + warp;
     if (job >= (int64_t)ntiles * chunks) return;
     pred_job<Op, SPL, PA>(g, tile_src, rows, slot_row, out_row0, pred_out, flat_tiles, (int)(job / chunks),
-                          (int)(job % chunks) * PV, sp[warp], lane);
+                          (int)(job % chunks) * PV, &sp[warp][0][0], lane);
 }
 
 template <class Op, int SPL, int MINB, int PA, int PW = 8 / Op::PACK>
