@@ -331,10 +331,21 @@ def main():
                 and a.depot is None and not a.nearfar)
     if captured and os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("bf_frontier_kernel", {}).get("dram_bytes")
-    # ALU view: one DPX add+min (VIADDMNMX, ALU pipe: 64 lanes/clk/SM) per
-    # useful relaxation, at the clock seen under load
+    # ALU view: one DPX add-min lane-op per useful relaxation (packed rows:
+    # VIADDMNMX.U16x2, two relaxations per lane-op). Peak = the measured DPX
+    # rate on this GPU model (tools/dpx_peak.cu: 1 warp instruction / clk /
+    # SM for both forms -> profiles/r02_dpx_peak.jsonl), scaled to the clock
+    # seen under load; fp32 rows add and min with two instructions, so the
+    # 32-bit figure is an upper bound there
     clk = (ck.get("sm_mhz") or 1965.0) * 1e6
-    alu_peak = 148 * 64 * clk
+    dpx = {}
+    dpath = os.path.join(ROOT, "profiles", "r02_dpx_peak.jsonl")
+    if os.path.exists(dpath):
+        for ln in open(dpath):
+            r = json.loads(ln)
+            dpx[r["op"]] = r["warp_instr_per_clk_per_sm"] * 32 * r["sms"]
+    lanes = dpx.get("VIADDMNMX.U16x2" if rb == 16 else "VIADDMNMX.U32", 148 * 32)
+    alu_peak = lanes * clk * (2 if rb == 16 else 1)
     alu_ach = useful / bf_s if bf_s > 0 else None
     line = {
         "metric": METRIC, "value": B / (ms / 1e3), "unit": "orders/s", "n_gpus": world, "steps": a.steps,
@@ -364,7 +375,8 @@ def main():
                      "note": "latency-bound frontier sweep; see DESIGN.md section 9"},
         "roofline_alu": {"bound": "alu", "achieved": alu_ach / 1e12 if alu_ach else None,
                          "peak": alu_peak / 1e12, "unit": "T relaxations/s",
-                         "frac": alu_ach / alu_peak if alu_ach else None},
+                         "frac": alu_ach / alu_peak if alu_ach else None,
+                         "peak_kind": "measured DPX rate (profiles/r02_dpx_peak.jsonl)" if dpx else "assumed"},
         "gpu_launches": int(launches[0]),
         "clocks": ck,
         "e2e": e2e,
