@@ -111,7 +111,7 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
+def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False, depot=None):
     """The oracle as it stands, on the host cores, on a bounded sample: BF from
     a prefix of the distinct sources and exact routing of a prefix of the
     orders (their D rows recomputed by the oracle); extrapolated to the whole
@@ -138,7 +138,8 @@ def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
                      order_nodes=orders.order_nodes[:int(orders.order_ptr[nord])].copy())
         sstops = np.unique(sub.order_nodes)
         t0 = time.perf_counter()
-        res = oracle.route_orders(g, sub, m=m, nthreads=threads, pairs=pairs)
+        res = oracle.route_orders(g, sub, m=m, nthreads=threads, pairs=pairs,
+                                  depot=-1 if depot is None else depot)
         dt = time.perf_counter() - t0
         assert res["rc"] == 0
         t_route = max(0.0, (dt - t_bf * sstops.size)) / nord
@@ -153,6 +154,19 @@ def cpu_baseline(g, orders, seconds, S_total, m=1, pairs=False):
                       f"extrapolated to all {B} orders", "extrapolated": True}
 
 
+def workload_config(a, g, orders, S):
+    """The config dict both arms print (same keys and values)."""
+    return {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]", "orders": orders.B,
+            "sources": S, "V": g.V, "E": g.E, "m": a.m, "pred": not a.no_pred,
+            "stitch": "boundary pairs (NEXT-1)" if a.pairs else ("paper O7" if a.m >= 2 else "exact"),
+            "tour": "open" if a.depot is None else f"closed through node {a.depot} (NEXT-4)",
+            "sweep": "near-far (NEXT-3)" if a.nearfar else "frontier",
+            "l2": ("working set (dist rows 4*V*S = %.1f GB) >> 126 MB L2; no flush needed" % (4 * g.V * S / 1e9))
+            if 4 * g.V * S > 4 * 126e6 else
+            ("working set (dist rows 4*V*S = %.3f GB) is L2-sized: steps run L2-warm "
+             "(a parity-case line, not the headline workload)" % (4 * g.V * S / 1e9))}
+
+
 def run_reference(a):
     """--impl reference: the CPU oracle on the same config/metric, bounded."""
     rank = int(os.environ.get("RANK", "0"))
@@ -165,15 +179,15 @@ def run_reference(a):
     cb = None
     for s in range(a.warmup + a.steps):
         t0 = time.perf_counter()
-        cb = cpu_baseline(g, orders, max(2.0, a.cpu_seconds / max(1, a.steps)), S, m=a.m, pairs=a.pairs)
+        cb = cpu_baseline(g, orders, max(2.0, a.cpu_seconds / max(1, a.steps)), S, m=a.m, pairs=a.pairs,
+                          depot=a.depot)
         if s >= a.warmup:
             per_step.append(time.perf_counter() - t0)
     val = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "orders/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * orders.B / val,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.wtype,
-            "data": "synthetic", "config": {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]",
-                                            "orders": orders.B, "sources": S, "V": g.V, "E": g.E},
+            "data": "synthetic", "config": workload_config(a, g, orders, S),
             "cpu_baseline": cb,
             "e2e": {"value": val, "unit": "orders/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s_per_sample": float(np.mean(per_step)) if per_step else None}
@@ -351,17 +365,9 @@ def main():
         "metric": METRIC, "value": B / (ms / 1e3), "unit": "orders/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": a.wtype, "data": "synthetic",
-        "config": {"workload": WORKLOAD if a.config == 5 else f"configs[{a.config-1}]", "orders": B,
-                   "sources": S, "V": g.V, "E": E, "m": a.m, "pred": not a.no_pred,
-                   "stitch": "boundary pairs (NEXT-1)" if a.pairs else ("paper O7" if a.m >= 2 else "exact"),
-                   "tour": "open" if a.depot is None else f"closed through node {a.depot} (NEXT-4)",
-                   "sweep": "near-far (NEXT-3)" if a.nearfar else "frontier",
-                   "bf_rows": ("packed u16x2, exact (15-bit bound checked per tile, else a 32-bit redo); "
-                               "outputs int32") if rb == 16 else "32-bit",
-                   "l2": ("working set (dist rows 4*V*S = %.1f GB) >> 126 MB L2; no flush needed" % (4 * g.V * S / 1e9))
-                   if 4 * g.V * S > 4 * 126e6 else
-                   ("working set (dist rows 4*V*S = %.3f GB) is L2-sized: steps run L2-warm "
-                    "(a parity-case line, not the headline workload)" % (4 * g.V * S / 1e9))},
+        "config": workload_config(a, g, orders, S),
+        "bf_rows": ("packed u16x2 keys (d << 4 | pred index), exact (bound checked, else packed / 32-bit redo); "
+                    "outputs int32") if rb == 16 else "32-bit",
         "edges_relaxed_per_sec": {"useful": useful / (ms / 1e3), "useful_bf_only": useful / bf_s if bf_s else None,
                                   "performed_bf_only": (relax[0] / a.steps) / bf_s if bf_s else None,
                                   "unit": "edges/s", "convention": "useful = S*E (one traversal of every arc per source)"},
@@ -382,7 +388,7 @@ def main():
         "e2e": e2e,
     }
     if not a.no_cpu and world == 1:   # rank 0 at N=1 only
-        line["cpu_baseline"] = cpu_baseline(g, orders, a.cpu_seconds, S, m=a.m, pairs=a.pairs)
+        line["cpu_baseline"] = cpu_baseline(g, orders, a.cpu_seconds, S, m=a.m, pairs=a.pairs, depot=a.depot)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
