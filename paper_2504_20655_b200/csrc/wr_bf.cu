@@ -936,6 +936,11 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
     }
 }
 
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 // Launch shapes (threads per CTA, min CTAs per SM) compiled for the sweep;
 // WR_BF_CONFIG selects one (tuning knob; default measured best).
 template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool LIST = false, int VB = 2, int TPS = 2,
@@ -948,6 +953,7 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
         smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV *
                                   SkewStage<32 * SPL * Op::PACK>::RS * sizeof(int32_t));
+    smem += (size_t)env_int("WR_SMEM_PAD", 0);   // experiment knob: less L1 (carveout study)
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     if (smem > (size_t)max_optin) return false;
@@ -956,7 +962,8 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     WR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     WR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
     per_sm = std::max(per_sm, 1);
-    const int grid = (int)std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
+    int grid = (int)std::min<int64_t>(run.ntiles, (int64_t)per_sm * nsm);
+    if (const int cap = env_int("WR_BF_GRID", 0)) grid = std::max(1, std::min(grid, cap));   // experiment knob
     DBuf<int> counter(1);
     WR_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
     NearFar nfa;
@@ -976,10 +983,6 @@ static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_sta
     return true;   // the counter goes back to the stream-ordered pool: no sync needed
 }
 
-static int env_int(const char *name, int dflt) {
-    const char *e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
 
 template <class Op, bool DENSE, int SPL>
 static void launch_dispatch(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {

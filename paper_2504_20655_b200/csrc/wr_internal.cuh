@@ -155,7 +155,6 @@ struct wr_graph {
     wr::DBuf<int> xy;       // [V*2] or empty
     wr::DBuf<int> z;        // [V] rack level or empty
     mutable wr::DBuf<int> hop_c;  // [V] BFS hops from a central vertex (tile cost key), built on first use
-    mutable std::vector<int> h_xy, h_z;  // host copies of xy / z for tile building, on first use
     int bbox[6] = {0, 0, 0, 0, 0, 0};   // xmin, xmax, ymin, ymax, zmin, zmax
     wr::DevGraph view() const {
         return wr::DevGraph{V, (int)E, in_ptr.p, in_src.p, in_w.p, in_arc.p, out_ptr.p, out_dst.p};

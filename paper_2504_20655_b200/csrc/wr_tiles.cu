@@ -13,7 +13,6 @@
 #include <algorithm>
 
 #include <climits>
-#include <thread>
 #include <vector>
 #include <cstdlib>
 #include "wr_internal.cuh"
@@ -129,64 +128,230 @@ __global__ void tiles_from_perm_kernel(const int *sources, int64_t lo, const int
     }
 }
 
-// Recursive coordinate bisection of the sources into tiles (host): a node
-// of k = ceil(n / tsw) tiles is split along the longest side of its
+// Recursive coordinate bisection of the sources into tiles, on the device:
+// a node of k = ceil(n / tsw) tiles is split along the longest side of its
 // bounding box (x, y at scale 2, rack level at scale 1: a level step is
 // half an aisle step in the generators' weights) so that the left part
 // holds exactly floor(k / 2) full tiles; leaves are single tiles, the only
-// partial tile is the last leaf. Measured on C5: a Morton-curve cut makes
-// some tiles straddle a curve jump (span 31-63 cells instead of 7), and a
-// tile's sweep time follows its spatial spread (corr 0.69; 17 ms compact
-// vs 40-52 ms straddling), not its rounds.
-static void rcb(int *idx, int n, int tsw, const int *cx, const int *cy, const int *cz, int depth = 0) {
-    if (n <= tsw) return;
-    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
-    for (int i = 0; i < n; ++i) {
-        const int c[3] = {cx[idx[i]], cy[idx[i]], cz[idx[i]]};
+// partial tile is the last leaf. The tree's shape depends on n and tsw only,
+// so the host lists every level's nodes up front and each level is one
+// launch (one CTA per node: bounding box, radix select of the split key,
+// stable partition) - no host round trip inside the step. Measured on C5: a
+// Morton-curve cut makes some tiles straddle a curve jump (span 31-63 cells
+// instead of 7), and a tile's sweep time follows its spatial spread (corr
+// 0.69; 17 ms compact vs 40-52 ms straddling), not its rounds.
+constexpr int RCB_NT = 1024;
+constexpr uint32_t RCB_FULL = 0xffffffffu;
+constexpr int RCB_BINS = 4096;   // 12-bit digits
+
+__global__ void rcb_coords_kernel(const int *sources, int64_t lo, int n, const int *xy, const int *z, int *cx,
+                                  int *cy, int *cz, int *idx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = sources[lo + i];
+    cx[i] = xy[2 * v];
+    cy[i] = xy[2 * v + 1];
+    cz[i] = z ? z[v] : 0;
+    idx[i] = i;
+}
+
+// exclusive block scan of one int per thread (RCB_NT threads); returns the total
+__device__ int rcb_scan(int x, int &excl, int *sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(RCB_FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sh[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int w = sh[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(RCB_FULL, wi, o);
+            if (lane >= o) wi += y;
+        }
+        sh[lane] = wi - w;
+        if (lane == 31) sh[32] = wi;
+    }
+    __syncthreads();
+    excl = sh[warp] + inc - x;
+    const int total = sh[32];
+    __syncthreads();
+    return total;
+}
+
+// node = {start, count, nl}: the first nl positions of the node's range end
+// up holding sources whose split key is <= every key on the right
+__global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, int *idx, int *tmp,
+                                                           const int *__restrict__ cx, const int *__restrict__ cy,
+                                                           const int *__restrict__ cz) {
+    __shared__ int hist[RCB_BINS];
+    __shared__ int sh[40];
+    __shared__ int s_red[6][32];
+    const int4 nd = nodes[blockIdx.x];
+    const int s = nd.x, n = nd.y, nl = nd.z;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int *id = idx + s;
+    // ---- bounding box
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (int i = threadIdx.x; i < n; i += RCB_NT) {
+        const int j = id[i];
+        const int c[3] = {cx[j], cy[j], cz[j]};
+#pragma unroll
         for (int a = 0; a < 3; ++a) {
-            lo[a] = std::min(lo[a], c[a]);
-            hi[a] = std::max(hi[a], c[a]);
+            mn[a] = min(mn[a], c[a]);
+            mx[a] = max(mx[a], c[a]);
         }
     }
-    int axis = 0;
-    for (int a = 1; a < 3; ++a)
-        if (hi[a] - lo[a] > hi[axis] - lo[axis]) axis = a;
-    const int *key = axis == 0 ? cx : axis == 1 ? cy : cz;
-    const int k = (n + tsw - 1) / tsw;
-    const int nl = (k / 2) * tsw;
-    std::nth_element(idx, idx + nl, idx + n, [&](int a, int b) { return key[a] < key[b] || (key[a] == key[b] && a < b); });
-    if (depth < 4 && n > 8192) {   // the two halves are independent: top levels on host threads
-        std::thread left([=] { rcb(idx, nl, tsw, cx, cy, cz, depth + 1); });
-        rcb(idx + nl, n - nl, tsw, cx, cy, cz, depth + 1);
-        left.join();
-    } else {
-        rcb(idx, nl, tsw, cx, cy, cz, depth + 1);
-        rcb(idx + nl, n - nl, tsw, cx, cy, cz, depth + 1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        mn[a] = __reduce_min_sync(RCB_FULL, mn[a]);
+        mx[a] = __reduce_max_sync(RCB_FULL, mx[a]);
+        if (lane == 0) { s_red[a][warp] = mn[a]; s_red[3 + a][warp] = mx[a]; }
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = __reduce_min_sync(RCB_FULL, s_red[a][lane]);
+            mx[a] = __reduce_max_sync(RCB_FULL, s_red[3 + a][lane]);
+        }
+        if (lane == 0) {
+            const long long side[3] = {2LL * ((long long)mx[0] - mn[0]), 2LL * ((long long)mx[1] - mn[1]),
+                                       (long long)mx[2] - mn[2]};
+            int axis = 0;
+            for (int a = 1; a < 3; ++a)
+                if (side[a] > side[axis]) axis = a;
+            sh[34] = axis;
+            sh[35] = mn[axis];
+            sh[36] = (int)((uint32_t)mx[axis] - (uint32_t)mn[axis]);   // < 2^32
+        }
+    }
+    __syncthreads();
+    const int *key = sh[34] == 0 ? cx : sh[34] == 1 ? cy : cz;
+    const int klo = sh[35];
+    const uint32_t range = (uint32_t)sh[36];
+    // ---- radix select: P = the key of rank nl (0-based) in the node
+    int bits = 0;
+    while (bits < 32 && (range >> bits)) ++bits;
+    uint32_t prefix = 0;   // the high bits of P found so far
+    int rank = nl;         // rank of P among the keys that share the prefix
+    for (int hi = bits; hi > 0;) {   // digit = key bits [shift, hi), bits >= hi fixed by prefix
+        const int shift = max(0, hi - 12);
+        const uint32_t dmask = (1u << (hi - shift)) - 1u;
+        for (int b = threadIdx.x; b < RCB_BINS; b += RCB_NT) hist[b] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += RCB_NT) {
+            const uint32_t k = ((uint32_t)key[id[i]] - (uint32_t)klo);
+            if (hi >= 32 || (k >> hi) == (prefix >> hi)) atomicAdd(&hist[(k >> shift) & dmask], 1);
+        }
+        __syncthreads();
+        constexpr int PER = RCB_BINS / RCB_NT;
+        int part = 0;
+#pragma unroll
+        for (int b = 0; b < PER; ++b) part += hist[threadIdx.x * PER + b];
+        int before = 0;
+        rcb_scan(part, before, sh);
+        if (rank >= before && rank < before + part) {   // exactly one thread
+            int r = rank - before, b = threadIdx.x * PER;
+            while (r >= hist[b]) r -= hist[b++];
+            sh[37] = b;
+            sh[38] = r;
+        }
+        __syncthreads();
+        prefix |= (uint32_t)sh[37] << shift;
+        rank = sh[38];
+        __syncthreads();
+        hi = shift;
+    }
+    const uint32_t P = prefix;
+    // ---- stable partition: keys < P, then (nl - #less) keys == P, left
+    const int chunk = (n + RCB_NT - 1) / RCB_NT;
+    const int c0 = min(n, threadIdx.x * chunk), c1 = min(n, c0 + chunk);
+    int lt = 0, eq = 0;
+    for (int i = c0; i < c1; ++i) {
+        const uint32_t k = ((uint32_t)key[id[i]] - (uint32_t)klo);
+        lt += k < P;
+        eq += k == P;
+    }
+    int lt0 = 0, eq0 = 0;
+    const int nlt = rcb_scan(lt, lt0, sh);
+    rcb_scan(eq, eq0, sh);
+    const int quota = nl - nlt;
+    int rt0 = (c0 - lt0 - eq0) + max(0, eq0 - quota);   // right-side elements before this chunk
+    for (int i = c0; i < c1; ++i) {
+        const int j = id[i];
+        const uint32_t k = ((uint32_t)key[j] - (uint32_t)klo);
+        int pos;
+        if (k < P) pos = lt0++;
+        else if (k == P && eq0 < quota) pos = nlt + eq0++;
+        else {
+            if (k == P) ++eq0;
+            pos = nl + rt0++;
+        }
+        tmp[s + pos] = j;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += RCB_NT) id[i] = tmp[s + i];
+}
+
+// the tree's levels: count of internal nodes per depth (host) ...
+static void rcb_level_sizes(int n, int tsw, int depth, std::vector<int> &cnt) {
+    if (n <= tsw) return;
+    const int k = (n + tsw - 1) / tsw, nl = (k / 2) * tsw;
+    if ((int)cnt.size() <= depth) cnt.resize(depth + 1, 0);
+    ++cnt[depth];
+    rcb_level_sizes(nl, tsw, depth + 1, cnt);
+    rcb_level_sizes(n - nl, tsw, depth + 1, cnt);
+}
+
+// ... and the same walk on the device writes the nodes (no host-to-device copy)
+struct RcbLevels {
+    int off[32];
+};
+__global__ void rcb_nodes_kernel(int n, int tsw, RcbLevels lv, int4 *nodes) {
+    int cur[32];
+    for (int d = 0; d < 32; ++d) cur[d] = lv.off[d];
+    int st_s[64], st_n[64], st_d[64], top = 0;
+    st_s[0] = 0; st_n[0] = n; st_d[0] = 0; top = 1;
+    while (top > 0) {
+        --top;
+        const int s = st_s[top], m = st_n[top], d = st_d[top];
+        if (m <= tsw) continue;
+        const int k = (m + tsw - 1) / tsw, nl = (k / 2) * tsw;
+        nodes[cur[d]++] = make_int4(s, m, nl, 0);
+        st_s[top] = s + nl; st_n[top] = m - nl; st_d[top] = d + 1; ++top;
+        st_s[top] = s; st_n[top] = nl; st_d[top] = d + 1; ++top;
     }
 }
 
-static bool rcb_perm(const wr_graph *g, const int *d_sources, int64_t lo, int n, int tsw, int *d_perm,
+static void rcb_perm(const wr_graph *g, const int *d_sources, int64_t lo, int n, int tsw, int *d_perm,
                      cudaStream_t st) {
-    if (g->h_xy.empty()) {   // host copy of the coordinates, once per graph
-        g->h_xy.resize((size_t)2 * g->V);
-        WR_CUDA(cudaMemcpy(g->h_xy.data(), g->xy.p, 8 * (size_t)g->V, cudaMemcpyDeviceToHost));
-        g->h_z.assign(g->V, 0);
-        if (g->z.p) WR_CUDA(cudaMemcpy(g->h_z.data(), g->z.p, 4 * (size_t)g->V, cudaMemcpyDeviceToHost));
+    std::vector<int> cnt;
+    rcb_level_sizes(n, tsw, 0, cnt);
+    if (cnt.size() > 32) WR_THROW(WR_EINTERNAL, "rcb: tree too deep");
+    RcbLevels lv{};
+    int total = 0;
+    for (size_t L = 0; L < cnt.size(); ++L) {
+        lv.off[L] = total;
+        total += cnt[L];
     }
-    std::vector<int> src(n), cx(n), cy(n), cz(n), idx(n);
-    WR_CUDA(cudaMemcpyAsync(src.data(), d_sources + lo, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
-    WR_CUDA(cudaStreamSynchronize(st));
-    for (int i = 0; i < n; ++i) {
-        const int v = src[i];
-        cx[i] = 2 * g->h_xy[2 * (size_t)v];
-        cy[i] = 2 * g->h_xy[2 * (size_t)v + 1];
-        cz[i] = g->h_z[v];
-        idx[i] = i;
+    DBuf<int> cx(n), cy(n), cz(n), tmp(n);
+    DBuf<int4> nodes(std::max(total, 1));
+    rcb_nodes_kernel<<<1, 1, 0, st>>>(n, tsw, lv, nodes.p);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    rcb_coords_kernel<<<(n + 255) / 256, 256, 0, st>>>(d_sources, lo, n, g->xy.p, g->z.p, cx.p, cy.p, cz.p, d_perm);
+    count_launch();
+    WR_LAUNCH_CHECK();
+    for (size_t L = 0; L < cnt.size(); ++L) {
+        rcb_level_kernel<<<cnt[L], RCB_NT, 0, st>>>(nodes.p + lv.off[L], d_perm, tmp.p, cx.p, cy.p, cz.p);
+        count_launch();
+        WR_LAUNCH_CHECK();
     }
-    rcb(idx.data(), n, tsw, cx.data(), cy.data(), cz.data());
-    WR_CUDA(cudaMemcpyAsync(d_perm, idx.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
-    WR_CUDA(cudaStreamSynchronize(st));   // idx lifetime
-    return true;
 }
 
 // Tile count: by default ceil(n / tsw) full tiles. WR_TILE_BALANCE=1 spreads
@@ -254,8 +419,7 @@ int make_tiles_ordered(const wr_graph *g, const int *d_sources, int64_t lo, int6
                                                                tile_src, slot_row, pos_of);
     count_launch();
     WR_LAUNCH_CHECK();
-    WR_CUDA(cudaStreamSynchronize(st));   // perm lifetime
-    return ntiles;
+    return ntiles;   // temporaries go back to the stream-ordered pool
 }
 
 }  // namespace wr
