@@ -1108,8 +1108,9 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
     const int tid = threadIdx.x;
     const int gtid = (int)crank * HK_THREADS + tid, gstride = HK_CL * HK_THREADS;
     __shared__ uint32_t Ds[DSTRIDE];
+    __shared__ uint32_t DsT[MS * (MS + 1)];   // DsT[j * 17 + i] = D[i][j] (conflict-free column reads)
     __shared__ uint32_t Din[MS], Dout[MS];   // closed tour (NEXT-4): the depot legs
-    __shared__ int s_i;
+    __shared__ int s_i, s_slow;
     uint32_t *W = ws + (size_t)(blockIdx.x / HK_CL) * ws_stride;
     for (;;) {
         if (crank == 0 && tid == 0) s_i = atomicAdd(next, 1);
@@ -1122,54 +1123,81 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
         const int n = R.ng;   // stops routed; local stop a is order stop nib(R.gmap, a)
         const bool closed = R.dep >= 0;
         const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+        if (tid == 0) s_slow = 0;
+        __syncthreads();
+        // int32 fast path: every leg finite and |leg| < 2^23, so prefix sums
+        // and bounds stay within +-2^29 and absent terms can be padded with
+        // +-2^30 instead of tested (results identical to the general path)
+        const auto leg_slow = [&](uint32_t v) {
+            if (!std::is_same<C, CostI32>::value) return false;
+            return v == C::INF || (int)v >= (1 << 23) || (int)v <= -(1 << 23);
+        };
         for (int e = tid; e < DSTRIDE; e += HK_THREADS) {
             const int a = e / MS, b = e % MS;
-            Ds[e] = (a < n && b < n) ? D[nib(R.gmap, a) * MS + nib(R.gmap, b)] : 0u;
+            const uint32_t v = (a < n && b < n) ? D[nib(R.gmap, a) * MS + nib(R.gmap, b)] : 0u;
+            Ds[e] = v;
+            DsT[b * (MS + 1) + a] = v;
+            if (leg_slow(v)) s_slow = 1;
         }
         if (closed && tid < n) {
             Din[tid] = D[R.dep * MS + nib(R.gmap, tid)];
             Dout[tid] = D[nib(R.gmap, tid) * MS + R.dep];
+            if (leg_slow(Din[tid]) || leg_slow(Dout[tid])) s_slow = 1;
         }
         const uint16_t *sets = L.sets;
         const int *off = L.off[n - HK_MIN];
         __syncthreads();
+        const bool fast = std::is_same<C, CostI32>::value && !s_slow;   // same in every CTA of the cluster
         // F({j}, j) = 0, or the depot leg of a closed tour
         if (gtid < n) __stcg(W + (size_t)(1u << gtid) * HK_RS + gtid, closed ? Din[gtid] : 0u);
         __syncthreads();
         cl.sync();
-        // 1. forward layers |S| = 2..n
+        // 1. forward layers |S| = 2..n, one item per (P, j): P of layer
+        //    |S| - 1, j not in P, S = P + j. Consecutive items share P (one
+        //    row fetch per warp), the column D[.][j] comes from DsT, and the
+        //    row's absent entries are masked (never read by the oracle's
+        //    min, reading R2): INF for fp32 (fl(INF + d) = INF is the
+        //    largest key; D is never -0), +2^30 on the int fast path
+        const uint32_t full = (1u << n) - 1u;
         for (int k = 2; k <= n; ++k) {
-            const int base = off[k], items = (off[k + 1] - base) * k;
-            // two states per thread per step: both predecessor rows (8 x 16 B)
-            // are in flight before either is reduced
-            for (int x0 = gtid; x0 < items; x0 += 2 * gstride) {
-                uint32_t S2[2], j2[2], P2[2], r[2][16];
-                bool ok2[2];
+            const int pb = off[k - 1], fan = n - k + 1, items = (off[k] - pb) * fan;
+            for (int x = gtid; x < items; x += gstride) {
+                const int pidx = x / fan, b = x - pidx * fan;
+                const uint32_t P = sets[pb + pidx];
+                const int j = __fns(~P & full, 0, b + 1);
+                const uint32_t *dcol = DsT + j * (MS + 1);
+                const uint4 *row = reinterpret_cast<const uint4 *>(W + (size_t)P * HK_RS);
+                uint32_t r[16];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int x = x0 + u * gstride;
-                    ok2[u] = x < items;
-                    const int xx = ok2[u] ? x : x0;
-                    const int sidx = xx / k, b = xx - sidx * k;
-                    S2[u] = sets[base + sidx];
-                    j2[u] = __fns(S2[u], 0, b + 1);
-                    P2[u] = S2[u] & ~(1u << j2[u]);
-                    const uint4 *row = reinterpret_cast<const uint4 *>(W + (size_t)P2[u] * HK_RS);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 v = __ldcg(row + q);
-                        r[u][4 * q] = v.x; r[u][4 * q + 1] = v.y; r[u][4 * q + 2] = v.z; r[u][4 * q + 3] = v.w;
-                    }
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 v = __ldcg(row + q);
+                    r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
                 }
+                uint32_t outv;
+                if (fast) {
+                    int bi = 0x7fffffff;
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    if (!ok2[u]) continue;
+                    for (int a2 = 0; a2 < 16; ++a2) {
+                        const int ra = ((P >> a2) & 1u) ? (int)r[a2] : (1 << 30);
+                        bi = min(bi, ra + (int)dcol[a2]);
+                    }
+                    outv = (uint32_t)bi;
+                } else if (std::is_same<C, CostF32>::value) {
                     uint32_t best = 0xffffffffu;
 #pragma unroll
-                    for (int a = 0; a < 16; ++a)
-                        if ((P2[u] >> a) & 1u) best = min(best, C::key(H::fwd(r[u][a], Ds[a * MS + j2[u]])));
-                    __stcg(W + (size_t)S2[u] * HK_RS + j2[u], C::unkey(best));
+                    for (int a2 = 0; a2 < 16; ++a2) {
+                        const uint32_t ra = ((P >> a2) & 1u) ? r[a2] : CostF32::INF;
+                        best = min(best, C::key(H::fwd(ra, dcol[a2])));
+                    }
+                    outv = C::unkey(best);
+                } else {
+                    uint32_t best = 0xffffffffu;
+#pragma unroll
+                    for (int a2 = 0; a2 < 16; ++a2)
+                        if ((P >> a2) & 1u) best = min(best, C::key(H::fwd(r[a2], dcol[a2])));
+                    outv = C::unkey(best);
                 }
+                __stcg(W + (size_t)(P | (1u << j)) * HK_RS + j, outv);
             }
             cl.sync();
         }
@@ -1217,11 +1245,21 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
                 for (int q = 0; q < 16; ++q)
                     mv[q] = ((rest >> q) & 1u) ? __ldcg(W + (size_t)(S | (1u << q)) * HK_RS + q) : H::NONE;
                 uint32_t best = H::NONE;
+                if (fast) {   // NONE -> -2^30: its c stays below -2^29, every real c above
+                    int bi = -(1 << 30) - (1 << 24);
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    if (!((rest >> q) & 1u)) continue;
-                    const uint32_t c = H::inv(Ds[j * MS + q], mv[q]);
-                    if (H::gt(c, best)) best = c;
+                    for (int q = 0; q < 16; ++q) {
+                        const int m = mv[q] == H::NONE ? -(1 << 30) : (int)mv[q];
+                        bi = max(bi, m - (int)Ds[j * MS + q]);
+                    }
+                    best = bi < -(1 << 29) ? H::NONE : (uint32_t)bi;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        if (!((rest >> q) & 1u)) continue;
+                        const uint32_t c = H::inv(Ds[j * MS + q], mv[q]);
+                        if (H::gt(c, best)) best = c;
+                    }
                 }
                 __stcg(W + (size_t)S * HK_RS + j, best);
             }

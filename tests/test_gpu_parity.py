@@ -358,6 +358,54 @@ def test_route_orders_held_karp_fp32_absorption():
     assert (res["status"] == 0).all()
 
 
+def _hk_digraph(seed, V=30, wmax=1000, neg=False, src_only=None, sink_only=None, ring=False):
+    """Random digraph for the Held-Karp int paths: weights in [1, wmax), or
+    reweighted by potentials (w + pi(u) - pi(v), some arcs negative, no
+    negative cycle); optional out-arcs-only / in-arcs-only nodes (INF legs);
+    ring: only arcs a -> a+1, a+3 (mod V), so legs span many arcs."""
+    rng = np.random.default_rng(seed)
+    pi = rng.integers(0, wmax // 2, V) if neg else np.zeros(V, np.int64)
+    src, dst, w = [], [], []
+    for a in range(V):
+        for b in range(V):
+            if ring:
+                if (b - a) % V not in (1, 3):
+                    continue
+            elif a == b or rng.random() > 0.5 or a == sink_only or b == src_only:
+                continue
+            src.append(a); dst.append(b); w.append(int(rng.integers(wmax // 2 if ring else 1, wmax)) + int(pi[a]) - int(pi[b]))
+    return G(V, src, dst, np.array(w, np.int32), xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+
+
+@pytest.mark.parametrize("case", ["fast", "large_legs", "negative", "inf_legs"])
+def test_route_orders_held_karp_int_paths(case):
+    """NEXT-2 int32: the Held-Karp kernel's fast path (every leg finite and
+    |leg| < 2^23: padded min/max, no INF tests) and its general path (a leg
+    >= 2^23, or unreachable pairs) both equal the oracle (O5)."""
+    kw = {"fast": dict(wmax=1000), "large_legs": dict(wmax=1 << 22, ring=True), "negative": dict(wmax=1000, neg=True),
+          "inf_legs": dict(wmax=1000, src_only=3, sink_only=7)}[case]
+    g = _hk_digraph(95, **kw)
+    rng = np.random.default_rng(96)
+    sizes = [13, 14, 15, 16] * 3
+    seqs = []
+    for k in sizes:
+        pick = rng.choice(g.V, k, replace=False)
+        if case == "inf_legs":
+            pick = np.unique(np.concatenate([pick[: k - 2], [3, 7]]))
+            while pick.size < k:
+                pick = np.unique(np.concatenate([pick, rng.choice(g.V, 1)]))
+        seqs.append(np.sort(pick))
+    nodes = np.concatenate(seqs).astype(np.int32)
+    ptr = np.concatenate([[0], np.cumsum([s.size for s in seqs])]).astype(np.int64)
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, len(seqs)
+    res, _ = compare_orders(g, orders, m=1)
+    assert (res["n"] >= 13).all()
+
+
 def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
     G = G or wr.Graph.from_gen(g)
     res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk, flags=flags) \
