@@ -1042,8 +1042,9 @@ __device__ inline float f32_inv(float d, float m) {
     if (isinf(m)) return __int_as_float(0x7f800000);
     const uint32_t mb = __float_as_uint(m);
     const int e = (int)(mb >> 23);
-    const double ulp = e > 0 ? ldexp(1.0, e - 150) : ldexp(1.0, -149);
-    const double T = (double)m + 0.5 * ulp;
+    // half an ulp of m: 2^(e - 151) for normal m, 2^-150 for subnormal (built directly)
+    const double half = __longlong_as_double((long long)((e > 0 ? e : 1) - 151 + 1023) << 52);
+    const double T = (double)m + half;
     const double lo = __dsub_rd(T, (double)d), hi = __dsub_ru(T, (double)d);
     float c = __double2float_rd(lo);
     if ((mb & 1u) && lo == hi && (double)c == lo) c = __uint_as_float(__float_as_uint(c) - 1u);   // strict
@@ -1265,50 +1266,53 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
             }
             cl.sync();
         }
-        // 3. lexicographic greedy (one thread)
-        if (crank == 0 && tid == 0) {
+        // 3. lexicographic greedy (one warp: lane q tests stop q, the
+        //    smallest passing lane is the pick - one L2 round trip per step)
+        if (crank == 0 && tid < 32) {
+            const int lane = tid;
             uint32_t S = 0, c = 0;
             int j = -1, seq[MS];
             bool ok = true;
             for (int a = 0; a < n && ok; ++a) {
-                int pick = -1;
-                uint32_t cn = 0;
-                for (int q = 0; q < n && pick < 0; ++q) {
-                    if ((S >> q) & 1u) continue;
-                    const uint32_t m = __ldcg(W + (size_t)(S | (1u << q)) * HK_RS + q);
-                    uint32_t nx = 0;
+                bool pass = false;
+                uint32_t nx = 0;
+                if (lane < n && !((S >> lane) & 1u)) {
+                    const uint32_t m = __ldcg(W + (size_t)(S | (1u << lane)) * HK_RS + lane);
                     if (a == 0) {   // the first stop's prefix: 0, or the depot leg
-                        const uint32_t c0 = closed ? Din[q] : 0u;
-                        if (m != H::NONE && !H::gt(c0, m)) { pick = q; nx = c0; }
-                    } else if (H::step(c, Ds[j * MS + q], m, nx)) {
-                        pick = q;
+                        nx = closed ? Din[lane] : 0u;
+                        pass = m != H::NONE && !H::gt(nx, m);
+                    } else {
+                        pass = H::step(c, Ds[j * MS + lane], m, nx);
                     }
-                    cn = nx;
                 }
-                ok = pick >= 0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                ok = bal != 0u;
                 if (!ok) break;
+                const int pick = __ffs(bal) - 1;
+                c = __shfl_sync(0xffffffffu, nx, pick);
                 seq[a] = pick;
                 S |= 1u << pick;
                 j = pick;
-                c = cn;
             }
-            if (ok && closed) c = H::fwd(c, Dout[j]);   // the return leg
-            const int *s = stops + (o_lo + t) * MS;
-            res.n = n;
-            res.status = ok ? WR_OK : WR_EINTERNAL;
-            res.m_used = 1;
-            res.cost_bits = c;
-            int64_t rank = 0;   // Lehmer rank among the n! orders
-            for (int a = 0; a < n && ok; ++a) {
-                int smaller = 0;
-                for (int b = a + 1; b < n; ++b) smaller += seq[b] < seq[a];
-                rank += smaller * fact(n - 1 - a);
+            if (lane == 0) {
+                if (ok && closed) c = H::fwd(c, Dout[j]);   // the return leg
+                const int *s = stops + (o_lo + t) * MS;
+                res.n = n;
+                res.status = ok ? WR_OK : WR_EINTERNAL;
+                res.m_used = 1;
+                res.cost_bits = c;
+                int64_t rank = 0;   // Lehmer rank among the n! orders
+                for (int a = 0; a < n && ok; ++a) {
+                    int smaller = 0;
+                    for (int b = a + 1; b < n; ++b) smaller += seq[b] < seq[a];
+                    rank += smaller * fact(n - 1 - a);
+                }
+                res.rank = rank;
+                for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[nib(R.gmap, seq[a])] : -1;
+                out[t] = res;
+                // work: forward transitions n (n-1) 2^(n-2), as many in the bound pass
+                atomicAdd(&counters[0], 2ull * (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
             }
-            res.rank = rank;
-            for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[nib(R.gmap, seq[a])] : -1;
-            out[t] = res;
-            // work: forward transitions n (n-1) 2^(n-2), as many in the bound pass
-            atomicAdd(&counters[0], 2ull * (unsigned long long)n * (n - 1) * (1ull << (n - 2)));
         }
         cl.sync();   // the table is reused by the cluster's next order
     }
