@@ -130,22 +130,53 @@ __device__ __forceinline__ uint32_t ret_leg(const uint32_t *Ds, int ns, int last
     return cost;
 }
 
-template <class C, int L, bool CL, int SH>
+// PR (branch and bound, legs known >= 0 so prefix costs never decrease): a
+// child whose prefix key already exceeds min(B, the lane's best key) holds
+// no leaf that could win (ties are kept: the test is strict), so its
+// (L-1)! leaves are skipped and only counted in the rank.
+// The bound adds the legs still to come: every unvisited stop x is entered
+// once, by a leg >= mi[x] (its cheapest incoming leg), and a closed tour
+// still returns to the depot (>= the cheapest return leg); lb = that sum.
+// int32: exact, prune iff key(prefix + lb) > bound. fp32: lb is summed and
+// reduced with round-down, and a route continuing a prefix c with k more
+// non-negative legs costs at least (c + sum)(1 - 2^-24)^k, so the test is
+// RD(RD(c + lb) * (1 - 17 * 2^-24)) > bound (k <= 16) - still exact.
+template <class C>
+__device__ __forceinline__ uint32_t bb_sub(uint32_t lb, uint32_t m) {
+    if constexpr (std::is_same<C, CostI32>::value) return lb - m;
+    return __float_as_uint(__fsub_rd(__uint_as_float(lb), __uint_as_float(m)));
+}
+template <class C>
+__device__ __forceinline__ bool bb_prune(uint32_t c, uint32_t lb, uint32_t bound_key) {
+    if constexpr (std::is_same<C, CostI32>::value) return C::key(c + lb) > bound_key;
+    const float low = __fmul_rd(__fadd_rd(__uint_as_float(c), __uint_as_float(lb)), 1.0f - 17.0f * 0x1p-24f);
+    return low > __uint_as_float(bound_key);
+}
+template <class C, int L, bool CL, int SH, bool PR>
 struct Dfs {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
-                                               Best &best, uint32_t &rank) {
+                                               Best &best, uint32_t &rank, uint32_t B, const uint32_t *mi = nullptr,
+                                               uint32_t lb = 0) {
         uint32_t rem = unused;
         while (rem) {
             const int x = __ffs(rem) - 1;
             rem &= rem - 1;
-            Dfs<C, L - 1, CL, SH>::run(Ds, ns, unused & ~(1u << x), x, C::add(cost, DSL(prev * ns + x)), best, rank);
+            const uint32_t c2 = C::add(cost, DSL(prev * ns + x));
+            uint32_t lb2 = 0;
+            if constexpr (PR) lb2 = bb_sub<C>(lb, mi[x]);
+            if (PR && bb_prune<C>(c2, lb2, min(B, best.key))) {
+                rank += c_fact[L - 1];
+                continue;
+            }
+            Dfs<C, L - 1, CL, SH, PR>::run(Ds, ns, unused & ~(1u << x), x, c2, best, rank, B, mi, lb2);
         }
     }
 };
-template <class C, bool CL, int SH>
-struct Dfs<C, 2, CL, SH> {   // two stops left, a < b: leaves (a, b) then (b, a)
+template <class C, bool CL, int SH, bool PR>
+struct Dfs<C, 2, CL, SH, PR> {   // two stops left, a < b: leaves (a, b) then (b, a)
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
-                                               Best &best, uint32_t &rank) {
+                                               Best &best, uint32_t &rank, uint32_t, const uint32_t * = nullptr,
+                                               uint32_t = 0) {
         const int a = __ffs(unused) - 1;
         const int b = __ffs(unused & (unused - 1)) - 1;
         const uint32_t cab = C::add(C::add(cost, DSL(prev * ns + a)), DSL(a * ns + b));
@@ -154,10 +185,11 @@ struct Dfs<C, 2, CL, SH> {   // two stops left, a < b: leaves (a, b) then (b, a)
         leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, cba), best, rank);
     }
 };
-template <class C, bool CL, int SH>
-struct Dfs<C, 3, CL, SH> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
+template <class C, bool CL, int SH, bool PR>
+struct Dfs<C, 3, CL, SH, PR> {   // three stops left, a < b < c: the 6 leaves in lexicographic order, straight-line
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
-                                               Best &best, uint32_t &rank) {
+                                               Best &best, uint32_t &rank, uint32_t, const uint32_t * = nullptr,
+                                               uint32_t = 0) {
         const int a = __ffs(unused) - 1;
         const uint32_t u2 = unused & (unused - 1);
         const int b = __ffs(u2) - 1;
@@ -175,31 +207,38 @@ struct Dfs<C, 3, CL, SH> {   // three stops left, a < b < c: the 6 leaves in lex
         leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, C::add(cb, DSL(b0 + a))), best, rank);   // c b a
     }
 };
-template <class C, bool CL, int SH>
-struct Dfs<C, 1, CL, SH> {
+template <class C, bool CL, int SH, bool PR>
+struct Dfs<C, 1, CL, SH, PR> {
     __device__ __forceinline__ static void run(const uint32_t *Ds, int ns, uint32_t unused, int prev, uint32_t cost,
-                                               Best &best, uint32_t &rank) {
+                                               Best &best, uint32_t &rank, uint32_t, const uint32_t * = nullptr,
+                                               uint32_t = 0) {
         const int a = __ffs(unused) - 1;
         leaf<C>(ret_leg<C, CL, SH>(Ds, ns, a, C::add(cost, DSL(prev * ns + a))), best, rank);
     }
 };
 
-template <class C, bool CL, int SH>
+template <class C, bool CL, int SH, bool PR>
 __device__ __forceinline__ void walk_subtree(int L, const uint32_t *Ds, int ns, uint32_t unused, int prev,
-                                             uint32_t cost, Best &best, uint32_t &rank) {
+                                             uint32_t cost, Best &best, uint32_t &rank, uint32_t B,
+                                             const uint32_t *mi = nullptr, uint32_t lb = 0) {
     switch (L) {
-        case 1: Dfs<C, 1, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 2: Dfs<C, 2, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 3: Dfs<C, 3, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 4: Dfs<C, 4, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 5: Dfs<C, 5, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        case 6: Dfs<C, 6, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
-        default: Dfs<C, 7, CL, SH>::run(Ds, ns, unused, prev, cost, best, rank); break;
+        case 1: Dfs<C, 1, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        case 2: Dfs<C, 2, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        case 3: Dfs<C, 3, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        case 4: Dfs<C, 4, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        case 5: Dfs<C, 5, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        case 6: Dfs<C, 6, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
+        default: Dfs<C, 7, CL, SH, PR>::run(Ds, ns, unused, prev, cost, best, rank, B, mi, lb); break;
     }
 }
 
 // One warp per work item (problem, prefix range). D submatrix staged in smem.
 constexpr int ENUM_WARPS = 8;
+// Branch and bound from this many stops (C4 exact, 11 stops: 81.5 -> 57 ms
+// per step; 6-8-stop orders enumerate faster without the bound's divergence)
+#ifndef ENUM_BB_MIN
+#define ENUM_BB_MIN 9
+#endif
 // SH = 5: dynamic shared memory holds per warp ns_max^2 elements x 32 lane
 // copies (large problems: 9-13 stops, where bank conflicts of a single copy
 // dominate); SH = 0: one copy per warp (6-8 stops: occupancy matters more).
@@ -219,6 +258,9 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
     const int ns = n + (closed ? 1 : 0);   // closed: local index n is the depot
     const uint32_t *D = Dall + (size_t)pr.order * DSTRIDE;
     uint32_t *Dw = sDyn + (size_t)warp * ns_max * ns_max * (SH ? 32 : 1);
+    bool neg = false;   // int32: a negative or INF leg (prefix costs may then decrease or wrap)
+    __shared__ uint32_t sMi[ENUM_WARPS][MS];
+    uint32_t ret_min = 0;
     // stage: lane l loads element e = l, l + 32, ...; replicated: every
     // element is then broadcast to the 32 lane copies by a shuffle
     for (int e0 = 0; e0 < ns * ns; e0 += 32) {
@@ -228,6 +270,7 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
             const int a = e / ns, b = e % ns;
             const int ia = a < n ? nib(pr.map, a) : pr.dep, ib = b < n ? nib(pr.map, b) : pr.dep;
             v = D[ia * MS + ib];
+            neg |= std::is_same<C, CostI32>::value && ((int)v < 0 || v == CostI32::INF);
         }
         if constexpr (SH) {
             const int cnt = min(32, ns * ns - e0);
@@ -238,12 +281,54 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
     }
     __syncwarp();
     const uint32_t *Ds = Dw + (SH ? lane : 0);   // element e at Ds[e << SH]
+    // branch and bound when every leg is >= 0: the bound B starts at the
+    // best of 32 nearest-neighbour routes (lane l starts at stop l % n)
+    const bool prune = n >= ENUM_BB_MIN && !__any_sync(0xffffffffu, neg);
+    uint32_t B = 0xffffffffu;
+    if (prune) {
+        uint32_t unusedb = (1u << n) - 1u, cb = 0;
+        int pv = closed ? n : -1;
+        for (int a = 0; a < n; ++a) {
+            int pick = -1;
+            uint32_t pk = 0;
+            if (a == 0) {
+                pick = lane % n;
+            } else {
+                for (int x = 0; x < n; ++x) {   // nearest unvisited, ties -> smallest index
+                    if (!((unusedb >> x) & 1u)) continue;
+                    const uint32_t k = C::key(DSL(pv * ns + x));
+                    if (pick < 0 || k < pk) { pick = x; pk = k; }
+                }
+            }
+            if (pv >= 0) cb = C::add(cb, DSL(pv * ns + pick));
+            unusedb &= ~(1u << pick);
+            pv = pick;
+        }
+        if (closed) cb = C::add(cb, DSL(pv * ns + n));
+        B = __reduce_min_sync(0xffffffffu, C::key(cb));
+        {   // cheapest incoming leg per stop, cheapest return (int32 and fp32 >= 0: min of the bits)
+            if (lane < n) {
+                uint32_t m = 0xffffffffu;
+                for (int y = 0; y < n; ++y)
+                    if (y != lane) m = min(m, C::key(DSL(y * ns + lane)));
+                sMi[warp][lane] = C::unkey(m);
+            }
+            uint32_t r = 0xffffffffu;
+            if (closed && lane < n) r = C::key(DSL(lane * ns + n));
+            ret_min = closed ? C::unkey(__reduce_min_sync(0xffffffffu, r)) : 0u;
+            __syncwarp();
+        }
+    }
     const int p = prefix_depth(n);
     const int L = n - p;
     const uint32_t sub = c_fact[L];
     const uint32_t div0 = c_fact[n - 1] / sub;   // prefixes per first-element choice
     Best best{0xffffffffu, 0xffffffffu};
-    for (int q = item.prefix_lo + lane; q < item.prefix_hi; q += 32) {
+    for (int q0 = item.prefix_lo; q0 < item.prefix_hi; q0 += 32) {
+        if (prune)   // share the lanes' best keys (all lanes reach this point together)
+            B = min(B, __reduce_min_sync(0xffffffffu, best.key));
+        const int q = q0 + lane;
+        if (q >= item.prefix_hi) continue;
         // decode prefix q (mixed radix n, n-1, ..., n-p+1), lexicographic
         uint32_t unused = (1u << n) - 1u;
         uint32_t rem = (uint32_t)q, div = div0;
@@ -261,8 +346,23 @@ __global__ void __launch_bounds__(ENUM_WARPS * 32) route_enum_kernel(const Route
             prev = x;
         }
         uint32_t rank = (uint32_t)q * sub;
-        if (closed) walk_subtree<C, true, SH>(L, Ds, ns, unused, prev, cost, best, rank);
-        else walk_subtree<C, false, SH>(L, Ds, ns, unused, prev, cost, best, rank);
+        uint32_t lb = 0;
+        if (prune) {
+            lb = ret_min;
+            for (uint32_t u2 = unused; u2; u2 &= u2 - 1) {
+                const uint32_t m = sMi[warp][__ffs(u2) - 1];
+                if constexpr (std::is_same<C, CostI32>::value) lb += m;
+                else lb = __float_as_uint(__fadd_rd(__uint_as_float(lb), __uint_as_float(m)));
+            }
+        }
+        if (prune && bb_prune<C>(cost, lb, min(B, best.key))) continue;   // the whole subtree
+        if (prune) {
+            if (closed) walk_subtree<C, true, SH, true>(L, Ds, ns, unused, prev, cost, best, rank, B, sMi[warp], lb);
+            else walk_subtree<C, false, SH, true>(L, Ds, ns, unused, prev, cost, best, rank, B, sMi[warp], lb);
+        } else {
+            if (closed) walk_subtree<C, true, SH, false>(L, Ds, ns, unused, prev, cost, best, rank, B);
+            else walk_subtree<C, false, SH, false>(L, Ds, ns, unused, prev, cost, best, rank, B);
+        }
     }
     uint64_t packed = ((uint64_t)best.key << 32) | best.rank;
 #pragma unroll
