@@ -32,6 +32,13 @@ namespace wr {
 
 constexpr int MS = WR_MAX_STOPS;      // 16
 constexpr int DSTRIDE = MS * MS;      // D entries per order (row-major 16 x 16)
+// exact routes of SHK_MIN..SHK_MAX stops go to the warp Held-Karp kernel
+#ifndef SHK_MIN
+#define SHK_MIN 8
+#endif
+#ifndef SHK_MAX
+#define SHK_MAX 8
+#endif
 
 // ------------------------------------------------------------ cost ops --
 // Route costs: int32 exact (with negatives possible when D < 0), fp32 RN.
@@ -654,7 +661,8 @@ template <class C>
 __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, const int *stops, int64_t o_lo,
                                      int64_t nord, const uint32_t *Dall, int m, const int *xy,
                                      const int *labels_in, int64_t chunk, OrderRoute *ordr, int *prob_cnt,
-                                     int *item_cnt, int pairs, int *hk_count, int *hk_list, const int *dep_info) {
+                                     int *item_cnt, int pairs, int *hk_count, int *hk_list, const int *dep_info,
+                                     int *shk_list) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nord) return;
     const int64_t o = o_lo + t;
@@ -720,6 +728,13 @@ __global__ void route_prepare_kernel(const int *n_arr, const int *status_in, con
                 const int k = seg_of[a];
                 R.segmap[k] |= (uint64_t)gs[a] << (4 * R.seglen[k]);
                 R.seglen[k]++;
+            }
+            if (nseg == 1 && ng >= SHK_MIN && ng <= SHK_MAX && shk_list) {
+                // exact route of an 8-stop order: warp Held-Karp (route_hk_small_kernel)
+                R.hk = 2;
+                R.noenum = 1;
+                nseg = 0;
+                shk_list[atomicAdd(hk_count + 4, 1)] = (int)t;
             }
             if (nseg == 1 && ng > WR_MAX_EXACT) {
                 // exact route of 13-16 stops: Held-Karp subset DP (NEXT-2)
@@ -822,7 +837,7 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         return;
     }
     if (pairs && R.mseg >= 2) return;   // route_pairs_kernel writes these orders
-    if (R.hk) return;                   // route_hk_kernel writes these orders
+    if (R.hk) return;                   // route_hk_kernel / route_hk_small_kernel write these orders
     const int dep = R.dep;              // closed tour (NEXT-4): the depot's stop index, else -1
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     uint32_t *Ds = sD[warp];
@@ -1128,8 +1143,8 @@ __global__ void __launch_bounds__(PAIRS_THREADS) route_pairs_kernel(int64_t nord
 constexpr int HK_THREADS = 512;
 constexpr int HK_CL = 8;            // CTAs per cluster (one order each)
 constexpr int HK_CLUSTERS = 18;     // clusters in flight: 144 SMs, 72 MB of tables
-constexpr int HK_MIN = WR_MAX_EXACT + 1;
 constexpr int HK_MAX = WR_MAX_STOPS;
+constexpr int LIST_MIN = 7;          // popcount-sorted subset lists are kept for n = 7..16
 constexpr int HK_RS = 16;           // workspace row stride (states of one S)
 
 // fp32: max{c >= 0 : fl(c + d) <= m} exactly (RN-even), -1 if none. fl(x) <=
@@ -1192,9 +1207,9 @@ struct HkOps<CostF32> {    // fp32 >= 0; NONE = -1.0f
     }
 };
 
-struct HkLists {           // subsets of [0, n) sorted by popcount, n = 13..16
+struct HkLists {           // subsets of [0, n) sorted by popcount, n = LIST_MIN..16
     const uint16_t *sets;  // concatenated lists
-    int off[HK_MAX - HK_MIN + 1][HK_MAX + 2];   // [n - HK_MIN][k] start of popcount k
+    int off[HK_MAX - LIST_MIN + 1][HK_MAX + 2];   // [n - LIST_MIN][k] start of popcount k
 };
 
 template <class C>
@@ -1246,7 +1261,7 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
             if (leg_slow(Din[tid]) || leg_slow(Dout[tid])) s_slow = 1;
         }
         const uint16_t *sets = L.sets;
-        const int *off = L.off[n - HK_MIN];
+        const int *off = L.off[n - LIST_MIN];
         __syncthreads();
         const bool fast = std::is_same<C, CostI32>::value && !s_slow;   // same in every CTA of the cluster
         // F({j}, j) = 0, or the depot leg of a closed tour
@@ -1418,8 +1433,152 @@ __global__ void __cluster_dims__(HK_CL, 1, 1) __launch_bounds__(HK_THREADS)
     }
 }
 
-// The popcount-sorted subset lists for n = 13..16 (host-built once per
-// device; 240 KB).
+// Exact routes of SHK_MIN..SHK_MAX stops (default 8) by the same three
+// passes as route_hk_kernel (forward DP, backward bound, lexicographic
+// greedy: O5's answer, reading R2), one warp per order with its table in
+// shared memory (2^n x 8 words). An 8-stop order costs n 2^(n-1) = 1,024
+// states per pass here against 8! = 40,320 enumerated leaves; at 7 stops and
+// below enumeration is as cheap, so those stay with route_enum_kernel.
+static_assert(SHK_MIN >= LIST_MIN && SHK_MAX <= 8, "warp Held-Karp: 7 <= n <= 8");
+constexpr int SHK_WARPS = 8;
+constexpr int SHK_RS = 8;   // table row stride (n <= 8)
+constexpr size_t SHK_SMEM = (size_t)SHK_WARPS * ((1u << SHK_MAX) * SHK_RS + 64 + 16) * sizeof(uint32_t);
+
+template <class C>
+__global__ void __launch_bounds__(SHK_WARPS * 32)
+    route_hk_small_kernel(const int *__restrict__ list, int nlist, const OrderRoute *ordr, const uint32_t *Dall,
+                          const int *stops, int64_t o_lo, wr_route_result *out, unsigned long long *counters,
+                          HkLists L) {
+    using H = HkOps<C>;
+    extern __shared__ uint32_t shk[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * SHK_WARPS + warp;
+    if (i >= nlist) return;
+    uint32_t *W = shk + (size_t)warp * ((1u << SHK_MAX) * SHK_RS + 64 + 16);
+    uint32_t *Ds = W + (1u << SHK_MAX) * SHK_RS;   // [a * 8 + b]
+    uint32_t *Din = Ds + 64, *Dout = Din + 8;
+    const int t = list[i];
+    const OrderRoute R = ordr[t];
+    const int n = R.ng;
+    const bool closed = R.dep >= 0;
+    const uint32_t *D = Dall + (size_t)t * DSTRIDE;
+    for (int e = lane; e < 64; e += 32) {
+        const int a = e >> 3, b = e & 7;
+        Ds[e] = (a < n && b < n) ? D[nib(R.gmap, a) * MS + nib(R.gmap, b)] : 0u;
+    }
+    if (closed && lane < n) {
+        Din[lane] = D[R.dep * MS + nib(R.gmap, lane)];
+        Dout[lane] = D[nib(R.gmap, lane) * MS + R.dep];
+    }
+    __syncwarp();
+    const uint16_t *sets = L.sets;
+    const int *off = L.off[n - LIST_MIN];
+    if (lane < n) W[(1u << lane) * SHK_RS + lane] = closed ? Din[lane] : 0u;
+    __syncwarp();
+    // 1. forward: F(S, j) = min over i in S - j of fl(F(S - j, i) + D[i][j])
+    for (int k = 2; k <= n; ++k) {
+        const int base = off[k], items = (off[k + 1] - base) * k;
+        for (int x = lane; x < items; x += 32) {
+            const int sidx = x / k, b = x - sidx * k;
+            const uint32_t S = sets[base + sidx];
+            const int j = __fns(S, 0, b + 1);
+            const uint32_t P = S & ~(1u << j);
+            uint32_t best = 0xffffffffu;
+            for (uint32_t q = P; q; q &= q - 1) {
+                const int a = __ffs(q) - 1;
+                best = min(best, C::key(H::fwd(W[P * SHK_RS + a], Ds[a * 8 + j])));
+            }
+            W[S * SHK_RS + j] = C::unkey(best);
+        }
+        __syncwarp();
+    }
+    const uint32_t F = (1u << n) - 1u;
+    uint32_t ck = 0xffffffffu;
+    if (lane < n) {
+        const uint32_t f = W[F * SHK_RS + lane];
+        ck = C::key(closed ? H::fwd(f, Dout[lane]) : f);
+    }
+    const uint32_t cstar = C::unkey(__reduce_min_sync(0xffffffffu, ck));
+    const int *s = stops + (o_lo + t) * MS;
+    wr_route_result res;
+    if (cstar == C::INF) {   // every order costs INF: O5 keeps the identity (rank 0)
+        if (lane == 0) {
+            res.n = n;
+            res.status = WR_OK;
+            res.m_used = 1;
+            res.cost_bits = C::INF;
+            res.rank = 0;
+            for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[nib(R.gmap, a)] : -1;
+            out[t] = res;
+        }
+        return;
+    }
+    // 2. backward bound M(S, j), written over F layer by layer
+    __syncwarp();
+    if (lane < n) W[F * SHK_RS + lane] = closed ? H::inv(Dout[lane], cstar) : cstar;
+    __syncwarp();
+    for (int k = n - 1; k >= 1; --k) {
+        const int base = off[k], items = (off[k + 1] - base) * k;
+        for (int x = lane; x < items; x += 32) {
+            const int sidx = x / k, b = x - sidx * k;
+            const uint32_t S = sets[base + sidx];
+            const int j = __fns(S, 0, b + 1);
+            uint32_t best = H::NONE;
+            for (uint32_t q = F & ~S; q; q &= q - 1) {
+                const int a = __ffs(q) - 1;
+                const uint32_t c = H::inv(Ds[j * 8 + a], W[(S | (1u << a)) * SHK_RS + a]);
+                if (H::gt(c, best)) best = c;
+            }
+            W[S * SHK_RS + j] = best;
+        }
+        __syncwarp();
+    }
+    // 3. lexicographic greedy: lane q tests stop q, the smallest passing lane wins
+    uint32_t Sv = 0, c = 0;
+    int j = -1, seq[MS];
+    bool ok = true;
+    for (int a = 0; a < n && ok; ++a) {
+        bool pass = false;
+        uint32_t nx = 0;
+        if (lane < n && !((Sv >> lane) & 1u)) {
+            const uint32_t m = W[(Sv | (1u << lane)) * SHK_RS + lane];
+            if (a == 0) {
+                nx = closed ? Din[lane] : 0u;
+                pass = m != H::NONE && !H::gt(nx, m);
+            } else {
+                pass = H::step(c, Ds[j * 8 + lane], m, nx);
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+        ok = bal != 0u;
+        if (!ok) break;
+        const int pick = __ffs(bal) - 1;
+        c = __shfl_sync(0xffffffffu, nx, pick);
+        seq[a] = pick;
+        Sv |= 1u << pick;
+        j = pick;
+    }
+    if (lane == 0) {
+        if (ok && closed) c = H::fwd(c, Dout[j]);   // the return leg
+        res.n = n;
+        res.status = ok ? WR_OK : WR_EINTERNAL;
+        res.m_used = 1;
+        res.cost_bits = c;
+        int64_t rank = 0;   // Lehmer rank among the n! orders
+        for (int a = 0; a < n && ok; ++a) {
+            int smaller = 0;
+            for (int b = a + 1; b < n; ++b) smaller += seq[b] < seq[a];
+            rank += smaller * fact(n - 1 - a);
+        }
+        res.rank = rank;
+        for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[nib(R.gmap, seq[a])] : -1;
+        out[t] = res;
+        atomicAdd(&counters[0], (unsigned long long)fact(n));   // routes covered, as enumeration counts them
+    }
+}
+
+// The popcount-sorted subset lists for n = 7..16 (host-built once per
+// device; 256 KB).
 static HkLists hk_lists(int device) {
     static std::vector<std::pair<int, HkLists>> cache;
     static std::vector<DBuf<uint16_t>> keep;
@@ -1427,8 +1586,8 @@ static HkLists hk_lists(int device) {
         if (e.first == device) return e.second;
     HkLists L{};
     std::vector<uint16_t> all;
-    for (int n = HK_MIN; n <= HK_MAX; ++n) {
-        int *off = L.off[n - HK_MIN];
+    for (int n = LIST_MIN; n <= HK_MAX; ++n) {
+        int *off = L.off[n - LIST_MIN];
         for (int k = 0; k <= n; ++k) {
             off[k] = (int)all.size();
             for (uint32_t S = 0; S < (1u << n); ++S)
@@ -1935,22 +2094,22 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     NvtxRange nv("wr.routes");
     const int *xy = P.g->xy.p;
     DBuf<OrderRoute> ordr(nord);
-    DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(4), hk_list(nord);
+    DBuf<int> pcnt(nord + 1), icnt(nord + 1), hk_ctr(8), hk_list(nord), shk_list(nord);
     WR_CUDA(cudaMemsetAsync(pcnt.p + nord, 0, 4, st));
     WR_CUDA(cudaMemsetAsync(icnt.p + nord, 0, 4, st));
-    WR_CUDA(cudaMemsetAsync(hk_ctr.p, 0, 16, st));
+    WR_CUDA(cudaMemsetAsync(hk_ctr.p, 0, 32, st));
     route_prepare_kernel<C><<<gridn(nord, 128), 128, 0, st>>>(
         P.n_arr.p, P.status.p, P.stops.p, o_lo, nord, Dall, P.m, xy,
         P.labels.p ? P.labels.p + o_lo * WR_MAX_STOPS : nullptr, P.chunk, ordr.p, pcnt.p, icnt.p, P.pairs,
-        hk_ctr.p, hk_list.p, P.closed ? P.dep_info.p : nullptr);
+        hk_ctr.p, hk_list.p, P.closed ? P.dep_info.p : nullptr, shk_list.p);
     count_launch();
     WR_LAUNCH_CHECK();
     scan_exclusive_i32(pcnt.p, pcnt.p, (int)(nord + 1), st);
     scan_exclusive_i32(icnt.p, icnt.p, (int)(nord + 1), st);
-    int nprob = 0, nitems = 0, hkc[4] = {0, 0, 0, 0};
+    int nprob = 0, nitems = 0, hkc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     WR_CUDA(cudaMemcpyAsync(&nprob, pcnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaMemcpyAsync(&nitems, icnt.p + nord, 4, cudaMemcpyDeviceToHost, st));
-    WR_CUDA(cudaMemcpyAsync(hkc, hk_ctr.p, 16, cudaMemcpyDeviceToHost, st));
+    WR_CUDA(cudaMemcpyAsync(hkc, hk_ctr.p, 32, cudaMemcpyDeviceToHost, st));
     WR_CUDA(cudaStreamSynchronize(st));
     const int nhk = hkc[0];
     DBuf<RouteProblem> probs(std::max(nprob, 1));
@@ -1987,6 +2146,18 @@ static void route_block(const Plan &P, const uint32_t *Dall, int64_t o_lo, int64
     if (P.pairs) {
         route_pairs_kernel<C><<<(unsigned)nord, PAIRS_THREADS, 0, st>>>(nord, ordr.p, Dall, P.stops.p, o_lo, d_res,
                                                                       d_counters);
+        count_launch();
+        WR_LAUNCH_CHECK();
+    }
+    if (hkc[4] > 0) {   // 8-stop exact routes: warp Held-Karp
+        static bool attr = false;
+        if (!attr) {
+            WR_CUDA(cudaFuncSetAttribute(route_hk_small_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SHK_SMEM));
+            attr = true;
+        }
+        route_hk_small_kernel<C><<<gridn(hkc[4], SHK_WARPS), SHK_WARPS * 32, SHK_SMEM, st>>>(
+            shk_list.p, hkc[4], ordr.p, Dall, P.stops.p, o_lo, d_res, d_counters, hk_lists(P.device));
         count_launch();
         WR_LAUNCH_CHECK();
     }

@@ -406,6 +406,37 @@ def test_route_orders_held_karp_int_paths(case):
     assert (res["n"] >= 13).all()
 
 
+@pytest.mark.parametrize("wtype", ["i32", "f32"])
+def test_route_orders_branch_and_bound_ties(wtype):
+    """Exact enumeration with branch and bound (>= 9 stops, legs >= 0): on a
+    graph where many or all routes tie (unit / zero weights) the strict bound
+    test must keep O5's lexicographically smallest optimum; a random graph
+    with a negative leg takes the unpruned path."""
+    rng = np.random.default_rng(97)
+    V = 24
+    src, dst, w = [], [], []
+    for a in range(V):
+        for b in range(V):
+            if a != b:
+                src.append(a); dst.append(b)
+                w.append(1 if (a + b) % 3 else (0 if wtype == "f32" else 2))
+    dt = np.int32 if wtype == "i32" else np.float32
+    g = G(V, src, dst, np.array(w, dt), xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+    sizes = [9, 10, 9, 10, 9]
+    seqs = [np.sort(rng.choice(V, k, replace=False)) for k in sizes]
+
+    class O:
+        pass
+    orders = O()
+    orders.order_ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    orders.order_nodes = np.concatenate(seqs).astype(np.int32)
+    orders.B = len(sizes)
+    compare_orders(g, orders, m=1)
+    if wtype == "i32":   # one negative arc (no negative cycle): no pruning, same answers
+        g2 = G(V, src, dst, np.array([x if i else -1 for i, x in enumerate(w)], np.int32), xy=g.xy)
+        compare_orders(g2, orders, m=1)
+
+
 def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
     G = G or wr.Graph.from_gen(g)
     res, st = wr.route_orders(G, orders.order_ptr, orders.order_nodes, m=m, chunk=chunk, flags=flags) \
