@@ -325,7 +325,7 @@ __device__ __forceinline__ Vec<SPL> relax_vertex(const DevGraph &g, const uint32
 // Task-queue capacity per vertex: per-warp queues of 32 x QC packed (u, w)
 // pairs after the bitmaps in dynamic shared memory.
 #ifndef WR_QCAP
-#define WR_QCAP 16
+#define WR_QCAP 12   // C5's in-degree is <= 10; more changed in-arcs take relax_vertex
 #endif
 constexpr int QCAP = WR_QCAP;
 #ifndef WR_AQ
@@ -357,7 +357,7 @@ __device__ __forceinline__ void nf_append(NfState &nf, int which, int w, int NW)
 template <class Op, bool DELTA, int SPL, int QC, int VB, int TPS, bool LIST, bool NF = false>
 __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__restrict__ R, int w, uint32_t m,
                                                int lane, unsigned long long &relax, const ChgView pchg,
-                                               uint32_t *nxt, int *nlist, int *nlen, int2 *q,
+                                               uint32_t *nxt, uint16_t *nlist, int *nlen, int2 *q,
                                                uint32_t *touched, bool &ovf, uint32_t thr2,
                                                NfState *nfp = nullptr) {
     constexpr int TSW = 32 * SPL;
@@ -539,7 +539,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
         for (int e = o0; e < o1; ++e) {
             const int x = g.out_dst[e];
             if (LIST) {
-                if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u) nlist[atomicAdd(nlen, 1)] = x >> 5;
+                if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u) nlist[atomicAdd(nlen, 1)] = (uint16_t)(x >> 5);
             } else {
                 atomicOr(&nxt[x >> 5], 1u << (x & 31));
             }
@@ -555,7 +555,7 @@ __device__ __forceinline__ uint32_t relax_word(const DevGraph &g, uint32_t *__re
 //              of this round's improvements), swapped each round;
 //   touched    vertices whose row has been written (lazy rows);
 //   chg[2]     round-stamped change words (ChgView), by round parity;
-//   list[2]    the non-zero words of cur / nxt, so a round visits only its
+//   list[2]    the non-zero words of cur / nxt (16-bit word indices), so a round visits only its
 //              candidate words, handed out to warps dynamically (one shared
 //              counter per round) - no scan over all V/32 words and no
 //              static word-to-warp split that leaves warps idle at the
@@ -574,8 +574,8 @@ __host__ __device__ constexpr FrontierSmem frontier_smem(int NW, int nwarps, int
                         (size_t)2 * NW,
                         ((size_t)3 * NW + 1) & ~(size_t)1,
                         (((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)4 * NW,
-                        ((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 3) & ~(size_t)3,
-                        (((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)6 * NW + 3) & ~(size_t)3) +
+                        ((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)5 * NW + 3) & ~(size_t)3,
+                        (((((size_t)3 * NW + 1) & ~(size_t)1) + (size_t)5 * NW + 3) & ~(size_t)3) +
                             (size_t)nwarps * 32 * QC * 2};
 }
 
@@ -596,8 +596,13 @@ struct SkewStage {
     static constexpr int RS = TS + TS / 32 + 1;
     __device__ static int at(int s) { return s + (s >> 5); }
 };
-template <int SPL>
-using KeyedStage = SkewStage<64 * SPL>;
+// keyed pred jobs stage in-arc indices, not vertex ids: per vertex one word
+// per lane holding its 2 SPL slots' 4-bit indices, plus the vertex's in-arc
+// tails (<= 16) - 48 words per vertex instead of 265, which keeps the fused
+// kernel's shared memory (and so its L1 carveout) at the frontier's size
+struct KeyedStage {
+    static constexpr int WORDS = 32 + 16;   // per vertex: packed indices, tails
+};
 template <int SPL>
 __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__restrict__ tile_src,
                                                const uint32_t *__restrict__ rows, const int *__restrict__ slot_row,
@@ -628,7 +633,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
     const FrontierSmem L = frontier_smem(NW, NWARPS, QC);
     uint32_t *const touched = smem + L.touched;
     uint2 *const chg = reinterpret_cast<uint2 *>(smem + L.chg);
-    int *const list = reinterpret_cast<int *>(smem + L.list);
+    uint16_t *const list = reinterpret_cast<uint16_t *>(smem + L.list);   // NW < 2^16 (launch_shape)
     int2 *const q = reinterpret_cast<int2 *>(smem + L.queue) + warp * (32 * QC);
     const int NWB = (NW + 31) >> 5;
     NfState nf{};
@@ -694,7 +699,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                     atomicOr(&touched[s >> 5], 1u << (s & 31));
                     for (int e = g.out_ptr[s]; e < g.out_ptr[s + 1]; ++e) {
                         const int x = g.out_dst[e];
-                        if (atomicOr(&cur[x >> 5], 1u << (x & 31)) == 0u) list[NW + atomicAdd(&s_len[1], 1)] = x >> 5;
+                        if (atomicOr(&cur[x >> 5], 1u << (x & 31)) == 0u) list[NW + atomicAdd(&s_len[1], 1)] = (uint16_t)(x >> 5);
                     }
                 }
             }
@@ -734,8 +739,8 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             } else {
                 // ---- relax the candidate words of list r&1, claimed one at a
                 // time; improvements append to list (r+1)&1
-                const int *lc = list + (r & 1) * NW;
-                int *ln = list + ((r + 1) & 1) * NW;
+                const uint16_t *lc = list + (r & 1) * NW;
+                uint16_t *ln = list + ((r + 1) & 1) * NW;
                 const int len = s_len[r % 3];
                 int *const nlen = &s_len[(r + 1) % 3];
                 if (threadIdx.x == 0) s_len[(r + 2) % 3] = s_head[(r + 2) % 3] = 0;   // used in round r-1
@@ -760,7 +765,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             bool nf_released = false;
             if constexpr (NF) {
                 uint2 *cc = chg + (r & 1) * NW;
-                int *ln = LIST ? list + ((r + 1) & 1) * NW : nullptr;
+                uint16_t *ln = LIST ? list + ((r + 1) & 1) * NW : nullptr;
                 int *const nlen = LIST ? &s_len[(r + 1) % 3] : nullptr;
                 // near-far release: deferred vertices whose key is <= T
                     // now propagate as if they had changed in round r (change
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
                             if (rel) {   // mark the out-neighbours for round r+1
                                 for (int e2 = g.out_ptr[v]; e2 < g.out_ptr[v + 1]; ++e2) {
                                     const int x = g.out_dst[e2];
-                                    if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u && LIST) ln[atomicAdd(nlen, 1)] = x >> 5;
+                                    if (atomicOr(&nxt[x >> 5], 1u << (x & 31)) == 0u && LIST) ln[atomicAdd(nlen, 1)] = (uint16_t)(x >> 5);
                                 }
                             }
                             const uint32_t kk = __reduce_min_sync(FULL, ((keep >> lane) & 1u) ? key : 0xffffffffu);
@@ -921,7 +926,7 @@ __global__ void __launch_bounds__(NT, MINB) bf_frontier_kernel(DevGraph g, const
             if constexpr (Op::KEYED)
                 pred_job_keyed<SPL>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, t,
                                     (int)(j % chunks) * PV,
-                                    reinterpret_cast<int32_t *>(smem) + warp * PV * KeyedStage<SPL>::RS, lane,
+                                    reinterpret_cast<int32_t *>(smem) + warp * PV * KeyedStage::WORDS, lane,
                                     thr2 & 0xffffu, &stats->overflow, srow_cache, srow_tile);
             else
                 pred_job<Op, SPL, FPA>(g, tile_src, rows, slot_row, fuse.out_row0, fuse.pred_out, fuse.flat_tiles, t,
@@ -948,11 +953,13 @@ template <class Op, bool DENSE, int NT, int MINB, int SPL, int QC = QCAP, bool L
 static bool launch_shape(const wr_graph *g, const BfRun &run, BfTileStats *d_stats, cudaStream_t st) {
     auto kern = bf_frontier_kernel<Op, DENSE, NT, MINB, SPL, QC, VB, TPS, LIST && !DENSE, NF>;
     const int NW = (g->V + 31) / 32;
+    if (NW > 65535) return false;   // 16-bit word lists
     size_t smem = frontier_smem(NW, NT / 32, QC).words * sizeof(uint32_t);
     if (NF) smem += (size_t)(NW + 2 * ((NW + 31) / 32)) * sizeof(uint32_t);   // deferred bitmap + inlist bitmaps
     if (run.fuse.pred_out)   // the fused pred jobs' staging rows reuse it
         smem = std::max(smem, (size_t)(NT / 32) * PredShape::PV *
-                                  SkewStage<32 * SPL * Op::PACK>::RS * sizeof(int32_t));
+                                  (Op::KEYED ? KeyedStage::WORDS : SkewStage<32 * SPL * Op::PACK>::RS) *
+                                  sizeof(int32_t));
     smem += (size_t)env_int("WR_SMEM_PAD", 0);   // experiment knob: less L1 (carveout study)
     int max_optin = 0;
     WR_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
@@ -1512,11 +1519,12 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
                                                int64_t out_row0, int32_t *__restrict__ pred_out, int tile, int c0,
                                                int32_t *spw, int lane, uint32_t thr, int *overflow,
                                                int (&srow)[2 * SPL], int &srow_tile) {
-    using KS = KeyedStage<SPL>;
     constexpr int TSW = 32 * SPL;
     constexpr int TS = TSW * 2;
-    constexpr int NS = SPL * 2;
+    constexpr int NS = SPL * 2;    // slots per lane (<= 8 nibbles)
     constexpr int PV = PredShape::PV;
+    uint32_t *const kidx = reinterpret_cast<uint32_t *>(spw);   // [PV][32] packed in-arc indices
+    int32_t *const tails_s = spw + PV * 32;                      // [PV][16] in-arc tails
     const int V = g.V;
     const uint32_t *Rl = rows + (size_t)tile * V * TSW + lane * SPL;
     const int nv = min(PV, V - c0);
@@ -1529,26 +1537,25 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
 #pragma unroll
     for (int jv = 0; jv < PV; jv += 2) {
         if (jv >= nv) break;
-        // the in-arc tails of vertices jv (lanes 0-15) and jv + 1 (16-31) in
-        // registers (in-degree <= 15): a slot's pred is one shuffle away
+        // the in-arc tails of vertices jv (lanes 0-15) and jv + 1 (16-31)
         const int half = lane >> 4, vj = min(jv + half, nv - 1);
         const int lo = __shfl_sync(FULL, a_lane, vj), hi = __shfl_sync(FULL, a_lane, vj + 1);
-        const int tails = (lane & 15) < hi - lo ? g.in_src[lo + (lane & 15)] : -1;
+        tails_s[(jv + half) * 16 + (lane & 15)] = (lane & 15) < hi - lo ? g.in_src[lo + (lane & 15)] : -1;
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
             if (jv + d >= nv) break;
+            uint32_t packed = 0;
 #pragma unroll
             for (int j = 0; j < SPL; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t key1 = (key[jv + d].x[j] >> (16 * h)) & 0xffffu;
-                    const uint32_t k = key1 & 0xfu;
                     // range check of the keyed rows (the sweep skips it): a stored
                     // distance at or past 0x7ff - max_w may hide a clipped path
                     ovf |= key1 >= thr && key1 != 0x7fffu;
-                    const int u = __shfl_sync(FULL, tails, 16 * d + (int)(k & 15u));
-                    spw[(jv + d) * KS::RS + KS::at(lane * NS + j * 2 + h)] = k == 15u ? -1 : u;
+                    packed |= (key1 & 0xfu) << (4 * (j * 2 + h));
                 }
+            kidx[(jv + d) * 32 + lane] = packed;
         }
     }
     if (__any_sync(FULL, ovf) && lane == 0) atomicOr(overflow, 1);
@@ -1562,18 +1569,23 @@ __device__ __forceinline__ void pred_job_keyed(const DevGraph &g, const int *__r
         }
         srow_tile = tile;
     }
+    // pred of (vertex jv, slot sl) = tail number k of vertex jv, k = 15: none
+    const auto pred_of = [&](int jv, int sl) {
+        const uint32_t k = (kidx[jv * 32 + sl / NS] >> (4 * (sl % NS))) & 0xfu;
+        return k == 15u ? -1 : tails_s[jv * 16 + k];
+    };
 #pragma unroll
     for (int k = 0; k < TS / 32; ++k) {
         if (srow[k] < 0) continue;
         const int sl_in = lane + 32 * k;
         int32_t *dst = pred_out + (out_row0 + srow[k]) * (int64_t)V + c0;
         if (vec) {
-            const int a = KS::at(sl_in);
-            reinterpret_cast<int4 *>(dst)[0] = make_int4(spw[a], spw[KS::RS + a], spw[2 * KS::RS + a], spw[3 * KS::RS + a]);
+            reinterpret_cast<int4 *>(dst)[0] =
+                make_int4(pred_of(0, sl_in), pred_of(1, sl_in), pred_of(2, sl_in), pred_of(3, sl_in));
             reinterpret_cast<int4 *>(dst)[1] =
-                make_int4(spw[4 * KS::RS + a], spw[5 * KS::RS + a], spw[6 * KS::RS + a], spw[7 * KS::RS + a]);
+                make_int4(pred_of(4, sl_in), pred_of(5, sl_in), pred_of(6, sl_in), pred_of(7, sl_in));
         } else {
-            for (int jv = 0; jv < nv; ++jv) dst[jv] = spw[jv * KS::RS + KS::at(sl_in)];
+            for (int jv = 0; jv < nv; ++jv) dst[jv] = pred_of(jv, sl_in);
         }
     }
     __syncwarp();   // spw is reused by the warp's next job
