@@ -175,6 +175,25 @@ def test_bf_negative_weights_depth_v_minus_1():
         assert e.value.code == wr.WR_ENEGCYCLE
 
 
+def test_bf_long_path_stamp_restamp():
+    """A 70,000-vertex path needs ~70k rounds from an end: the sweep's 16-bit
+    change stamps are restamped every 2^15 rounds and wrap at 2^16, and the
+    distances / preds / routes must still equal the oracle's."""
+    V = 70000
+    a = np.arange(V - 1, dtype=np.int32)
+    g = G(V, np.concatenate([a, a + 1]), np.concatenate([a + 1, a]), np.ones(2 * (V - 1), np.int32),
+          xy=np.stack([np.arange(V), np.zeros(V)], 1).astype(np.int32))
+    check_bf(g, np.array([0, 5, 40000], np.int32))
+    Gp = wr.Graph(g.V, g.src, g.dst, g.w, xy=g.xy)
+
+    class O:
+        pass
+    orders = O()
+    nodes = np.array([0, 69999, 3, 65540, 32770, 7, 65536, 32768, 1], np.int32)
+    orders.order_ptr, orders.order_nodes, orders.B = np.array([0, 2, 5, 9], np.int64), nodes, 3
+    compare_orders(g, orders, m=1, G=Gp)
+
+
 def test_bf_targets_repeats_and_device_outputs():
     g = gen.config(3, wtype="f32")[0]
     rng = np.random.default_rng(1)
