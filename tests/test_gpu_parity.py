@@ -175,6 +175,18 @@ def test_bf_negative_weights_depth_v_minus_1():
         assert e.value.code == wr.WR_ENEGCYCLE
 
 
+def test_bf_flat_competing_predecessors():
+    """The hand-derived O3 flat-rule fixtures of test_oracle_bf (competing
+    tight tails with equal and different hop counts; steep beats flat) on
+    the GPU: all sources, dist and pred equal to the oracle."""
+    g = G(5, [0, 0, 1, 1, 2, 2, 3], [1, 2, 2, 3, 3, 4, 4], np.zeros(7, dtype=np.int32))
+    check_bf(g, np.arange(5, dtype=np.int32))
+    g2 = G(4, [0, 0, 2, 1, 2], [1, 2, 1, 3, 3], np.array([2, 1, 1, 0, 1], dtype=np.int32))
+    check_bf(g2, np.arange(4, dtype=np.int32))
+    g3 = G(5, [0, 0, 1, 1, 2, 2, 3], [1, 2, 2, 3, 3, 4, 4], np.zeros(7, dtype=np.float32))
+    check_bf(g3, np.arange(5, dtype=np.int32))
+
+
 def test_bf_long_path_stamp_restamp():
     """A 70,000-vertex path needs ~70k rounds from an end: the sweep's 16-bit
     change stamps are restamped every 2^15 rounds and wrap at 2^16, and the

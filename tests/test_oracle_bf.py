@@ -341,6 +341,26 @@ def test_pred_flat_zero_weight_cycle():
     assert p.tolist() == [-1, 0, 1, 2]
 
 
+def test_pred_flat_competing_predecessors_hand_derived():
+    """O3's flat rule with competing tight predecessors, derived by hand.
+    All-zero graph from s = 0: arcs 0->1, 0->2, 1->2, 1->3, 2->3, 2->4, 3->4.
+    Every arc is tight and none is steep (d = 0 everywhere); hop over tight
+    arcs: hop = [0, 1, 1, 2, 2]. pred[2]: tails 0 (hop 0), 1 (hop 1) -> 0;
+    pred[3]: tails 1, 2 (both hop 1) -> the smaller, 1; pred[4]: tails 2
+    (hop 1), 3 (hop 2) -> 2."""
+    g = G(5, [0, 0, 1, 1, 2, 2, 3], [1, 2, 2, 3, 3, 4, 4], np.zeros(7, dtype=np.int32))
+    d = oracle.bf(g, 0)
+    assert d.tolist() == [0, 0, 0, 0, 0]
+    assert oracle.pred(g, 0, d).tolist() == [-1, 0, 0, 1, 2]
+    # mixed: 0->1 (2), 0->2 (1), 2->1 (1), 1->3 (0), 2->3 (1): d = [0, 2, 1, 2].
+    # v = 1 has two steep tight tails (0, 2) -> the smaller, 0; v = 3 has a
+    # flat tight tail 1 (d1 = d3) and a steep one 2 -> the steep rule wins, 2
+    g2 = G(4, [0, 0, 2, 1, 2], [1, 2, 1, 3, 3], np.array([2, 1, 1, 0, 1], dtype=np.int32))
+    d2 = oracle.bf(g2, 0)
+    assert d2.tolist() == [0, 2, 1, 2]
+    assert oracle.pred(g2, 0, d2).tolist() == [-1, 0, 0, 2]
+
+
 def test_certificate_accepts_oracle_and_rejects_corruption():
     g = gen.aisle(4, 10, 4, wtype="f32", jitter_seed=9)
     srcs = np.array([0, 5, 17, 39, 56], dtype=np.int32)
