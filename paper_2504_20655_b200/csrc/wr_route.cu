@@ -1478,8 +1478,9 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
     // 1. forward: F(S, j) = min over i in S - j of fl(F(S - j, i) + D[i][j])
     for (int k = 2; k <= n; ++k) {
         const int base = off[k], items = (off[k + 1] - base) * k;
+        const float rk = 1.0f / (float)k;
         for (int x = lane; x < items; x += 32) {
-            const int sidx = x / k, b = x - sidx * k;
+            const int sidx = (int)(((float)x + 0.5f) * rk), b = x - sidx * k;   // x < 2^10: exact
             const uint32_t S = sets[base + sidx];
             const int j = __fns(S, 0, b + 1);
             const uint32_t P = S & ~(1u << j);
@@ -1519,8 +1520,9 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
     __syncwarp();
     for (int k = n - 1; k >= 1; --k) {
         const int base = off[k], items = (off[k + 1] - base) * k;
+        const float rk = 1.0f / (float)k;
         for (int x = lane; x < items; x += 32) {
-            const int sidx = x / k, b = x - sidx * k;
+            const int sidx = (int)(((float)x + 0.5f) * rk), b = x - sidx * k;   // x < 2^10: exact
             const uint32_t S = sets[base + sidx];
             const int j = __fns(S, 0, b + 1);
             uint32_t best = H::NONE;
