@@ -1471,6 +1471,15 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
         Dout[lane] = D[nib(R.gmap, lane) * MS + R.dep];
     }
     __syncwarp();
+    // int32 fast path (as route_hk_kernel): every leg finite and |leg| < 2^23,
+    // so F and M stay within +-2^29 and the INF / NONE tests can go
+    bool slow = false;
+    if (std::is_same<C, CostI32>::value) {
+        const auto bad = [](uint32_t v) { return v == C::INF || (int)v >= (1 << 23) || (int)v <= -(1 << 23); };
+        for (int e = lane; e < 64; e += 32) slow |= ((e >> 3) < n && (e & 7) < n) && bad(Ds[e]);
+        if (closed && lane < n) slow |= bad(Din[lane]) || bad(Dout[lane]);
+    }
+    const bool fast = std::is_same<C, CostI32>::value && !__any_sync(0xffffffffu, slow);
     const uint16_t *sets = L.sets;
     const int *off = L.off[n - LIST_MIN];
     if (lane < n) W[(1u << lane) * SHK_RS + lane] = closed ? Din[lane] : 0u;
@@ -1484,6 +1493,15 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
             const uint32_t S = sets[base + sidx];
             const int j = __fns(S, 0, b + 1);
             const uint32_t P = S & ~(1u << j);
+            if (fast) {
+                int bi = 0x7fffffff;
+                for (uint32_t q = P; q; q &= q - 1) {
+                    const int a = __ffs(q) - 1;
+                    bi = min(bi, (int)W[P * SHK_RS + a] + (int)Ds[a * 8 + j]);
+                }
+                W[S * SHK_RS + j] = (uint32_t)bi;
+                continue;
+            }
             uint32_t best = 0xffffffffu;
             for (uint32_t q = P; q; q &= q - 1) {
                 const int a = __ffs(q) - 1;
@@ -1525,6 +1543,16 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
             const int sidx = (int)(((float)x + 0.5f) * rk), b = x - sidx * k;   // x < 2^10: exact
             const uint32_t S = sets[base + sidx];
             const int j = __fns(S, 0, b + 1);
+            if (fast) {   // NONE -> -2^30: its c stays below -2^29, every real c above
+                int bi = -(1 << 30) - (1 << 24);
+                for (uint32_t q = F & ~S; q; q &= q - 1) {
+                    const int a = __ffs(q) - 1;
+                    const uint32_t mv = W[(S | (1u << a)) * SHK_RS + a];
+                    bi = max(bi, (mv == H::NONE ? -(1 << 30) : (int)mv) - (int)Ds[j * 8 + a]);
+                }
+                W[S * SHK_RS + j] = bi < -(1 << 29) ? H::NONE : (uint32_t)bi;
+                continue;
+            }
             uint32_t best = H::NONE;
             for (uint32_t q = F & ~S; q; q &= q - 1) {
                 const int a = __ffs(q) - 1;

@@ -417,7 +417,7 @@ def test_route_orders_held_karp_int_paths(case):
           "inf_legs": dict(wmax=1000, src_only=3, sink_only=7)}[case]
     g = _hk_digraph(95, **kw)
     rng = np.random.default_rng(96)
-    sizes = [13, 14, 15, 16] * 3
+    sizes = [13, 14, 15, 16, 8, 8] * 3   # 8 stops: the warp Held-Karp (same fast / general paths)
     seqs = []
     for k in sizes:
         pick = rng.choice(g.V, k, replace=False)
@@ -434,7 +434,7 @@ def test_route_orders_held_karp_int_paths(case):
     orders = O()
     orders.order_ptr, orders.order_nodes, orders.B = ptr, nodes, len(seqs)
     res, _ = compare_orders(g, orders, m=1)
-    assert (res["n"] >= 13).all()
+    assert (res["n"] >= 8).all()
 
 
 @pytest.mark.parametrize("wtype", ["i32", "f32"])
