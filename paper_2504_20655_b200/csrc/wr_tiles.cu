@@ -144,16 +144,21 @@ constexpr int RCB_NT = 1024;
 constexpr uint32_t RCB_FULL = 0xffffffffu;
 constexpr int RCB_BINS = 4096;   // 12-bit digits
 
-__global__ void rcb_coords_kernel(const int *sources, int64_t lo, int n, const int *xy, const int *z, int *cx,
-                                  int *cy, int *cz, int *idx) {
+// the sources' coordinates with their index, one 16-B element each, so every
+// pass over a node is a coalesced read and the partition moves whole elements
+__global__ void rcb_coords_kernel(const int *sources, int64_t lo, int n, const int *xy, const int *z, int4 *pts) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = sources[lo + i];
-    cx[i] = xy[2 * v];
-    cy[i] = xy[2 * v + 1];
-    cz[i] = z ? z[v] : 0;
-    idx[i] = i;
+    pts[i] = make_int4(xy[2 * v], xy[2 * v + 1], z ? z[v] : 0, i);
 }
+
+__global__ void rcb_perm_kernel(const int4 *pts, int n, int *perm) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) perm[i] = pts[i].w;
+}
+
+__device__ __forceinline__ int rcb_comp(const int4 &p, int axis) { return axis == 0 ? p.x : axis == 1 ? p.y : p.z; }
 
 // exclusive block scan of one int per thread (RCB_NT threads); returns the total
 __device__ int rcb_scan(int x, int &excl, int *sh) {
@@ -185,21 +190,20 @@ __device__ int rcb_scan(int x, int &excl, int *sh) {
 
 // node = {start, count, nl}: the first nl positions of the node's range end
 // up holding sources whose split key is <= every key on the right
-__global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, int *idx, int *tmp,
-                                                           const int *__restrict__ cx, const int *__restrict__ cy,
-                                                           const int *__restrict__ cz) {
+__global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, int4 *pts, int4 *tmp) {
     __shared__ int hist[RCB_BINS];
     __shared__ int sh[40];
     __shared__ int s_red[6][32];
+    __shared__ int s_wlt[RCB_NT / 32], s_weq[RCB_NT / 32];
     const int4 nd = nodes[blockIdx.x];
     const int s = nd.x, n = nd.y, nl = nd.z;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int *id = idx + s;
+    int4 *pt = pts + s;
     // ---- bounding box
     int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
     for (int i = threadIdx.x; i < n; i += RCB_NT) {
-        const int j = id[i];
-        const int c[3] = {cx[j], cy[j], cz[j]};
+        const int4 p = pt[i];
+        const int c[3] = {p.x, p.y, p.z};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             mn[a] = min(mn[a], c[a]);
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
         }
     }
     __syncthreads();
-    const int *key = sh[34] == 0 ? cx : sh[34] == 1 ? cy : cz;
+    const int axis = sh[34];
     const int klo = sh[35];
     const uint32_t range = (uint32_t)sh[36];
     // ---- radix select: P = the key of rank nl (0-based) in the node
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
         for (int b = threadIdx.x; b < RCB_BINS; b += RCB_NT) hist[b] = 0;
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += RCB_NT) {
-            const uint32_t k = ((uint32_t)key[id[i]] - (uint32_t)klo);
+            const uint32_t k = (uint32_t)rcb_comp(pt[i], axis) - (uint32_t)klo;
             if (hi >= 32 || (k >> hi) == (prefix >> hi)) atomicAdd(&hist[(k >> shift) & dmask], 1);
         }
         __syncthreads();
@@ -268,34 +272,60 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
         hi = shift;
     }
     const uint32_t P = prefix;
-    // ---- stable partition: keys < P, then (nl - #less) keys == P, left
-    const int chunk = (n + RCB_NT - 1) / RCB_NT;
-    const int c0 = min(n, threadIdx.x * chunk), c1 = min(n, c0 + chunk);
+    // ---- stable partition: keys < P, then (nl - #less) keys == P, left. Each
+    // warp owns a contiguous chunk read 32 elements at a time (coalesced);
+    // ballots rank the elements inside a group, a block scan the warps
+    constexpr int NWP = RCB_NT / 32;
+    const int wchunk = ((n + NWP - 1) / NWP + 31) & ~31;
+    const int w0 = min(n, warp * wchunk), w1 = min(n, w0 + wchunk);
+    const unsigned below = (1u << lane) - 1u;
     int lt = 0, eq = 0;
-    for (int i = c0; i < c1; ++i) {
-        const uint32_t k = ((uint32_t)key[id[i]] - (uint32_t)klo);
-        lt += k < P;
-        eq += k == P;
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+        const int i = i0 + lane;
+        const uint32_t k = i < w1 ? (uint32_t)rcb_comp(pt[i], axis) - (uint32_t)klo : 0xffffffffu;
+        lt += __popc(__ballot_sync(RCB_FULL, i < w1 && k < P));
+        eq += __popc(__ballot_sync(RCB_FULL, i < w1 && k == P));
     }
-    int lt0 = 0, eq0 = 0;
-    const int nlt = rcb_scan(lt, lt0, sh);
-    rcb_scan(eq, eq0, sh);
+    if (lane == 0) { s_wlt[warp] = lt; s_weq[warp] = eq; }
+    __syncthreads();
+    int lt0 = 0, eq0 = 0, nlt = 0;
+    for (int q = 0; q < NWP; ++q) {   // warps before this one, and the totals
+        if (q < warp) { lt0 += s_wlt[q]; eq0 += s_weq[q]; }
+        nlt += s_wlt[q];
+    }
     const int quota = nl - nlt;
-    int rt0 = (c0 - lt0 - eq0) + max(0, eq0 - quota);   // right-side elements before this chunk
-    for (int i = c0; i < c1; ++i) {
-        const int j = id[i];
-        const uint32_t k = ((uint32_t)key[j] - (uint32_t)klo);
-        int pos;
-        if (k < P) pos = lt0++;
-        else if (k == P && eq0 < quota) pos = nlt + eq0++;
-        else {
-            if (k == P) ++eq0;
-            pos = nl + rt0++;
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+        const int i = i0 + lane;
+        const bool ok = i < w1;
+        int4 p = make_int4(0, 0, 0, 0);
+        uint32_t k = 0xffffffffu;
+        if (ok) {
+            p = pt[i];
+            k = (uint32_t)rcb_comp(p, axis) - (uint32_t)klo;
         }
-        tmp[s + pos] = j;
+        const unsigned mlt = __ballot_sync(RCB_FULL, ok && k < P);
+        const unsigned meq = __ballot_sync(RCB_FULL, ok && k == P);
+        const int eq_rank = eq0 + __popc(meq & below);   // rank among the node's P keys
+        const bool eq_left = (meq >> lane) & 1u && eq_rank < quota;
+        if (ok) {
+            int pos;
+            if ((mlt >> lane) & 1u) {
+                pos = lt0 + __popc(mlt & below);
+            } else if (eq_left) {
+                pos = nlt + eq_rank;
+            } else {
+                // right side: every element before this one (node order) that is
+                // not left - (i - lefts before i)
+                const int left_before = lt0 + __popc(mlt & below) + min(eq0 + __popc(meq & below), quota);
+                pos = nl + (i - left_before);
+            }
+            tmp[s + pos] = p;
+        }
+        lt0 += __popc(mlt);
+        eq0 += __popc(meq);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += RCB_NT) id[i] = tmp[s + i];
+    for (int i = threadIdx.x; i < n; i += RCB_NT) pt[i] = tmp[s + i];
 }
 
 // the tree's levels: count of internal nodes per depth (host) ...
@@ -339,19 +369,22 @@ static void rcb_perm(const wr_graph *g, const int *d_sources, int64_t lo, int n,
         lv.off[L] = total;
         total += cnt[L];
     }
-    DBuf<int> cx(n), cy(n), cz(n), tmp(n);
+    DBuf<int4> pts(n), tmp(n);
     DBuf<int4> nodes(std::max(total, 1));
     rcb_nodes_kernel<<<1, 1, 0, st>>>(n, tsw, lv, nodes.p);
     count_launch();
     WR_LAUNCH_CHECK();
-    rcb_coords_kernel<<<(n + 255) / 256, 256, 0, st>>>(d_sources, lo, n, g->xy.p, g->z.p, cx.p, cy.p, cz.p, d_perm);
+    rcb_coords_kernel<<<(n + 255) / 256, 256, 0, st>>>(d_sources, lo, n, g->xy.p, g->z.p, pts.p);
     count_launch();
     WR_LAUNCH_CHECK();
     for (size_t L = 0; L < cnt.size(); ++L) {
-        rcb_level_kernel<<<cnt[L], RCB_NT, 0, st>>>(nodes.p + lv.off[L], d_perm, tmp.p, cx.p, cy.p, cz.p);
+        rcb_level_kernel<<<cnt[L], RCB_NT, 0, st>>>(nodes.p + lv.off[L], pts.p, tmp.p);
         count_launch();
         WR_LAUNCH_CHECK();
     }
+    rcb_perm_kernel<<<(n + 255) / 256, 256, 0, st>>>(pts.p, n, d_perm);
+    count_launch();
+    WR_LAUNCH_CHECK();
 }
 
 // Tile count: by default ceil(n / tsw) full tiles. WR_TILE_BALANCE=1 spreads
