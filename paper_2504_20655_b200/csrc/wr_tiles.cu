@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
     int4 *pt = pts + s;
     // ---- bounding box
     int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+#pragma unroll 4
     for (int i = threadIdx.x; i < n; i += RCB_NT) {
         const int4 p = pt[i];
         const int c[3] = {p.x, p.y, p.z};
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
         const uint32_t dmask = (1u << (hi - shift)) - 1u;
         for (int b = threadIdx.x; b < RCB_BINS; b += RCB_NT) hist[b] = 0;
         __syncthreads();
+#pragma unroll 4
         for (int i = threadIdx.x; i < n; i += RCB_NT) {
             const uint32_t k = (uint32_t)rcb_comp(pt[i], axis) - (uint32_t)klo;
             if (hi >= 32 || (k >> hi) == (prefix >> hi)) atomicAdd(&hist[(k >> shift) & dmask], 1);
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
     const int w0 = min(n, warp * wchunk), w1 = min(n, w0 + wchunk);
     const unsigned below = (1u << lane) - 1u;
     int lt = 0, eq = 0;
+#pragma unroll 4
     for (int i0 = w0; i0 < w1; i0 += 32) {
         const int i = i0 + lane;
         const uint32_t k = i < w1 ? (uint32_t)rcb_comp(pt[i], axis) - (uint32_t)klo : 0xffffffffu;
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(RCB_NT) rcb_level_kernel(const int4 *nodes, in
         eq0 += __popc(meq);
     }
     __syncthreads();
+#pragma unroll 4
     for (int i = threadIdx.x; i < n; i += RCB_NT) pt[i] = tmp[s + i];
 }
 
