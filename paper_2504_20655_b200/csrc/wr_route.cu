@@ -819,9 +819,13 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
                                       const RouteProblem *probs, const uint32_t *Dall, const int *stops,
                                       int64_t o_lo, wr_route_result *out, unsigned long long *counters, int pairs) {
     __shared__ uint32_t sD[4][DSTRIDE];
+    __shared__ unsigned long long s_perms;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t t = (int64_t)blockIdx.x * 4 + warp;
-    if (t >= nord) return;
+    if (threadIdx.x == 0) s_perms = 0;
+    __syncthreads();
+    do {   // one exit: the block adds its routes-covered count with one atomic
+    if (t >= nord) break;
     const OrderRoute R = ordr[t];
     const int n = R.ng;   // stops routed (closed tours: without a depot that has no line)
     const int *s = stops + (o_lo + t) * MS;
@@ -834,15 +838,17 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
     for (int k = 0; k < MS; ++k) res.seq[k] = -1;
     if (R.status != WR_OK) {
         if (lane == 0) out[t] = res;
-        return;
+        break;
     }
-    if (pairs && R.mseg >= 2) return;   // route_pairs_kernel writes these orders
-    if (R.hk) return;                   // route_hk_kernel / route_hk_small_kernel write these orders
+    if (pairs && R.mseg >= 2) break;   // route_pairs_kernel writes these orders
+    if (R.hk) break;                   // route_hk_kernel / route_hk_small_kernel write these orders
     const int dep = R.dep;              // closed tour (NEXT-4): the depot's stop index, else -1
     const uint32_t *D = Dall + (size_t)t * DSTRIDE;
     uint32_t *Ds = sD[warp];
-    for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
-    __syncwarp();
+    if (R.mseg >= 2 || (n < 2 && dep >= 0)) {   // only the stitch and an out-and-back read D here
+        for (int e = lane; e < DSTRIDE; e += 32) Ds[e] = D[e];
+        __syncwarp();
+    }
     uint64_t final_seq = 0;
     uint32_t final_cost = 0;
     unsigned long long perms = 0;
@@ -933,8 +939,11 @@ __global__ void route_finalize_kernel(int64_t nord, const OrderRoute *ordr, cons
         res.cost_bits = (n >= 2 || dep >= 0) ? final_cost : 0u;
         for (int a = 0; a < n; ++a) res.seq[a] = s[nib(final_seq, a)];
         out[t] = res;
-        atomicAdd(&counters[0], perms);
+        atomicAdd(&s_perms, perms);
     }
+    } while (false);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_perms) atomicAdd(&counters[0], s_perms);
 }
 
 // NEXT-1 boundary-pair stitch (WR_ROUTE_PAIRS; oracle:
@@ -1451,9 +1460,13 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
                           HkLists L) {
     using H = HkOps<C>;
     extern __shared__ uint32_t shk[];
+    __shared__ unsigned long long s_routes;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int i = blockIdx.x * SHK_WARPS + warp;
-    if (i >= nlist) return;
+    if (threadIdx.x == 0) s_routes = 0;
+    __syncthreads();
+    do {   // one exit: the block adds its routes-covered count with one atomic
+    if (i >= nlist) break;
     uint32_t *W = shk + (size_t)warp * ((1u << SHK_MAX) * SHK_RS + 64 + 16);
     uint32_t *Ds = W + (1u << SHK_MAX) * SHK_RS;   // [a * 8 + b]
     uint32_t *Din = Ds + 64, *Dout = Din + 8;
@@ -1530,7 +1543,7 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
             for (int a = 0; a < MS; ++a) res.seq[a] = a < n ? s[nib(R.gmap, a)] : -1;
             out[t] = res;
         }
-        return;
+        break;
     }
     // 2. backward bound M(S, j), written over F layer by layer
     __syncwarp();
@@ -1603,8 +1616,11 @@ __global__ void __launch_bounds__(SHK_WARPS * 32)
         res.rank = rank;
         for (int a = 0; a < MS; ++a) res.seq[a] = (ok && a < n) ? s[nib(R.gmap, seq[a])] : -1;
         out[t] = res;
-        atomicAdd(&counters[0], (unsigned long long)fact(n));   // routes covered, as enumeration counts them
+        atomicAdd(&s_routes, (unsigned long long)fact(n));   // routes covered, as enumeration counts them
     }
+    } while (false);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_routes) atomicAdd(&counters[0], s_routes);
 }
 
 // The popcount-sorted subset lists for n = 7..16 (host-built once per
