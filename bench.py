@@ -286,7 +286,10 @@ def main():
     if not a.no_e2e:
         h_ptr = torch.from_numpy(orders.order_ptr).pin_memory()
         h_nodes = torch.from_numpy(orders.order_nodes).pin_memory()
-        h_res = np.zeros(max(B, 1), dtype=wr.RESULT_DTYPE)
+        # results land in pinned host memory too (a pageable buffer would make
+        # the device-to-host copy a staged, synchronous one)
+        h_res_t = torch.empty(max(B, 1) * wr.RESULT_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+        h_res = h_res_t.numpy().view(wr.RESULT_DTYPE)
 
         def e2e_step():
             wr.route_orders(G, h_ptr.numpy(), h_nodes.numpy(), m=a.m, results=h_res, stream=stream, flags=rflags,
