@@ -187,10 +187,11 @@ def test_bf_flat_competing_predecessors():
     check_bf(g3, np.arange(5, dtype=np.int32))
 
 
-def test_bf_long_path_stamp_restamp():
-    """A 70,000-vertex path needs ~70k rounds from an end: the sweep's 16-bit
-    change stamps are restamped every 2^15 rounds and wrap at 2^16, and the
-    distances / preds / routes must still equal the oracle's."""
+def test_bf_long_path_many_rounds():
+    """A 70,000-vertex path needs ~70k rounds from an end (more than 2^16):
+    the sweep's round-stamped change words, word lists and the round-V
+    negative-cycle test must still give the oracle's distances, preds and
+    routes."""
     V = 70000
     a = np.arange(V - 1, dtype=np.int32)
     g = G(V, np.concatenate([a, a + 1]), np.concatenate([a + 1, a]), np.ones(2 * (V - 1), np.int32),
