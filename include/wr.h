@@ -281,7 +281,7 @@ typedef struct {
 typedef struct {
     int64_t orders;
     int64_t sources;          /* distinct stop nodes (BF sources)            */
-    int64_t permutations;     /* sequences evaluated, segments + exact       */
+    int64_t permutations;     /* sequences covered, segments + exact: enumerated, or proved no better (branch and bound, 8-stop Held-Karp); 13-16-stop Held-Karp orders add their DP transitions */
     int64_t stitch_candidates;
     int32_t segments;         /* BF source batches                           */
     int32_t rounds_max;

@@ -2,6 +2,8 @@
 by element on the same seeded inputs. Bar (north star): dist and route cost
 bit-exact for int32 AND fp32; pred equal to the canonical predecessor (O3);
 route sequences equal (lexicographic tie rules O5/O7)."""
+import math
+
 import numpy as np
 import pytest
 
@@ -488,7 +490,13 @@ def compare_orders(g, orders, m, chunk=0, G=None, results=None, flags=0):
 @pytest.mark.parametrize("k,B", [(1, None), (2, None), (3, 1024)])
 def test_route_orders_exact(k, B, wtype):
     g, orders, _ = gen.config(k, wtype=wtype, B=B)
-    compare_orders(g, orders, m=1)
+    res, st = compare_orders(g, orders, m=1)
+    # every order of <= 12 stops covers its n! sequences, however it is routed
+    # (enumeration, branch and bound, or the 8-stop warp Held-Karp)
+    ok = res["status"] == 0
+    n = res["n"][ok]
+    if n.size and n.max() <= 12:
+        assert st.permutations == sum(math.factorial(int(x)) for x in n if x >= 2)
 
 
 @pytest.mark.parametrize("wtype", ["i32", "f32"])
